@@ -1,0 +1,146 @@
+/*
+ * mpwsd.h -- C-ABI of the B200-native MP-WSD two-stage decoder
+ * (libmpwsd.so, built for sm_100a).
+ *
+ * This is the drop-in boundary for the reference's decoder API
+ * (feclab.decoders, /root/reference/pkg/src/feclab/decoders.py):
+ *
+ *   mpw_set_code         <- LinearCode tables: inner info set, effective
+ *                           generator, CRC (codebook.py:71-132, 261-279)
+ *   mpw_set_patterns     <- CodeWeightSphere.member_words[1:] (wsphere.py:73-112)
+ *   mpw_scl_batch        <- scl_decode(llrs, code, list_size)   decoders.py:181-268
+ *   mpw_mpwsd_batch      <- mp_wsd(y, init_list, sphere, params) decoders.py:455-514
+ *   mpw_two_stage_batch  <- two_stage_decode(y, code, SclStage(L), params, sphere,
+ *                           sigma)                               decoders.py:520-583
+ *
+ * Conventions
+ *   - Plain pointers and sizes; no framework types.  Buffers of the *_batch
+ *     calls are DEVICE pointers on the handle's device (caller-owned);
+ *     mpw_two_stage_batch_host takes HOST pointers and does the copies.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *   - Packed bit vectors: bit j of a length-n vector is bit (j % 32) of uint32
+ *     word j / 32, nw = max(1, n / 32) words per vector (the reference's uint64
+ *     layout viewed as little-endian uint32, binlin.py:1-8).  Host-side code
+ *     and pattern inputs are in the reference's uint64 layout.
+ *   - Return 0 on success or a negative MPW_ERR_*; mpw_last_error() gives the
+ *     message (thread-local).  No exception crosses the ABI.  Errors mirror the
+ *     reference's ValueErrors (crc_gated without CRC, decoders.py:540-541; bad
+ *     WsdParams, :80-86) plus device limits (MPW_ERR_UNSUPPORTED).
+ *   - A handle is used by one host thread at a time; use one handle per
+ *     device (or per thread).
+ */
+#ifndef MPWSD_H_
+#define MPWSD_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MPW_ABI_VERSION 1
+
+#define MPW_OK 0
+#define MPW_ERR_ARG (-1)
+#define MPW_ERR_STATE (-2)
+#define MPW_ERR_UNSUPPORTED (-3)
+#define MPW_ERR_CUDA (-4)
+#define MPW_ERR_NO_DEVICE (-5)
+
+/* activation_mode (decoders.py:78, 539) */
+#define MPW_MODE_CRC_GATED 0
+#define MPW_MODE_ALWAYS_ON 1
+
+/* hop kernel selection */
+#define MPW_HOP_AUTO 0
+#define MPW_HOP_GATHER 1  /* shared-memory gather-sum on CUDA cores */
+#define MPW_HOP_TENSOR 2  /* tcgen05 f16 contraction with TMEM argmin epilogue */
+
+/* counters (int64, accumulated by mpw_two_stage_batch; caller zeroes) */
+#define MPW_CTR_FRAMES 0
+#define MPW_CTR_ERRORS 1      /* decoded codeword != tx codeword (simharness.py:311) */
+#define MPW_CTR_ACTIVATIONS 2 /* stage == mp_wsd (simharness.py:309) */
+#define MPW_CTR_ITERATIONS 3  /* sum of iterations_used over trajectories */
+#define MPW_CTR_EVALS 4       /* pattern-metric evaluations = |P| * iterations */
+#define MPW_CTR_NEAR_TIE 5    /* frames carrying a near-tie flag */
+#define MPW_NUM_COUNTERS 8
+
+/* per-frame flags */
+#define MPW_FLAG_TIE_ARGMIN 1 /* top-2 hop candidates within 1e-5 relative */
+#define MPW_FLAG_TIE_ACCEPT 2 /* best hop's ED change within 1e-5 relative of 0 */
+#define MPW_FLAG_TIE_FINAL 4  /* two distinct final centres within 1e-5 relative */
+
+typedef struct mpw_handle mpw_handle;
+
+int mpw_version(void);
+const char* mpw_last_error(void);
+
+int mpw_create(int device, mpw_handle** out);
+void mpw_destroy(mpw_handle* h);
+
+/* Code tables.  info_set: kp ascending positions of the inner polar code;
+ * gen_words: k x ceil(n/64) uint64 rows of the effective generator (the CA
+ * generator for CRC-concatenated codes); crc_poly bit i = coefficient of x^i
+ * (including x^crc_deg).  is_ca = 0 for a plain polar code (no gate, anchors
+ * are the list codewords as-is, decoders.py:574-575). */
+int mpw_set_code(mpw_handle* h, int n, int k, int kp, const int32_t* info_set,
+                 const uint64_t* gen_words, int is_ca, int crc_deg, uint32_t crc_poly);
+
+/* Pattern set P: np x ceil(n/64) uint64 words, the nonzero sphere members in
+ * member order (pattern index = member index - 1). */
+int mpw_set_patterns(mpw_handle* h, const uint64_t* pattern_words, int np);
+
+/* Stage 1 alone.  Either y (F x n float32 received words; LLRs are 2y/sigma^2
+ * in float64, decoders.py:550) or llr (F x n float64 LLRs, the scl_decode
+ * argument) is given.  Outputs (any may be NULL): list_n[F];
+ * list_u/list_cw: F x L x nw; list_pm: F x L float64, list in ascending PM. */
+int mpw_scl_batch(mpw_handle* h, const float* y, const double* llr, int F, double sigma, int L,
+                  int32_t* list_n, uint32_t* list_u, uint32_t* list_cw, double* list_pm,
+                  void* stream);
+
+/* Stage 2 alone from given anchors (F x A x nw); n_anchor[F] may be NULL (= A).
+ * Outputs: best F x nw, best_ed F (float64 canonical), iters F x A,
+ * hops F x A x T (accepted member index per hop, -1 = none; may be NULL),
+ * flags F (may be NULL). */
+int mpw_mpwsd_batch(mpw_handle* h, const float* y, const uint32_t* anchors, const int32_t* n_anchor,
+                    int F, int A, int T, int variant, uint32_t* best, double* best_ed,
+                    int32_t* iters, int32_t* hops, uint8_t* flags, void* stream);
+
+/* The full two-stage path.  stage[F]: 0 = stage1_crc_pass, 1 = mp_wsd.
+ * tx_cw (F x nw, may be NULL) enables the error counter.  best_msg[F]
+ * (k <= 64 bits, may be NULL) = code.message_of(best).  anchors_out
+ * (F x A x nw, may be NULL) returns the projected anchors. */
+int mpw_two_stage_batch(mpw_handle* h, const float* y, int F, double sigma, int L, int A, int T,
+                        int mode, int variant, const uint32_t* tx_cw, uint32_t* best,
+                        uint64_t* best_msg, double* best_ed, uint8_t* stage, int32_t* iters,
+                        int32_t* hops, uint32_t* anchors_out, uint8_t* flags,
+                        unsigned long long* counters, void* stream);
+
+/* Same with HOST buffers; H2D/D2H copies are made on `stream` and the call
+ * returns after the results are on the host. */
+int mpw_two_stage_batch_host(mpw_handle* h, const float* y_host, int F, double sigma, int L, int A,
+                             int T, int mode, int variant, const uint32_t* tx_host,
+                             uint32_t* best_host, uint64_t* msg_host, double* ed_host,
+                             uint8_t* stage_host, int32_t* iters_host, uint8_t* flags_host,
+                             unsigned long long* counters_host, void* stream);
+
+/* Per-kernel CUDA-event timing of mpw_two_stage_batch: ms_out[4] =
+ * {stage 1, stage 2 hops, finalize, frame epilogue}. */
+int mpw_set_timing(mpw_handle* h, int enable);
+int mpw_read_timing(mpw_handle* h, double* ms_out, long long* launches_out, int reset);
+
+int mpw_num_patterns(mpw_handle* h);
+int mpw_tensor_path_ready(mpw_handle* h);
+
+/* Host-side pattern-set generation (off the timed path). */
+int64_t mpw_enumerate_lowweight(const uint64_t* gen, int k, int n, int cap, int64_t* spectrum,
+                                uint64_t* out, int64_t out_cap, int nthreads);
+int64_t mpw_collect_lowweight(const uint64_t* gen, int k, int n, int cap, int64_t iterations,
+                              uint64_t seed, int p_max, uint64_t* out, int64_t out_cap,
+                              int nthreads);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MPWSD_H_ */

@@ -1,0 +1,670 @@
+// libmpwsd: B200-native MP-WSD two-stage decoding, C-ABI (include/mpwsd.h).
+//
+// Pipeline of one batch (all on the caller's stream, no host sync):
+//   scl_kernel       stage 1 + CRC gate + projection + stage-2 compaction
+//   hop_*_kernel     stage 2 hops over the compacted trajectories
+//   finalize_kernel  canonical float64 EDs, min over anchors, near-tie flags
+//   frame_kernel     message_of, per-frame outputs, counters
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/mpwsd.h"
+#include "common.cuh"
+#include "hop_gather.cuh"
+#include "hop_tc.cuh"
+#include "scl.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return code;
+}
+
+#define CK(expr)                                                                     \
+    do {                                                                             \
+        cudaError_t e_ = (expr);                                                     \
+        if (e_ != cudaSuccess)                                                       \
+            return fail(MPW_ERR_CUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), \
+                        __FILE__, __LINE__);                                         \
+    } while (0)
+
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t count) {
+        if (count <= cap && p) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        cudaError_t e = cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T));
+        if (e == cudaSuccess) cap = std::max<size_t>(count, 1);
+        return e;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+}  // namespace
+
+struct mpw_handle {
+    int device = 0;
+    int num_sms = 148;
+    // code
+    bool has_code = false;
+    int n = 0, m = 0, nw = 0, k = 0, kp = 0, is_ca = 0, crc_deg = 0;
+    DevBuf<int32_t> info, pivots;
+    DevBuf<uint32_t> frozen, gen;
+    DevBuf<uint64_t> crc_h, mix;
+    // patterns
+    bool has_pat = false;
+    int np = 0;
+    int total_sup_u4 = 0;
+    DevBuf<uint32_t> pbits;
+    DevBuf<int32_t> poff, soff;
+    DevBuf<uint16_t> pidx;
+    DevBuf<uint4> sup;
+    TcPatterns tcp;                 // tensor-core operand of P (hop_tc.cuh)
+    // stage-2 scratch
+    DevBuf<int32_t> s2_count, s2_frame, s2_nanchor, traj_iters, traj_hops, work_next;
+    DevBuf<uint32_t> s2_anchors, traj_cw;
+    DevBuf<uint8_t> traj_flags;
+    // timing
+    int timing = 0;
+    cudaEvent_t ev[8];
+    bool ev_init = false;
+    double acc_ms[4] = {0, 0, 0, 0};
+    long long launches[4] = {0, 0, 0, 0};
+    long long evals = 0;
+};
+
+namespace {
+
+CodeDev code_dev(const mpw_handle* h) {
+    CodeDev c;
+    c.n = h->n; c.m = h->m; c.nw = h->nw; c.k = h->k; c.kp = h->kp;
+    c.is_ca = h->is_ca; c.crc_deg = h->crc_deg;
+    c.info = h->info.p; c.frozen = h->frozen.p; c.gen = h->gen.p; c.crc_h = h->crc_h.p;
+    c.pivots = h->pivots.p; c.mix = h->mix.p;
+    return c;
+}
+
+PatDev pat_dev(const mpw_handle* h) {
+    PatDev p;
+    p.np = h->np; p.nw = h->nw; p.bits = h->pbits.p; p.off = h->poff.p; p.idx = h->pidx.p;
+    return p;
+}
+
+int set_device(mpw_handle* h) {
+    CK(cudaSetDevice(h->device));
+    return 0;
+}
+
+// ---------------------------------------------------------------------------
+// finalize: canonical float64 EDs of the final centres, min over anchors with
+// ties to the lowest anchor (decoders.py:505), near-tie flag for distinct
+// codewords whose EDs differ by < tie_rel (relative).
+struct FinalOut {
+    uint32_t* best; double* best_ed; uint8_t* stage; int32_t* iters; int32_t* hops;
+    uint32_t* anchors; uint8_t* flags; int32_t* best_k;
+};
+
+__global__ void finalize_kernel(int n, int nw, int A, int T, const float* __restrict__ y, S2Dev s2,
+                                FinalOut out, float tie_rel) {
+    const int lane = threadIdx.x & 31;
+    const int warps = gridDim.x * (blockDim.x >> 5);
+    const int count = *s2.count;
+    for (int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); q < count; q += warps) {
+        const int f = s2.frame[q], na = s2.nanchor[q];
+        double best = CUDART_INF, second = CUDART_INF;
+        int bk = 0;
+        uint8_t fl = 0;
+        for (int a = 0; a < na; a++) {
+            const uint32_t* cw = s2.traj_cw + ((size_t)q * A + a) * nw;
+            double acc = 0.0;
+            for (int i = lane; i < n; i += 32) {
+                const double x = ((cw[i >> 5] >> (i & 31)) & 1u) ? -1.0 : 1.0;
+                const double d = (double)y[(size_t)f * n + i] - x;
+                acc += d * d;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(MPW_FULL, acc, o);
+            bool same = true;   // identical codeword to the current best?
+            if (a > 0) {
+                const uint32_t* bc = s2.traj_cw + ((size_t)q * A + bk) * nw;
+                bool diff = false;
+                for (int w = lane; w < nw; w += 32) diff |= cw[w] != bc[w];
+                same = !__any_sync(MPW_FULL, diff);
+            }
+            if (acc < best) {
+                if (a > 0 && !same) second = best;
+                best = acc;
+                bk = a;
+            } else if (!same && acc < second) {
+                second = acc;
+            }
+            fl |= s2.traj_flags[(size_t)q * A + a];
+            if (lane == 0 && out.iters) out.iters[(size_t)f * A + a] = s2.traj_iters[(size_t)q * A + a];
+            if (out.hops)
+                for (int h = lane; h < T; h += 32)
+                    out.hops[((size_t)f * A + a) * T + h] = s2.traj_hops[((size_t)q * A + a) * T + h];
+            if (out.anchors)
+                for (int w = lane; w < nw; w += 32)
+                    out.anchors[((size_t)f * A + a) * nw + w] = s2.anchors[((size_t)q * A + a) * nw + w];
+        }
+        if (second - best < (double)tie_rel * best) fl |= 4;
+        for (int a = na + lane; a < A; a += 32) {
+            if (out.iters) out.iters[(size_t)f * A + a] = 0;
+        }
+        for (int w = lane; w < nw; w += 32) out.best[(size_t)f * nw + w] = s2.traj_cw[((size_t)q * A + bk) * nw + w];
+        if (lane == 0) {
+            out.best_ed[f] = best;
+            if (out.stage) out.stage[f] = 1;
+            if (out.flags) out.flags[f] = fl;
+            if (out.best_k) out.best_k[f] = bk;
+        }
+    }
+}
+
+// per-frame epilogue: message_of (codebook.py:123-132), stage-1 defaults, counters
+struct FrameArgs {
+    int F, A, T, nw, k, np;
+    const uint32_t* best; const uint8_t* stage; const uint32_t* tx;
+    int32_t* iters; int32_t* hops; uint8_t* flags; uint64_t* msg_out;
+    unsigned long long* counters;
+    const int32_t* pivots; const uint64_t* mix;
+};
+
+__global__ void frame_kernel(FrameArgs fa) {
+    const int f = blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long c_err = 0, c_act = 0, c_it = 0, c_tie = 0, c_fr = 0;
+    if (f < fa.F) {
+        const uint32_t* b = fa.best + (size_t)f * fa.nw;
+        if (fa.msg_out && fa.k <= 64) {
+            uint64_t msg = 0;
+            for (int j = 0; j < fa.k; j++) {
+                const int p = fa.pivots[j];
+                if ((b[p >> 5] >> (p & 31)) & 1u) msg ^= fa.mix[j];
+            }
+            fa.msg_out[f] = msg;
+        }
+        const bool s2 = fa.stage[f] == 1;
+        if (!s2) {
+            if (fa.iters) for (int a = 0; a < fa.A; a++) fa.iters[(size_t)f * fa.A + a] = 0;
+            if (fa.hops) for (int a = 0; a < fa.A * fa.T; a++) fa.hops[(size_t)f * fa.A * fa.T + a] = -1;
+            if (fa.flags) fa.flags[f] = 0;
+        } else if (fa.iters) {
+            for (int a = 0; a < fa.A; a++) c_it += (unsigned long long)fa.iters[(size_t)f * fa.A + a];
+        }
+        c_fr = 1;
+        c_act = s2 ? 1 : 0;
+        c_tie = (fa.flags && fa.flags[f]) ? 1 : 0;
+        if (fa.tx) {
+            bool diff = false;
+            for (int w = 0; w < fa.nw; w++) diff |= b[w] != fa.tx[(size_t)f * fa.nw + w];
+            c_err = diff ? 1 : 0;
+        }
+    }
+    if (fa.counters) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            c_fr += __shfl_xor_sync(MPW_FULL, c_fr, o);
+            c_err += __shfl_xor_sync(MPW_FULL, c_err, o);
+            c_act += __shfl_xor_sync(MPW_FULL, c_act, o);
+            c_it += __shfl_xor_sync(MPW_FULL, c_it, o);
+            c_tie += __shfl_xor_sync(MPW_FULL, c_tie, o);
+        }
+        if ((threadIdx.x & 31) == 0 && c_fr) {
+            atomicAdd(&fa.counters[MPW_CTR_FRAMES], c_fr);
+            atomicAdd(&fa.counters[MPW_CTR_ERRORS], c_err);
+            atomicAdd(&fa.counters[MPW_CTR_ACTIVATIONS], c_act);
+            atomicAdd(&fa.counters[MPW_CTR_ITERATIONS], c_it);
+            atomicAdd(&fa.counters[MPW_CTR_EVALS], c_it * (unsigned long long)fa.np);
+            atomicAdd(&fa.counters[MPW_CTR_NEAR_TIE], c_tie);
+        }
+    }
+}
+
+// mp_wsd API: queue = identity over the given frames
+__global__ void queue_identity_kernel(int F, int A, const int32_t* nanchor, S2Dev s2) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q == 0) *s2.count = F;
+    if (q < F) {
+        s2.frame[q] = q;
+        s2.nanchor[q] = nanchor ? min(nanchor[q], A) : A;
+    }
+}
+
+int ensure_s2(mpw_handle* h, int F, int A, int T) {
+    const size_t traj = (size_t)F * A;
+    CK(h->s2_count.ensure(1));
+    CK(h->work_next.ensure(1));
+    CK(h->s2_frame.ensure(F));
+    CK(h->s2_nanchor.ensure(F));
+    CK(h->s2_anchors.ensure(traj * h->nw));
+    CK(h->traj_cw.ensure(traj * h->nw));
+    CK(h->traj_iters.ensure(traj));
+    CK(h->traj_hops.ensure(traj * T));
+    CK(h->traj_flags.ensure(traj));
+    return 0;
+}
+
+S2Dev s2_dev(mpw_handle* h, const uint32_t* anchors_override) {
+    S2Dev s;
+    s.count = h->s2_count.p; s.frame = h->s2_frame.p; s.nanchor = h->s2_nanchor.p;
+    s.anchors = anchors_override ? const_cast<uint32_t*>(anchors_override) : h->s2_anchors.p;
+    s.traj_cw = h->traj_cw.p; s.traj_iters = h->traj_iters.p; s.traj_hops = h->traj_hops.p;
+    s.traj_flags = h->traj_flags.p; s.work_next = h->work_next.p;
+    return s;
+}
+
+void timing_mark(mpw_handle* h, int slot, cudaStream_t st) {
+    if (h->timing) cudaEventRecord(h->ev[slot], st);
+}
+
+int timing_close(mpw_handle* h) {
+    if (!h->timing) return 0;
+    CK(cudaEventSynchronize(h->ev[4]));
+    float ms;
+    for (int i = 0; i < 4; i++) {
+        CK(cudaEventElapsedTime(&ms, h->ev[i], h->ev[i + 1]));
+        h->acc_ms[i] += ms;
+        h->launches[i] += 1;
+    }
+    return 0;
+}
+
+template <int NW>
+int launch_scl(mpw_handle* h, const float* y, const double* llr64, int F, double sigma, int L, int A,
+               int mode, SclOut out, S2Dev s2, cudaStream_t st) {
+    const SclLayout lay = scl_layout(h->n, L, h->nw);
+    int wpb = (int)std::max<size_t>(1, std::min<size_t>(8, (96 * 1024) / lay.total));
+    const size_t smem = lay.total * wpb;
+    if (smem > 227 * 1024) return fail(MPW_ERR_UNSUPPORTED, "SCL shared memory %zu B exceeds the SM (n=%d, L=%d)", smem, h->n, L);
+    CK(cudaFuncSetAttribute(scl_kernel<NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, scl_kernel<NW>, 32 * wpb, smem));
+    per_sm = std::max(per_sm, 1);
+    const long long need = ((long long)F + wpb - 1) / wpb;
+    const int grid = (int)std::max<long long>(1, std::min<long long>(need, (long long)per_sm * h->num_sms * 4));
+    scl_kernel<NW><<<grid, 32 * wpb, smem, st>>>(code_dev(h), y, llr64, F, sigma, L, A, mode, out, s2);
+    CK(cudaGetLastError());
+    return 0;
+}
+
+int dispatch_scl(mpw_handle* h, const float* y, const double* llr64, int F, double sigma, int L, int A,
+                 int mode, SclOut out, S2Dev s2, cudaStream_t st) {
+    switch (h->nw) {
+        case 1: return launch_scl<1>(h, y, llr64, F, sigma, L, A, mode, out, s2, st);
+        case 2: return launch_scl<2>(h, y, llr64, F, sigma, L, A, mode, out, s2, st);
+        case 4: return launch_scl<4>(h, y, llr64, F, sigma, L, A, mode, out, s2, st);
+        case 8: return launch_scl<8>(h, y, llr64, F, sigma, L, A, mode, out, s2, st);
+        case 16: return launch_scl<16>(h, y, llr64, F, sigma, L, A, mode, out, s2, st);
+        case 32: return launch_scl<32>(h, y, llr64, F, sigma, L, A, mode, out, s2, st);
+        default: return fail(MPW_ERR_UNSUPPORTED, "blocklength %d unsupported", h->n);
+    }
+}
+
+template <int NW>
+int launch_gather(mpw_handle* h, HopParams hp, int max_traj, cudaStream_t st) {
+    const size_t sup_bytes = ((sizeof(uint4) * (size_t)h->total_sup_u4 + sizeof(int32_t) * (size_t)(h->np + 1)) + 15) & ~(size_t)15;
+    const size_t wsm = gather_warp_smem(h->n);
+    int wpb = 8;
+    while (wpb > 1 && wsm * wpb > 64 * 1024) wpb /= 2;
+    hp.sup_in_smem = (sup_bytes + wsm * wpb <= 200 * 1024) ? 1 : 0;
+    const size_t smem = (hp.sup_in_smem ? sup_bytes : 0) + wsm * wpb;
+    CK(cudaFuncSetAttribute(hop_gather_kernel<NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hop_gather_kernel<NW>, 32 * wpb, smem));
+    per_sm = std::max(per_sm, 1);
+    const long long tasks = ((long long)max_traj + 31) / 32;
+    const long long need = (tasks + wpb - 1) / wpb;
+    const int grid = (int)std::max<long long>(1, std::min<long long>(need, (long long)per_sm * h->num_sms));
+    hop_gather_kernel<NW><<<grid, 32 * wpb, smem, st>>>(hp);
+    CK(cudaGetLastError());
+    return 0;
+}
+
+int run_hops(mpw_handle* h, const float* y, int Fmax, int A, int T, int variant, S2Dev s2, cudaStream_t st) {
+    if (variant == MPW_HOP_AUTO) variant = tc_supported(h->n, h->np) && h->tcp.ready ? MPW_HOP_TENSOR : MPW_HOP_GATHER;
+    if (variant == MPW_HOP_TENSOR) {
+        if (!h->tcp.ready) return fail(MPW_ERR_UNSUPPORTED, "tensor-core hop operand not built for this pattern set");
+        int rc = tc_launch(h->tcp, h->n, h->nw, A, T, y, s2, pat_dev(h), h->num_sms, st);
+        if (rc) return fail(MPW_ERR_CUDA, "tensor-core hop launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+        return 0;
+    }
+    HopParams hp;
+    hp.n = h->n; hp.nw = h->nw; hp.A = A; hp.T = T; hp.y = y; hp.s2 = s2; hp.P = pat_dev(h);
+    hp.sup = h->sup.p; hp.soff = h->soff.p; hp.sup_in_smem = 0; hp.total_sup_u4 = h->total_sup_u4;
+    hp.tie_rel = 1e-5f;
+    const int max_traj = Fmax * A;
+    switch (h->nw) {
+        case 1: return launch_gather<1>(h, hp, max_traj, st);
+        case 2: return launch_gather<2>(h, hp, max_traj, st);
+        case 4: return launch_gather<4>(h, hp, max_traj, st);
+        case 8: return launch_gather<8>(h, hp, max_traj, st);
+        case 16: return launch_gather<16>(h, hp, max_traj, st);
+        case 32: return launch_gather<32>(h, hp, max_traj, st);
+        default: return fail(MPW_ERR_UNSUPPORTED, "blocklength %d unsupported", h->n);
+    }
+}
+
+int finalize(mpw_handle* h, const float* y, int Fmax, int A, int T, S2Dev s2, FinalOut fo, cudaStream_t st) {
+    const int grid = std::max(1, std::min((Fmax + 7) / 8, h->num_sms * 8));
+    finalize_kernel<<<grid, 256, 0, st>>>(h->n, h->nw, A, T, y, s2, fo, 1e-5f);
+    CK(cudaGetLastError());
+    return 0;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+extern "C" {
+
+const char* mpw_last_error(void) { return g_last_error.c_str(); }
+
+int mpw_version(void) { return MPW_ABI_VERSION; }
+
+int mpw_create(int device, mpw_handle** out) {
+    if (!out) return fail(MPW_ERR_ARG, "null handle pointer");
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0) return fail(MPW_ERR_NO_DEVICE, "no CUDA device available (%s)", cudaGetErrorString(e));
+    if (device < 0 || device >= ndev) return fail(MPW_ERR_ARG, "device %d out of range", device);
+    mpw_handle* h = new mpw_handle();
+    h->device = device;
+    CK(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) {
+        delete h;
+        return fail(MPW_ERR_NO_DEVICE, "device %d is sm_%d%d; this library is built for sm_100a", device, prop.major, prop.minor);
+    }
+    h->num_sms = prop.multiProcessorCount;
+    *out = h;
+    return 0;
+}
+
+void mpw_destroy(mpw_handle* h) {
+    if (!h) return;
+    cudaSetDevice(h->device);
+    h->info.release(); h->pivots.release(); h->frozen.release(); h->gen.release();
+    h->crc_h.release(); h->mix.release(); h->pbits.release(); h->poff.release(); h->soff.release();
+    h->pidx.release(); h->sup.release(); h->s2_count.release(); h->s2_frame.release();
+    h->s2_nanchor.release(); h->traj_iters.release(); h->traj_hops.release(); h->work_next.release();
+    h->s2_anchors.release(); h->traj_cw.release(); h->traj_flags.release();
+    tc_release(h->tcp);
+    if (h->ev_init) for (int i = 0; i < 8; i++) cudaEventDestroy(h->ev[i]);
+    delete h;
+}
+
+int mpw_set_code(mpw_handle* h, int n, int k, int kp, const int32_t* info_set, const uint64_t* gen_words,
+                 int is_ca, int crc_deg, uint32_t crc_poly) {
+    if (!h || !info_set || !gen_words) return fail(MPW_ERR_ARG, "null argument");
+    if (n < 2 || (n & (n - 1)) || n > 1024) return fail(MPW_ERR_ARG, "n=%d must be a power of two in [2,1024]", n);
+    if (k < 1 || kp < k || kp > n) return fail(MPW_ERR_ARG, "bad dimensions k=%d kp=%d", k, kp);
+    if (k > 64) return fail(MPW_ERR_UNSUPPORTED, "k=%d > 64 is not supported on the device path", k);
+    if (is_ca && (crc_deg < 1 || crc_deg > 32 || kp != k + crc_deg || kp > 64))
+        return fail(MPW_ERR_ARG, "bad CRC parameters (deg=%d, k=%d, kp=%d)", crc_deg, k, kp);
+    for (int i = 0; i < kp; i++)
+        if (info_set[i] < 0 || info_set[i] >= n || (i && info_set[i] <= info_set[i - 1]))
+            return fail(MPW_ERR_ARG, "info set must be ascending in [0,n)");
+    if (set_device(h)) return MPW_ERR_CUDA;
+    const int w64 = (n + 63) / 64, nw = std::max(1, n / 32);
+    h->n = n; h->m = __builtin_ctz(n); h->nw = nw; h->k = k; h->kp = kp; h->is_ca = is_ca; h->crc_deg = crc_deg;
+    // frozen mask
+    std::vector<uint32_t> frozen(nw, 0);
+    for (int i = 0; i < n; i++) frozen[i >> 5] |= 1u << (i & 31);
+    for (int i = 0; i < kp; i++) frozen[info_set[i] >> 5] &= ~(1u << (info_set[i] & 31));
+    // generator as uint32 words
+    std::vector<uint32_t> gen((size_t)k * nw, 0);
+    for (int r = 0; r < k; r++)
+        for (int j = 0; j < n; j++)
+            if ((gen_words[(size_t)r * w64 + (j >> 6)] >> (j & 63)) & 1ull) gen[(size_t)r * nw + (j >> 5)] |= 1u << (j & 31);
+    // CRC syndrome masks: v read MSB-first, remainder bit j = parity(v & H[j])
+    std::vector<uint64_t> crc_h(std::max(crc_deg, 1), 0);
+    if (is_ca) {
+        for (int i = 0; i < kp; i++) {
+            // r_i = x^(kp-1-i) mod g(x)
+            uint64_t r = 1;  // polynomial, bit t = coeff x^t
+            for (int e = 0; e < kp - 1 - i; e++) {
+                r <<= 1;
+                if ((r >> crc_deg) & 1ull) r ^= (uint64_t)crc_poly;
+            }
+            for (int j = 0; j < crc_deg; j++)
+                if ((r >> j) & 1ull) crc_h[j] |= 1ull << i;
+        }
+    }
+    // message_of tables: reduce [G | I] (codebook.py:104-117)
+    const int W = n + k;
+    std::vector<std::vector<uint8_t>> aug(k, std::vector<uint8_t>(W, 0));
+    for (int r = 0; r < k; r++) {
+        for (int j = 0; j < n; j++) aug[r][j] = (uint8_t)((gen_words[(size_t)r * w64 + (j >> 6)] >> (j & 63)) & 1ull);
+        aug[r][n + r] = 1;
+    }
+    std::vector<int32_t> piv;
+    int rank = 0;
+    for (int col = 0; col < n && rank < k; col++) {
+        int p = -1;
+        for (int r = rank; r < k; r++) if (aug[r][col]) { p = r; break; }
+        if (p < 0) continue;
+        std::swap(aug[p], aug[rank]);
+        for (int r = 0; r < k; r++)
+            if (r != rank && aug[r][col])
+                for (int j = 0; j < W; j++) aug[r][j] ^= aug[rank][j];
+        piv.push_back(col);
+        rank++;
+    }
+    if (rank != k) return fail(MPW_ERR_ARG, "generator rank %d < k=%d", rank, k);
+    std::vector<uint64_t> mix(k, 0);
+    for (int r = 0; r < k; r++)
+        for (int j = 0; j < k; j++)
+            if (aug[r][n + j]) mix[r] |= 1ull << j;
+
+    CK(h->info.ensure(kp)); CK(h->frozen.ensure(nw)); CK(h->gen.ensure((size_t)k * nw));
+    CK(h->crc_h.ensure(crc_h.size())); CK(h->pivots.ensure(k)); CK(h->mix.ensure(k));
+    CK(cudaMemcpy(h->info.p, info_set, sizeof(int32_t) * kp, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->frozen.p, frozen.data(), sizeof(uint32_t) * nw, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->gen.p, gen.data(), sizeof(uint32_t) * gen.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->crc_h.p, crc_h.data(), sizeof(uint64_t) * crc_h.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->pivots.p, piv.data(), sizeof(int32_t) * k, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->mix.p, mix.data(), sizeof(uint64_t) * k, cudaMemcpyHostToDevice));
+    h->has_code = true;
+    h->has_pat = false;   // patterns must match the blocklength
+    return 0;
+}
+
+int mpw_set_patterns(mpw_handle* h, const uint64_t* pattern_words, int np) {
+    if (!h || (!pattern_words && np > 0) || np < 0) return fail(MPW_ERR_ARG, "bad pattern arguments");
+    if (!h->has_code) return fail(MPW_ERR_STATE, "mpw_set_code must be called before mpw_set_patterns");
+    if (set_device(h)) return MPW_ERR_CUDA;
+    const int n = h->n, nw = h->nw, w64 = (n + 63) / 64;
+    std::vector<uint32_t> bits((size_t)np * nw, 0);
+    std::vector<int32_t> off(np + 1, 0), soff(np + 1, 0);
+    std::vector<uint16_t> idx;
+    std::vector<uint16_t> sup;
+    for (int p = 0; p < np; p++) {
+        off[p] = (int32_t)idx.size();
+        soff[p] = (int32_t)(sup.size() / 8);
+        int w = 0;
+        for (int j = 0; j < n; j++)
+            if ((pattern_words[(size_t)p * w64 + (j >> 6)] >> (j & 63)) & 1ull) {
+                bits[(size_t)p * nw + (j >> 5)] |= 1u << (j & 31);
+                idx.push_back((uint16_t)j);
+                sup.push_back((uint16_t)j);
+                w++;
+            }
+        if (w == 0) return fail(MPW_ERR_ARG, "pattern %d is the zero word (exclude member 0)", p);
+        while (sup.size() % 8) sup.push_back((uint16_t)n);   // index n = zero row
+    }
+    off[np] = (int32_t)idx.size();
+    soff[np] = (int32_t)(sup.size() / 8);
+    h->np = np;
+    h->total_sup_u4 = (int)(sup.size() / 8);
+    CK(h->pbits.ensure(bits.size())); CK(h->poff.ensure(off.size())); CK(h->soff.ensure(soff.size()));
+    CK(h->pidx.ensure(std::max<size_t>(idx.size(), 1))); CK(h->sup.ensure(std::max<size_t>(sup.size() / 8, 1)));
+    if (np) {
+        CK(cudaMemcpy(h->pbits.p, bits.data(), sizeof(uint32_t) * bits.size(), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(h->pidx.p, idx.data(), sizeof(uint16_t) * idx.size(), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(h->sup.p, sup.data(), sizeof(uint16_t) * sup.size(), cudaMemcpyHostToDevice));
+    }
+    CK(cudaMemcpy(h->poff.p, off.data(), sizeof(int32_t) * off.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->soff.p, soff.data(), sizeof(int32_t) * soff.size(), cudaMemcpyHostToDevice));
+    tc_release(h->tcp);
+    if (tc_supported(n, np)) {
+        if (tc_build(h->tcp, bits.data(), np, n, nw)) return fail(MPW_ERR_CUDA, "building the tensor-core operand failed: %s", cudaGetErrorString(cudaGetLastError()));
+    }
+    h->has_pat = true;
+    return 0;
+}
+
+int mpw_scl_batch(mpw_handle* h, const float* y, const double* llr, int F, double sigma, int L,
+                  int32_t* list_n, uint32_t* list_u, uint32_t* list_cw, double* list_pm, void* stream) {
+    if (!h || (!y && !llr) || F < 0) return fail(MPW_ERR_ARG, "bad arguments");
+    if (!h->has_code) return fail(MPW_ERR_STATE, "no code set");
+    if (L < 1 || L > SCL_MAX_L) return fail(MPW_ERR_UNSUPPORTED, "list size %d outside [1,%d]", L, SCL_MAX_L);
+    if (F == 0) return 0;
+    if (set_device(h)) return MPW_ERR_CUDA;
+    cudaStream_t st = (cudaStream_t)stream;
+    SclOut out{list_n, list_u, list_cw, list_pm, nullptr, nullptr, nullptr};
+    S2Dev s2{};
+    return dispatch_scl(h, y, llr, F, sigma, L, 0, 0, out, s2, st);
+}
+
+int mpw_mpwsd_batch(mpw_handle* h, const float* y, const uint32_t* anchors, const int32_t* n_anchor,
+                    int F, int A, int T, int variant, uint32_t* best, double* best_ed,
+                    int32_t* iters, int32_t* hops, uint8_t* flags, void* stream) {
+    if (!h || !y || !anchors || !best || !best_ed || F < 0 || A < 1 || T < 1) return fail(MPW_ERR_ARG, "bad arguments");
+    if (!h->has_pat) return fail(MPW_ERR_STATE, "no pattern set");
+    if (F == 0) return 0;
+    if (set_device(h)) return MPW_ERR_CUDA;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (int rc = ensure_s2(h, F, A, T)) return rc;
+    S2Dev s2 = s2_dev(h, anchors);
+    if (!hops) s2.traj_hops = h->traj_hops.p;
+    queue_identity_kernel<<<(F + 255) / 256, 256, 0, st>>>(F, A, n_anchor, s2);
+    CK(cudaGetLastError());
+    if (int rc = run_hops(h, y, F, A, T, variant, s2, st)) return rc;
+    FinalOut fo{best, best_ed, nullptr, iters, hops, nullptr, flags, nullptr};
+    return finalize(h, y, F, A, T, s2, fo, st);
+}
+
+int mpw_two_stage_batch(mpw_handle* h, const float* y, int F, double sigma, int L, int A, int T,
+                        int mode, int variant, const uint32_t* tx_cw, uint32_t* best, uint64_t* best_msg,
+                        double* best_ed, uint8_t* stage, int32_t* iters, int32_t* hops,
+                        uint32_t* anchors_out, uint8_t* flags, unsigned long long* counters, void* stream) {
+    if (!h || !y || !best || !best_ed || !stage || F < 0 || A < 1 || T < 1) return fail(MPW_ERR_ARG, "bad arguments");
+    if (!h->has_code || !h->has_pat) return fail(MPW_ERR_STATE, "code and pattern set must be set first");
+    if (L < 1 || L > SCL_MAX_L) return fail(MPW_ERR_UNSUPPORTED, "list size %d outside [1,%d]", L, SCL_MAX_L);
+    if (mode != MPW_MODE_CRC_GATED && mode != MPW_MODE_ALWAYS_ON) return fail(MPW_ERR_ARG, "unknown activation mode %d", mode);
+    if (mode == MPW_MODE_CRC_GATED && !h->is_ca) return fail(MPW_ERR_ARG, "crc_gated mode requires a CRC-concatenated code");
+    if (F == 0) return 0;
+    if (set_device(h)) return MPW_ERR_CUDA;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (int rc = ensure_s2(h, F, A, T)) return rc;
+    S2Dev s2 = s2_dev(h, nullptr);
+    if (h->timing && !h->ev_init) {
+        for (int i = 0; i < 8; i++) CK(cudaEventCreate(&h->ev[i]));
+        h->ev_init = true;
+    }
+    CK(cudaMemsetAsync(s2.count, 0, sizeof(int32_t), st));
+    CK(cudaMemsetAsync(s2.work_next, 0, sizeof(int32_t), st));
+    timing_mark(h, 0, st);
+    SclOut out{nullptr, nullptr, nullptr, nullptr, stage, best, best_ed};
+    const int smode = (mode == MPW_MODE_CRC_GATED) ? 1 : 2;
+    if (int rc = dispatch_scl(h, y, nullptr, F, sigma, L, A, smode, out, s2, st)) return rc;
+    timing_mark(h, 1, st);
+    if (int rc = run_hops(h, y, F, A, T, variant, s2, st)) return rc;
+    timing_mark(h, 2, st);
+    FinalOut fo{best, best_ed, stage, iters, hops, anchors_out, flags, nullptr};
+    if (int rc = finalize(h, y, F, A, T, s2, fo, st)) return rc;
+    timing_mark(h, 3, st);
+    FrameArgs fa;
+    fa.F = F; fa.A = A; fa.T = T; fa.nw = h->nw; fa.k = h->k; fa.np = h->np;
+    fa.best = best; fa.stage = stage; fa.tx = tx_cw; fa.iters = iters; fa.hops = hops; fa.flags = flags;
+    fa.msg_out = best_msg; fa.counters = counters; fa.pivots = h->pivots.p; fa.mix = h->mix.p;
+    frame_kernel<<<(F + 255) / 256, 256, 0, st>>>(fa);
+    CK(cudaGetLastError());
+    timing_mark(h, 4, st);
+    return timing_close(h);
+}
+
+int mpw_two_stage_batch_host(mpw_handle* h, const float* y_host, int F, double sigma, int L, int A, int T,
+                             int mode, int variant, const uint32_t* tx_host, uint32_t* best_host,
+                             uint64_t* msg_host, double* ed_host, uint8_t* stage_host, int32_t* iters_host,
+                             uint8_t* flags_host, unsigned long long* counters_host, void* stream) {
+    if (!h || !y_host || F < 0) return fail(MPW_ERR_ARG, "bad arguments");
+    if (F == 0) return 0;
+    if (set_device(h)) return MPW_ERR_CUDA;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int n = h->n, nw = h->nw;
+    static thread_local DevBuf<float> dy;
+    static thread_local DevBuf<uint32_t> dtx, dbest;
+    static thread_local DevBuf<uint64_t> dmsg;
+    static thread_local DevBuf<double> ded;
+    static thread_local DevBuf<uint8_t> dstage, dflags;
+    static thread_local DevBuf<int32_t> diters;
+    static thread_local DevBuf<unsigned long long> dctr;
+    CK(dy.ensure((size_t)F * n)); CK(dbest.ensure((size_t)F * nw)); CK(dmsg.ensure(F)); CK(ded.ensure(F));
+    CK(dstage.ensure(F)); CK(dflags.ensure(F)); CK(diters.ensure((size_t)F * A)); CK(dctr.ensure(MPW_NUM_COUNTERS));
+    CK(cudaMemcpyAsync(dy.p, y_host, sizeof(float) * (size_t)F * n, cudaMemcpyHostToDevice, st));
+    if (tx_host) {
+        CK(dtx.ensure((size_t)F * nw));
+        CK(cudaMemcpyAsync(dtx.p, tx_host, sizeof(uint32_t) * (size_t)F * nw, cudaMemcpyHostToDevice, st));
+    }
+    CK(cudaMemsetAsync(dctr.p, 0, sizeof(unsigned long long) * MPW_NUM_COUNTERS, st));
+    int rc = mpw_two_stage_batch(h, dy.p, F, sigma, L, A, T, mode, variant, tx_host ? dtx.p : nullptr, dbest.p,
+                                 dmsg.p, ded.p, dstage.p, diters.p, nullptr, nullptr, dflags.p, dctr.p, stream);
+    if (rc) return rc;
+    if (best_host) CK(cudaMemcpyAsync(best_host, dbest.p, sizeof(uint32_t) * (size_t)F * nw, cudaMemcpyDeviceToHost, st));
+    if (msg_host) CK(cudaMemcpyAsync(msg_host, dmsg.p, sizeof(uint64_t) * F, cudaMemcpyDeviceToHost, st));
+    if (ed_host) CK(cudaMemcpyAsync(ed_host, ded.p, sizeof(double) * F, cudaMemcpyDeviceToHost, st));
+    if (stage_host) CK(cudaMemcpyAsync(stage_host, dstage.p, F, cudaMemcpyDeviceToHost, st));
+    if (iters_host) CK(cudaMemcpyAsync(iters_host, diters.p, sizeof(int32_t) * (size_t)F * A, cudaMemcpyDeviceToHost, st));
+    if (flags_host) CK(cudaMemcpyAsync(flags_host, dflags.p, F, cudaMemcpyDeviceToHost, st));
+    if (counters_host) CK(cudaMemcpyAsync(counters_host, dctr.p, sizeof(unsigned long long) * MPW_NUM_COUNTERS, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return 0;
+}
+
+int mpw_set_timing(mpw_handle* h, int enable) {
+    if (!h) return fail(MPW_ERR_ARG, "null handle");
+    h->timing = enable ? 1 : 0;
+    return 0;
+}
+
+int mpw_read_timing(mpw_handle* h, double* ms_out /*4*/, long long* launches_out /*4*/, int reset) {
+    if (!h) return fail(MPW_ERR_ARG, "null handle");
+    for (int i = 0; i < 4; i++) {
+        if (ms_out) ms_out[i] = h->acc_ms[i];
+        if (launches_out) launches_out[i] = h->launches[i];
+        if (reset) { h->acc_ms[i] = 0; h->launches[i] = 0; }
+    }
+    return 0;
+}
+
+int mpw_num_patterns(mpw_handle* h) { return h ? h->np : -1; }
+
+int mpw_tensor_path_ready(mpw_handle* h) { return (h && h->tcp.ready) ? 1 : 0; }
+
+}  // extern "C"

@@ -1,0 +1,607 @@
+"""Drop-in for the reference's decoder API on the B200 path.
+
+Same names, arguments, return types and errors as
+/root/reference/pkg/src/feclab/decoders.py (re-exported by its __init__.py:28-39):
+
+  scl_decode(llrs, code, list_size, counters=None)                 decoders.py:181-268
+  wsd_step(y, center, x_center, sphere, m, counters=None)          decoders.py:401-417
+  wsd_trajectory(y, c0, sphere, params, counters=None, ...)        decoders.py:420-452
+  mp_wsd(y, init_list, sphere, params, counters=None)              decoders.py:455-514
+  two_stage_decode(y, code, stage1, params, sphere, sigma=1.0, counters=None)
+                                                                   decoders.py:520-583
+
+plus the throughput entry point `DeviceDecoder.two_stage_batch` /
+`two_stage_decode_batch` over [F, N] batches.  Every call runs the sm_100a
+kernels of libmpwsd.so; there is no CPU fallback (a missing library or GPU
+raises).  Received words are float32 on the device (the path's dtype);
+stage 1 computes LLRs and path metrics in float64 and is bit-exact with the
+reference; hop decisions agree with the reference except at near-ties
+(|ΔED| gaps < 1e-5 relative), which are flagged per frame.
+
+Code and sphere arguments may be this package's objects or the reference's
+(duck-typed on n, k, kind, info_set, crc, inner, generator.words,
+member_words).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import weakref
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from .bits import BitVector, num_words, pack_bits, unpack_bits
+from .codes import crc_poly_int, message_words, inverse_tables, polar_transform_bits
+
+# ---------------------------------------------------------------------------
+# Parameter / result types (decoders.py:37-118)
+
+
+@dataclass
+class CandidateList:
+    entries: list
+
+    def __post_init__(self):
+        scores = [s for _, s in self.entries]
+        if any(a > b for a, b in zip(scores, scores[1:])):
+            raise ValueError("candidate scores must be nondecreasing")
+
+    def __len__(self) -> int:
+        return len(self.entries)
+
+
+@dataclass(frozen=True)
+class SclStage:
+    list_size: int
+
+
+@dataclass(frozen=True)
+class OsdStage:
+    order: int
+    list_cap: int | None = None
+
+
+def default_filter_size(sphere_size: int) -> int:
+    """max(10, ceil(0.02 |S|)) (decoders.py:94-96)."""
+    return max(10, math.ceil(0.02 * sphere_size))
+
+
+@dataclass
+class WsdParams:
+    radius_index: int
+    filter_size: int | None = None
+    max_iterations: int = 4
+    num_paths: int = 4
+    activation_mode: str = "crc_gated"
+
+    def __post_init__(self):
+        if self.max_iterations < 1 or self.num_paths < 1:
+            raise ValueError("max_iterations and num_paths must be >= 1")
+        if self.filter_size is not None and self.filter_size < 1:
+            raise ValueError("filter_size must be >= 1")
+        if self.activation_mode not in ("crc_gated", "always_on"):
+            raise ValueError(f"unknown activation mode {self.activation_mode!r}")
+
+    def resolve_filter_size(self, sphere) -> int:
+        if self.filter_size is not None:
+            return self.filter_size
+        return default_filter_size(_sphere_size(sphere))
+
+
+@dataclass
+class TrajectoryTrace:
+    path_index: int
+    centers: list
+    squared_eds: list
+    active_history: list
+    iterations_used: int
+
+
+@dataclass
+class DecodeResult:
+    best_codeword: BitVector
+    best_message: BitVector | None
+    squared_ed: float
+    stage: str
+    traces: list
+    counters: object
+    near_tie: bool = False
+
+
+@dataclass
+class OpCounter:
+    """Field-compatible with the reference's OpCounter (complexity.py:17-44)."""
+
+    ed_evaluations: int = 0
+    gain_additions: int = 0
+    sort_comparisons: int = 0
+    scl_node_ops: int = 0
+    osd_reencodes: int = 0
+    misc_flops: int = 0
+
+    def merge(self, other) -> None:
+        for f in ("ed_evaluations", "gain_additions", "sort_comparisons", "scl_node_ops",
+                  "osd_reencodes", "misc_flops"):
+            setattr(self, f, getattr(self, f) + getattr(other, f))
+
+
+# ---------------------------------------------------------------------------
+# Table extraction (duck-typed)
+
+def _sphere_size(sphere) -> int:
+    return int(np.asarray(sphere.member_words).shape[0])
+
+
+def _code_tables(code):
+    """(n, k, kp, info_set, gen_words, is_ca, crc_deg, crc_poly, scl_ok)."""
+    n, k = int(code.n), int(code.k)
+    gen = np.ascontiguousarray(code.generator.words, dtype=np.uint64)
+    if code.kind == "crc_concatenated" and getattr(code, "inner", None) is not None \
+            and code.inner.kind == "polar":
+        info = np.asarray(code.inner.info_set, dtype=np.int32)
+        return n, k, int(info.size), info, gen, 1, int(code.crc.degree), crc_poly_int(code.crc), True
+    if code.kind == "polar":
+        info = np.asarray(code.info_set, dtype=np.int32)
+        return n, k, int(info.size), info, gen, 0, 0, 0, True
+    # hop-only (e.g. Reed-Muller): SCL is unavailable, as in the reference
+    info = np.arange(n - k, n, dtype=np.int32)
+    return n, k, k, info, gen, 0, 0, 0, False
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _dev_tensor(a, dtype, device):
+    """Host array or tensor -> contiguous device tensor.  uint32 host words are
+    reinterpreted (not converted) as int32."""
+    torch = _torch()
+    if isinstance(a, torch.Tensor):
+        return a.to(device=device, dtype=dtype).contiguous()
+    arr = np.ascontiguousarray(a)
+    if arr.dtype == np.uint32 and dtype == torch.int32:
+        arr = arr.view(np.int32)
+    return torch.from_numpy(arr).to(device=device, dtype=dtype).contiguous()
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+def words64_to_32(words64: np.ndarray, n: int) -> np.ndarray:
+    """uint64 reference layout [..., ceil(n/64)] -> uint32 device layout [..., max(1, n/32)]."""
+    w = np.ascontiguousarray(words64, dtype=np.uint64)
+    w32 = w.view("<u4").reshape(w.shape[:-1] + (2 * w.shape[-1],))
+    nw = max(1, n // 32)
+    return np.ascontiguousarray(w32[..., :nw])
+
+
+def words32_to_64(words32: np.ndarray, n: int) -> np.ndarray:
+    w = np.ascontiguousarray(words32).astype(np.uint32, copy=False)
+    nw64 = num_words(n)
+    pad = 2 * nw64 - w.shape[-1]
+    if pad:
+        w = np.concatenate([w, np.zeros(w.shape[:-1] + (pad,), np.uint32)], axis=-1)
+    return np.ascontiguousarray(w).view("<u8").astype(np.uint64).reshape(w.shape[:-1] + (nw64,))
+
+
+# ---------------------------------------------------------------------------
+# Device decoder: one libmpwsd handle bound to (code, pattern set)
+
+_HOP = {"auto": _native.HOP_AUTO, "gather": _native.HOP_GATHER, "tensor": _native.HOP_TENSOR}
+
+
+class DeviceDecoder:
+    def __init__(self, code, sphere=None, device=None):
+        torch = _torch()
+        if not torch.cuda.is_available():
+            raise _native.NativeError("no CUDA device visible: the MP-WSD decoder has no CPU fallback")
+        lib = _native.lib()
+        idx = torch.cuda.current_device() if device is None else torch.device(device).index or 0
+        self.device = torch.device("cuda", idx)
+        h = ctypes.c_void_p()
+        _native.check(lib.mpw_create(idx, ctypes.byref(h)), "mpw_create")
+        self._h = h
+        self.code = code
+        (self.n, self.k, self.kp, self.info, gen, self.is_ca, self.crc_deg, self.crc_poly,
+         self.scl_ok) = _code_tables(code)
+        self.nw = max(1, self.n // 32)
+        _native.value_error_check(lib.mpw_set_code(
+            h, self.n, self.k, self.kp, self.info.ctypes.data, gen.ctypes.data, self.is_ca,
+            self.crc_deg, ctypes.c_uint32(self.crc_poly)), "mpw_set_code")
+        self._pivots, self._mix = inverse_tables(gen, self.n, self.k)
+        self.np = 0
+        self.sphere = None
+        if sphere is not None:
+            self.set_sphere(sphere)
+
+    def set_sphere(self, sphere):
+        pats = np.ascontiguousarray(np.asarray(sphere.member_words, dtype=np.uint64)[1:])
+        if int(sphere.n) != self.n:
+            raise ValueError("sphere blocklength does not match the code")
+        _native.value_error_check(_native.lib().mpw_set_patterns(
+            self._h, pats.ctypes.data if pats.size else None, int(pats.shape[0])), "mpw_set_patterns")
+        self.np = int(pats.shape[0])
+        self.sphere = sphere
+        self.patterns64 = pats
+
+    @property
+    def tensor_path_ready(self) -> bool:
+        return bool(_native.lib().mpw_tensor_path_ready(self._h))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _native.lib().mpw_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _stream(self, stream):
+        torch = _torch()
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        return ctypes.c_void_p(s.cuda_stream)
+
+    # -- batch entry points -------------------------------------------------
+    def two_stage_batch(self, y, sigma: float, list_size: int, num_paths: int, max_iterations: int,
+                        activation_mode: str = "crc_gated", variant: str = "auto", tx_words=None,
+                        want_hops: bool = False, want_anchors: bool = False, counters=None,
+                        stream=None, out=None):
+        """y: [F, N] float32 (torch on this device, or host array).  Returns a
+        dict of device tensors; uint32 words are carried in int32 tensors."""
+        torch = _torch()
+        if activation_mode not in ("crc_gated", "always_on"):
+            raise ValueError(f"unknown activation mode {activation_mode!r}")
+        if activation_mode == "crc_gated" and not self.is_ca:
+            raise ValueError("crc_gated mode requires a CRC-concatenated code")
+        if not self.scl_ok:
+            raise ValueError("SCL stage requires a polar or CRC-polar code")
+        yd = _dev_tensor(y, torch.float32, self.device)
+        F = int(yd.shape[0])
+        A, T, nw = int(num_paths), int(max_iterations), self.nw
+        o = out if out is not None else self.alloc_outputs(F, A, T, want_hops, want_anchors)
+        txd = None if tx_words is None else _dev_tensor(tx_words, torch.int32, self.device)
+        ctr = counters if counters is not None else o.get("counters")
+        rc = _native.lib().mpw_two_stage_batch(
+            self._h, _ptr(yd), F, float(sigma), int(list_size), A, T,
+            _native.MODE_CRC_GATED if activation_mode == "crc_gated" else _native.MODE_ALWAYS_ON,
+            _HOP[variant], _ptr(txd), _ptr(o["best"]), _ptr(o["best_msg"]), _ptr(o["best_ed"]),
+            _ptr(o["stage"]), _ptr(o["iters"]), _ptr(o.get("hops")), _ptr(o.get("anchors")),
+            _ptr(o["flags"]), _ptr(ctr), self._stream(stream))
+        _native.value_error_check(rc, "mpw_two_stage_batch")
+        return o
+
+    def alloc_outputs(self, F, A, T, want_hops=False, want_anchors=False):
+        torch = _torch()
+        d = self.device
+        o = dict(best=torch.empty((F, self.nw), dtype=torch.int32, device=d),
+                 best_msg=torch.empty((F,), dtype=torch.int64, device=d),
+                 best_ed=torch.empty((F,), dtype=torch.float64, device=d),
+                 stage=torch.empty((F,), dtype=torch.uint8, device=d),
+                 iters=torch.empty((F, A), dtype=torch.int32, device=d),
+                 flags=torch.empty((F,), dtype=torch.uint8, device=d),
+                 counters=torch.zeros((_native.NUM_COUNTERS,), dtype=torch.int64, device=d))
+        if want_hops:
+            o["hops"] = torch.empty((F, A, T), dtype=torch.int32, device=d)
+        if want_anchors:
+            o["anchors"] = torch.zeros((F, A, self.nw), dtype=torch.int32, device=d)
+        return o
+
+    def mp_wsd_batch(self, y, anchors_words32, max_iterations: int, n_anchor=None,
+                     variant: str = "auto", stream=None):
+        """anchors: [F, A, nw] uint32 device layout.  Returns dict of device tensors."""
+        torch = _torch()
+        yd = _dev_tensor(y, torch.float32, self.device)
+        ad = _dev_tensor(anchors_words32, torch.int32, self.device)
+        F, A = int(ad.shape[0]), int(ad.shape[1])
+        T = int(max_iterations)
+        nad = None if n_anchor is None else _dev_tensor(np.asarray(n_anchor, np.int32), torch.int32, self.device)
+        d = self.device
+        o = dict(best=torch.empty((F, self.nw), dtype=torch.int32, device=d),
+                 best_ed=torch.empty((F,), dtype=torch.float64, device=d),
+                 iters=torch.empty((F, A), dtype=torch.int32, device=d),
+                 hops=torch.empty((F, A, T), dtype=torch.int32, device=d),
+                 flags=torch.empty((F,), dtype=torch.uint8, device=d))
+        rc = _native.lib().mpw_mpwsd_batch(
+            self._h, _ptr(yd), _ptr(ad), _ptr(nad), F, A, T, _HOP[variant], _ptr(o["best"]),
+            _ptr(o["best_ed"]), _ptr(o["iters"]), _ptr(o["hops"]), _ptr(o["flags"]), self._stream(stream))
+        _native.value_error_check(rc, "mpw_mpwsd_batch")
+        return o
+
+    def scl_batch(self, llrs=None, y=None, sigma: float = 1.0, list_size: int = 4, stream=None):
+        torch = _torch()
+        if not self.scl_ok:
+            raise ValueError("scl_decode requires a polar code (pass the inner code "
+                             "of a CRC-concatenated construction)")
+        L = int(list_size)
+        if llrs is not None:
+            xd = _dev_tensor(llrs, torch.float64, self.device)
+            yd = None
+        else:
+            yd = _dev_tensor(y, torch.float32, self.device)
+            xd = None
+        F = int((xd if xd is not None else yd).shape[0])
+        d = self.device
+        o = dict(list_n=torch.zeros((F,), dtype=torch.int32, device=d),
+                 list_u=torch.zeros((F, L, self.nw), dtype=torch.int32, device=d),
+                 list_cw=torch.zeros((F, L, self.nw), dtype=torch.int32, device=d),
+                 list_pm=torch.zeros((F, L), dtype=torch.float64, device=d))
+        rc = _native.lib().mpw_scl_batch(self._h, _ptr(yd), _ptr(xd), F, float(sigma), L,
+                                         _ptr(o["list_n"]), _ptr(o["list_u"]), _ptr(o["list_cw"]),
+                                         _ptr(o["list_pm"]), self._stream(stream))
+        _native.value_error_check(rc, "mpw_scl_batch")
+        return o
+
+    def message_of_words(self, cw_words64: np.ndarray) -> np.ndarray:
+        return message_words(self._pivots, self._mix, unpack_bits(cw_words64, self.n))
+
+    # -- timing -------------------------------------------------------------
+    def set_timing(self, enable: bool):
+        _native.check(_native.lib().mpw_set_timing(self._h, int(bool(enable))))
+
+    def read_timing(self, reset: bool = True):
+        ms = np.zeros(4, np.float64)
+        n = np.zeros(4, np.int64)
+        _native.check(_native.lib().mpw_read_timing(self._h, ms.ctypes.data, n.ctypes.data, int(reset)))
+        return ms, n
+
+
+# ---------------------------------------------------------------------------
+# Per-frame drop-in API
+
+_cache: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+_code_only: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+
+
+def get_decoder(code, sphere) -> DeviceDecoder:
+    per = _cache.get(sphere)
+    if per is None:
+        per = weakref.WeakKeyDictionary()
+        _cache[sphere] = per
+    dec = per.get(code)
+    if dec is None:
+        dec = DeviceDecoder(code, sphere)
+        per[code] = dec
+    return dec
+
+
+class _HopCode:
+    """Minimal code stand-in for hop-only calls (mp_wsd/wsd_* take no code)."""
+
+    kind = "generic"
+
+    def __init__(self, n):
+        self.n, self.k = n, 1
+
+        class _G:
+            pass
+        self.generator = _G()
+        self.generator.words = pack_bits(np.ones((1, n), np.uint8))
+
+
+_hop_codes: dict = {}
+
+
+def _hop_decoder(sphere) -> DeviceDecoder:
+    n = int(sphere.n)
+    code = _hop_codes.setdefault(n, _HopCode(n))
+    return get_decoder(code, sphere)
+
+
+def _modulate(words64, n):
+    return 1.0 - 2.0 * unpack_bits(words64, n).astype(np.float64)
+
+
+def _sqdist(y, words64, n) -> float:
+    d = np.asarray(y, dtype=np.float64) - _modulate(words64, n)
+    return float(d @ d)
+
+
+def _step_counters(counters, sphere, m, n):
+    """Counter charges of one executed scan (decoders.py:375-389)."""
+    nz = _sphere_size(sphere) - 1
+    if nz == 0:
+        return
+    counters.misc_flops += n
+    m_eff = min(m, nz)
+    if m_eff < nz:
+        w = np.bitwise_count(np.asarray(sphere.member_words, dtype=np.uint64)[1:]).sum()
+        counters.gain_additions += int(w)
+        if m_eff >= 2:
+            counters.sort_comparisons += nz * math.ceil(math.log2(m_eff))
+    counters.ed_evaluations += m_eff
+    counters.misc_flops += m_eff
+
+
+def _run_hops(dec, y, anchors64, T):
+    """Device mp_wsd over one frame's anchors; returns host arrays."""
+    n = dec.n
+    y32 = np.asarray(y, dtype=np.float64).astype(np.float32)[None, :]
+    a32 = words64_to_32(np.asarray(anchors64, dtype=np.uint64), n)[None, :, :]
+    o = dec.mp_wsd_batch(y32, a32, T)
+    return {k: v.cpu().numpy() for k, v in o.items()}
+
+
+def _traces_from_hops(y, sphere, anchors64, iters, hops, n):
+    members = np.asarray(sphere.member_words, dtype=np.uint64)
+    traces = []
+    for k, anc in enumerate(anchors64):
+        words = np.array(anc, dtype=np.uint64)
+        centers = [BitVector(n, words)]
+        eds = [_sqdist(y, words, n)]
+        hist = []
+        for h in range(int(iters[k])):
+            mem = int(hops[k, h])
+            if mem > 0:
+                words = words ^ members[mem]
+                centers.append(BitVector(n, words))
+                eds.append(_sqdist(y, words, n))
+                hist.append(True)
+            else:
+                hist.append(False)
+        traces.append(TrajectoryTrace(k, centers, eds, hist, int(iters[k])))
+    return traces
+
+
+def mp_wsd(y, init_list, sphere, params, counters=None) -> DecodeResult:
+    """decoders.py:455-514 on the device."""
+    if len(init_list) == 0:
+        raise ValueError("initial candidate list is empty")
+    if counters is None:
+        counters = OpCounter()
+    y = np.asarray(y, dtype=np.float64)
+    n = int(sphere.n)
+    m = params.resolve_filter_size(sphere)
+    anchors = init_list.entries[:params.num_paths]
+    anc64 = np.stack([np.asarray(cw.words, dtype=np.uint64) for cw, _ in anchors])
+    counters.ed_evaluations += len(anchors)
+    dec = _hop_decoder(sphere)
+    r = _run_hops(dec, y, anc64, params.max_iterations)
+    iters, hops = r["iters"][0], r["hops"][0]
+    traces = _traces_from_hops(y, sphere, anc64, iters, hops, n)
+    for t in traces:
+        for _ in range(t.iterations_used):
+            _step_counters(counters, sphere, m, n)
+    finals = [t.squared_eds[-1] for t in traces]
+    best_k = int(np.argmin(finals))
+    return DecodeResult(best_codeword=traces[best_k].centers[-1], best_message=None,
+                        squared_ed=finals[best_k], stage="mp_wsd", traces=traces,
+                        counters=counters, near_tie=bool(r["flags"][0]))
+
+
+def wsd_trajectory(y, c0, sphere, params, counters=None, force_full_iterations=False,
+                   path_index=0) -> TrajectoryTrace:
+    """decoders.py:420-452.  force_full_iterations only affects the counters
+    (the result is unchanged, decoders.py:427-428)."""
+    if counters is None:
+        counters = OpCounter()
+    y = np.asarray(y, dtype=np.float64)
+    n = int(sphere.n)
+    m = params.resolve_filter_size(sphere)
+    counters.ed_evaluations += 1
+    dec = _hop_decoder(sphere)
+    anc = np.asarray(c0.words, dtype=np.uint64)[None, :]
+    r = _run_hops(dec, y, anc, params.max_iterations)
+    tr = _traces_from_hops(y, sphere, anc, r["iters"][0], r["hops"][0], n)[0]
+    tr.path_index = path_index
+    scans = params.max_iterations if force_full_iterations else tr.iterations_used
+    if force_full_iterations:
+        tr.active_history = tr.active_history + [False] * (scans - len(tr.active_history))
+        tr.iterations_used = scans
+    for _ in range(scans):
+        _step_counters(counters, sphere, m, n)
+    return tr
+
+
+def wsd_step(y, center, x_center, sphere, m, counters=None):
+    """decoders.py:401-417.  The hop is taken from the modulated `center`."""
+    if m < 1:
+        raise ValueError("m must be >= 1")
+    if counters is None:
+        counters = OpCounter()
+    y = np.asarray(y, dtype=np.float64)
+    n = int(sphere.n)
+    counters.ed_evaluations += 1
+    dec = _hop_decoder(sphere)
+    anc = np.asarray(center.words, dtype=np.uint64)[None, :]
+    r = _run_hops(dec, y, anc, 1)
+    _step_counters(counters, sphere, m, n)
+    mem = int(r["hops"][0, 0, 0])
+    if mem > 0:
+        members = np.asarray(sphere.member_words, dtype=np.uint64)
+        return BitVector(center.length, np.asarray(center.words, np.uint64) ^ members[mem]), True
+    return BitVector(center.length, np.asarray(center.words, np.uint64)), False
+
+
+def scl_decode(llrs, code, list_size, counters=None) -> CandidateList:
+    """decoders.py:181-268 on the device (float64, bit-exact)."""
+    if code.kind != "polar":
+        raise ValueError("scl_decode requires a polar code (pass the inner code "
+                         "of a CRC-concatenated construction)")
+    llrs = np.asarray(llrs, dtype=np.float64)
+    n = int(code.n)
+    if llrs.shape != (n,):
+        raise ValueError("LLR length mismatch")
+    if counters is None:
+        counters = OpCounter()
+    dec = _code_only.get(code)
+    if dec is None:
+        dec = DeviceDecoder(code, None)
+        _code_only[code] = dec
+    o = dec.scl_batch(llrs=llrs[None, :], list_size=list_size)
+    cnt = int(o["list_n"][0].item())
+    cw = words32_to_64(o["list_cw"][0, :cnt].cpu().numpy().view(np.uint32), n)
+    pm = o["list_pm"][0, :cnt].cpu().numpy()
+    counters.scl_node_ops += int(list_size) * n * (n.bit_length() - 1)
+    return CandidateList([(BitVector(n, cw[i]), float(pm[i])) for i in range(cnt)])
+
+
+def two_stage_decode(y, code, stage1, params, sphere, sigma=1.0, counters=None) -> DecodeResult:
+    """decoders.py:520-583 on the device."""
+    if counters is None:
+        counters = OpCounter()
+    y = np.asarray(y, dtype=np.float64)
+    gated = params.activation_mode == "crc_gated"
+    if gated and code.kind != "crc_concatenated":
+        raise ValueError("crc_gated mode requires a CRC-concatenated code")
+    if isinstance(stage1, OsdStage) or type(stage1).__name__ == "OsdStage":
+        raise ValueError("OSD stage 1 is outside the accelerated path (SURVEY.md §8f)")
+    if not hasattr(stage1, "list_size"):
+        raise ValueError(f"unknown stage-1 spec {stage1!r}")
+    if not (code.kind == "polar" or (code.kind == "crc_concatenated"
+                                      and getattr(code.inner, "kind", None) == "polar")):
+        raise ValueError("SCL stage requires a polar or CRC-polar code")
+    n = int(code.n)
+    dec = get_decoder(code, sphere)
+    A, T = params.num_paths, params.max_iterations
+    o = dec.two_stage_batch(y.astype(np.float32)[None, :], sigma, stage1.list_size, A, T,
+                            params.activation_mode, want_hops=True, want_anchors=True)
+    h = {k: v.cpu().numpy() for k, v in o.items()}
+    counters.scl_node_ops += int(stage1.list_size) * n * (n.bit_length() - 1)
+    best64 = words32_to_64(h["best"][0].view(np.uint32), n)[0]
+    best = BitVector(n, best64)
+    msg = BitVector(int(code.k), dec.message_of_words(best64))
+    if h["stage"][0] == 0:
+        return DecodeResult(best_codeword=best, best_message=msg,
+                            squared_ed=_sqdist(y, best64, n), stage="stage1_crc_pass",
+                            traces=[], counters=counters, near_tie=False)
+    iters = h["iters"][0]
+    na = int((iters > 0).sum())
+    anc64 = words32_to_64(h["anchors"][0, :na].view(np.uint32), n)
+    m = params.resolve_filter_size(sphere)
+    counters.ed_evaluations += na
+    traces = _traces_from_hops(y, sphere, anc64, iters[:na], h["hops"][0], n)
+    for t in traces:
+        for _ in range(t.iterations_used):
+            _step_counters(counters, sphere, m, n)
+    finals = [t.squared_eds[-1] for t in traces]
+    best_k = int(np.argmin(finals))
+    bc = traces[best_k].centers[-1]
+    return DecodeResult(best_codeword=bc,
+                        best_message=BitVector(int(code.k), dec.message_of_words(np.asarray(bc.words))),
+                        squared_ed=finals[best_k], stage="mp_wsd", traces=traces,
+                        counters=counters, near_tie=bool(h["flags"][0]))
+
+
+def two_stage_decode_batch(Y, code, stage1, params, sphere, sigma=1.0, tx_words=None,
+                           variant="auto"):
+    """Batched two_stage_decode over Y [F, N]; returns the device dict of
+    DeviceDecoder.two_stage_batch (stage, best, best_msg, best_ed, iters,
+    flags, counters)."""
+    dec = get_decoder(code, sphere)
+    return dec.two_stage_batch(Y, sigma, stage1.list_size, params.num_paths,
+                               params.max_iterations, params.activation_mode,
+                               variant=variant, tx_words=tx_words)
+
+
+def _as_candidates(entries: list) -> CandidateList:
+    lst = CandidateList.__new__(CandidateList)
+    lst.entries = entries
+    return lst

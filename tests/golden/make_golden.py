@@ -1,0 +1,136 @@
+"""Generate golden vectors by running the REFERENCE (feclab) in this container.
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+Writes tests/golden/*.npz.  The reference is imported read-only and never at
+test time; the GPU box only sees these fixtures.  Inputs are the reference
+harness's per-trial streams (simharness.py:220-222, 295-301) rounded to
+float32 -- the dtype of the accelerated path -- and the reference decodes
+float64(y32), so both sides see identical values.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.abspath(os.path.join(HERE, "..", "..")))
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import feclab.codebook as fcb  # noqa: E402
+from feclab.binlin import BitMatrix, row_reduce  # noqa: E402
+from feclab.decoders import SclStage, WsdParams, scl_decode, two_stage_decode  # noqa: E402
+from feclab.wsphere import build_sphere, load_sphere  # noqa: E402
+
+from paper_2602_08501_b200 import channel, configs  # noqa: E402
+from paper_2602_08501_b200.sphere import save_sphere  # noqa: E402
+
+
+def ref_code(name):
+    """The reference's own construction of each BASELINE config's code."""
+    if name == "cfg1":
+        from feclab.binlin import BitVector
+        return fcb.build_ca_polar_code(64, 10, fcb.CrcSpec(6, BitVector.from_support([0, 5, 6], 7)))
+    if name == "cfg2":
+        # RM(2,7) as polar: a reliability order whose 29 most reliable entries
+        # are {i : popcount(i) >= 5} (survey probe; simharness reliability_source=file:)
+        idx = np.arange(128)
+        ranked = idx[np.lexsort((idx, np.array([bin(i).count("1") for i in idx])))]
+        return fcb.build_polar_code(128, 29, fcb.ReliabilityOrder(128, ranked, "rm"))
+    if name == "cfg3":
+        return fcb.build_ca_polar_code(128, 21)
+    if name == "cfg4":
+        return fcb.build_ca_polar_code(256, 53)
+    raise KeyError(name)
+
+
+def ref_sphere(name, code, mine):
+    path = os.path.join("/tmp", f"golden_{name}.cws")
+    save_sphere(mine, path)
+    s = load_sphere(path)      # the reference's CWS1 reader validates the file
+    if name in ("cfg1", "cfg3"):
+        r = build_sphere(code, 1)
+        assert np.array_equal(r.member_words, s.member_words), name
+    return s
+
+
+def gen_two_stage(name, frames, mode=None, ebno=None, seed=0, snr_idx=0):
+    cfg = configs.CONFIGS[name]
+    code = ref_code(name)
+    mine_code = cfg.code()
+    assert np.array_equal(np.asarray(code.generator.words), np.asarray(mine_code.generator.words)) \
+        or name == "cfg2"
+    if name == "cfg2":
+        a = row_reduce(BitMatrix(29, 128, np.asarray(mine_code.generator.words)))[0].words
+        b = row_reduce(code.generator)[0].words
+        assert np.array_equal(a, b)
+    sph = ref_sphere(name, code, configs.build_sphere_for(cfg, mine_code))
+    mode = mode or cfg.activation_mode
+    e = cfg.ebno_db[0] if ebno is None else ebno
+    sigma = channel.ebno_to_sigma(e, code.k / code.n)
+    msgs, cw, y = channel.trial_inputs(code, seed, snr_idx, range(frames), sigma)
+    y32 = y.astype(np.float32)
+    params = WsdParams(radius_index=sph.radius_index, max_iterations=cfg.max_iterations,
+                       num_paths=cfg.num_paths, activation_mode=mode)
+    A = cfg.num_paths
+    W = cw.shape[1]
+    out = dict(y32=y32, tx=cw, msgs=msgs, sigma=np.float64(sigma),
+               stage=np.zeros(frames, np.uint8), best=np.zeros((frames, W), np.uint64),
+               best_msg=np.zeros((frames, code.k), np.uint8),
+               squared_ed=np.zeros(frames), iters=np.zeros((frames, A), np.int32),
+               n_anchor=np.zeros(frames, np.int32), anchors=np.zeros((frames, A, W), np.uint64),
+               list_size=np.int32(cfg.list_size), num_paths=np.int32(A),
+               max_iterations=np.int32(cfg.max_iterations), gated=np.int32(mode == "crc_gated"),
+               sphere_sha256=np.bytes_(configs.sphere_digest(sph)))
+    t0 = time.time()
+    for f in range(frames):
+        r = two_stage_decode(y32[f].astype(np.float64), code, SclStage(cfg.list_size), params, sph,
+                             sigma=sigma)
+        out["stage"][f] = 0 if r.stage == "stage1_crc_pass" else 1
+        out["best"][f] = r.best_codeword.words
+        out["best_msg"][f] = r.best_message.bits()
+        out["squared_ed"][f] = r.squared_ed
+        for k, tr in enumerate(r.traces):
+            out["iters"][f, k] = tr.iterations_used
+            out["anchors"][f, k] = tr.centers[0].words
+        out["n_anchor"][f] = len(r.traces)
+    tag = f"{name}_{mode}_{str(e).replace('.', 'p')}dB"
+    np.savez_compressed(os.path.join(HERE, f"two_stage_{tag}.npz"), **out)
+    print(f"{tag}: {frames} frames, p_act={out['stage'].mean():.3f}, {time.time() - t0:.1f}s")
+
+
+def gen_scl(name, frames, seed=7):
+    cfg = configs.CONFIGS[name]
+    code = ref_code(name)
+    inner = code.inner if code.kind == "crc_concatenated" else code
+    sigma = cfg.sigma(code=code)
+    _, _, y = channel.trial_inputs(code, seed, 0, range(frames), sigma)
+    llrs = 2.0 * y.astype(np.float32).astype(np.float64) / (sigma * sigma)
+    L = cfg.list_size
+    W = (code.n + 63) // 64
+    cw = np.zeros((frames, L, W), np.uint64)
+    pm = np.full((frames, L), np.nan)
+    cnt = np.zeros(frames, np.int32)
+    for f in range(frames):
+        lst = scl_decode(llrs[f], inner, L)
+        cnt[f] = len(lst)
+        for i, (c, s) in enumerate(lst.entries):
+            cw[f, i] = c.words
+            pm[f, i] = s
+    np.savez_compressed(os.path.join(HERE, f"scl_{name}.npz"), llrs=llrs, list_n=cnt, list_cw=cw,
+                        list_pm=pm, list_size=np.int32(L), info_set=np.asarray(inner.info_set, np.int32))
+    print(f"scl_{name}: {frames} frames")
+
+
+if __name__ == "__main__":
+    for nm, fr in (("cfg1", 64), ("cfg2", 16), ("cfg3", 32), ("cfg4", 8)):
+        gen_scl(nm, fr)
+    gen_two_stage("cfg1", 400)
+    gen_two_stage("cfg1", 160, mode="always_on")
+    gen_two_stage("cfg3", 200, ebno=1.0)
+    gen_two_stage("cfg2", 100)
+    gen_two_stage("cfg4", 24)

@@ -1,0 +1,345 @@
+"""Benchmark of the MP-WSD two-stage hot path on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE config 4, the stage-2-forced throughput stress): CA-polar
+(256,64) = 53 message bits + CRC-11, 5G frozen set, SCL L=16 -> A=16
+projected anchors, T=8 hops over P = 62,434 subcode codewords of weight <= 56,
+BPSK/AWGN at Eb/N0 = 1.5 dB, float32 received words.  One step = one batch of
+`--frames` frames through stage 1 + stage 2 + finalize on one GPU; frames are
+sharded by range over ranks (weak scaling, no data-path collective; the
+counters are summed with one NCCL all-reduce at the end).
+
+value   = frames decoded by all ranks / max-over-ranks device time of K steps,
+          inputs resident in HBM (each step's input is larger than L2).
+e2e     = the same metric through mpw_two_stage_batch_host (host float32 y in,
+          host codewords/messages/stages/counters out, copies timed).
+roofline: the stage-2 hop kernel; algorithmic work per launch = evaluations E
+          (= |P| x executed scans) x the per-eval cost stated in DESIGN.md.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "decoded frames/s at 1/2/4/8 B200 (stage-2 forced); pattern-metric evals/s vs roofline"
+UNIT = "frames/s"
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+            "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._proc = None
+
+    def start(self):
+        try:
+            self._proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except OSError:
+            self._proc = None
+
+    def _read(self):
+        for line in self._proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self._proc:
+            self._proc.terminate()
+            try:
+                self._proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self._proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[4 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def _dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_oracle_rate(cfg, code, sph, sigma, y, seconds: float, threads: int):
+    """Oracle (plain-C float64 restatement of the reference) on a bounded
+    prefix of the same workload.  Returns (frames/s, frames, seconds)."""
+    from oracle import oracle as orc
+    A, T, L = cfg.num_paths, cfg.max_iterations, cfg.list_size
+    gated = cfg.activation_mode == "crc_gated"
+    n = min(len(y), max(threads, 16))
+    t0 = time.perf_counter()
+    orc.two_stage_batch(y[:n], code, sph, L, A, T, gated, sigma, nthreads=threads)
+    dt = time.perf_counter() - t0
+    per = dt / n
+    n2 = int(min(len(y), max(n, seconds / max(per, 1e-9))))
+    t0 = time.perf_counter()
+    orc.two_stage_batch(y[:n2], code, sph, L, A, T, gated, sigma, nthreads=threads)
+    dt = time.perf_counter() - t0
+    return n2 / dt, n2, dt
+
+
+def run_reference(args, cfg, code, sph, sigma):
+    """--impl reference: the reference algorithm's CPU implementation (the oracle
+    port, all host threads), same config/metric, each step a bounded sample."""
+    ws, rank, _ = _dist_env()
+    if rank != 0:
+        return
+    from paper_2602_08501_b200 import channel
+    threads = os.cpu_count() or 1
+    _, _, y = channel.bulk_inputs(code, args.seed, 0, 0, max(4096, threads * 64), sigma)
+    rates = []
+    total_fr = 0
+    total_t = 0.0
+    for s in range(args.warmup + args.steps):
+        r, fr, dt = cpu_oracle_rate(cfg, code, sph, sigma, y, args.ref_step_seconds, threads)
+        if s >= args.warmup:
+            rates.append(r)
+            total_fr += fr
+            total_t += dt
+    value = total_fr / total_t
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000.0 * total_t / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": _config(args, cfg, code, sph),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": f"{total_fr // args.steps} frames per step (bounded prefix of "
+                                       f"the cfg4 workload), oracle/oracle.c float64, {threads} threads"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def _config(args, cfg, code, sph):
+    return {"workload": f"{cfg.name}: CA-polar({code.n},{code.inner.k}) K={code.k}+CRC11, SCL L={cfg.list_size}, "
+                        f"A={cfg.num_paths}, T={cfg.max_iterations}, |P|={sph.nonzero_size} "
+                        f"(w<=56, wbar={sph.mean_nonzero_weight:.2f}), Eb/N0={cfg.ebno_db[0]} dB, stage 2 forced",
+            "frames_per_step_per_gpu": args.frames, "hop_variant": args.variant,
+            "l2": "inputs larger than L2 (frames x 256 x 4 B per step, two alternating batches)",
+            "parallelism": f"frame-range shards x{_dist_env()[0]}"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg4")
+    ap.add_argument("--frames", type=int, default=1 << 17)
+    ap.add_argument("--variant", default="auto", choices=["auto", "gather", "tensor"])
+    ap.add_argument("--seed", type=int, default=2026)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--ref-step-seconds", type=float, default=10.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+
+    from paper_2602_08501_b200 import channel, configs
+    cfg = configs.CONFIGS[args.config]
+    code = cfg.code()
+    sph = configs.build_sphere_for(cfg, code)
+    sigma = cfg.sigma(code=code)
+
+    if args.impl == "reference":
+        run_reference(args, cfg, code, sph, sigma)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2602_08501_b200.decoders import DeviceDecoder, words64_to_32
+
+    ws, rank, local = _dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    F = args.frames
+    nb = 2
+    # rank r decodes frames [r*nb*F, (r+1)*nb*F) of the block-keyed stream
+    first = rank * nb * F
+    _, tx, y = channel.bulk_inputs(code, args.seed, 0, first, nb * F, sigma)
+    y_dev = [torch.from_numpy(y[i * F:(i + 1) * F]).to(dev) for i in range(nb)]
+    tx_dev = [torch.from_numpy(words64_to_32(tx[i * F:(i + 1) * F], code.n).view(np.int32)).to(dev)
+              for i in range(nb)]
+    dec = DeviceDecoder(code, sph, device=dev)
+    A, T, L = cfg.num_paths, cfg.max_iterations, cfg.list_size
+    outs = [dec.alloc_outputs(F, A, T) for _ in range(nb)]
+    counters = torch.zeros(8, dtype=torch.int64, device=dev)
+
+    def step(i):
+        dec.two_stage_batch(y_dev[i % nb], sigma, L, A, T, cfg.activation_mode, variant=args.variant,
+                            tx_words=tx_dev[i % nb], counters=counters, out=outs[i % nb])
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    counters.zero_()
+    dec.set_timing(True)
+    dec.read_timing(reset=True)
+    clocks = ClockSampler(local)
+    clocks.start()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(args.steps):
+        step(i)
+    e1.record()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    clocks.stop()
+    ms = e0.elapsed_time(e1)
+    kms, klaunch = dec.read_timing(reset=True)
+    dec.set_timing(False)
+    ctr = counters.clone()
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(ctr, op=dist.ReduceOp.SUM)
+    ms_max = float(t.item())
+    ctr = ctr.cpu().numpy()
+    frames_all = F * args.steps * ws
+    value = frames_all / (ms_max / 1000.0)
+
+    # ---- end to end through the host-buffer C-ABI call
+    e2e = None
+    if not args.no_e2e:
+        import ctypes
+        from paper_2602_08501_b200 import _native
+        lib = _native.lib()
+        y_host = [torch.from_numpy(y[i * F:(i + 1) * F]).pin_memory() for i in range(nb)]
+        tx_host = [torch.from_numpy(words64_to_32(tx[i * F:(i + 1) * F], code.n).view(np.int32)).pin_memory()
+                   for i in range(nb)]
+        nw = max(1, code.n // 32)
+        best_h = torch.empty((F, nw), dtype=torch.int32).pin_memory()
+        msg_h = torch.empty((F,), dtype=torch.int64).pin_memory()
+        stage_h = torch.empty((F,), dtype=torch.uint8).pin_memory()
+        ctr_h = torch.zeros((8,), dtype=torch.int64).pin_memory()
+        mode = _native.MODE_CRC_GATED if cfg.activation_mode == "crc_gated" else _native.MODE_ALWAYS_ON
+        var = {"auto": 0, "gather": 1, "tensor": 2}[args.variant]
+        stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+        def host_step(i):
+            rc = lib.mpw_two_stage_batch_host(
+                dec._h, ctypes.c_void_p(y_host[i % nb].data_ptr()), F, sigma, L, A, T, mode, var,
+                ctypes.c_void_p(tx_host[i % nb].data_ptr()), ctypes.c_void_p(best_h.data_ptr()),
+                ctypes.c_void_p(msg_h.data_ptr()), None, ctypes.c_void_p(stage_h.data_ptr()), None, None,
+                ctypes.c_void_p(ctr_h.data_ptr()), stream)
+            _native.check(rc, "mpw_two_stage_batch_host")
+
+        host_step(0)
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for i in range(args.steps):
+            host_step(i)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        tw = torch.tensor([wall], dtype=torch.float64, device=dev)
+        if ws > 1:
+            dist.all_reduce(tw, op=dist.ReduceOp.MAX)
+        e2e = {"value": frames_all / float(tw.item()), "unit": UNIT,
+               "h2d_bytes_per_step": int(F * code.n * 4 + F * nw * 4),
+               "d2h_bytes_per_step": int(F * nw * 4 + F * 8 + F + 8 * 8),
+               "path": "mpw_two_stage_batch_host (pinned host y/tx in; codewords, messages, stages, counters out)"}
+
+    if rank == 0:
+        peaks, peak_kind = _peaks()
+        evals = int(ctr[4])
+        hop_ms = float(kms[1])
+        variant_used = "tensor" if (args.variant == "tensor" or (args.variant == "auto" and dec.tensor_path_ready)) else "gather"
+        if variant_used == "tensor":
+            flop = evals / ws * 4.0 * code.n          # 2 limbs x 2N per evaluation
+            ach = flop / (hop_ms / 1000.0) / 1e12
+            peak = peaks["bf16_tflops"]
+            roof = {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+                    "frac": ach / peak, "traffic": None, "kernel": "hop_tc_kernel",
+                    "peak_source": f"{peak_kind} bf16_tflops (burst)"}
+        else:
+            wbar = float(sph.mean_nonzero_weight)
+            byt = evals / ws * 4.0 * wbar                # smem bytes of the gather per evaluation
+            ach = byt / (hop_ms / 1000.0) / 1e9
+            peak = 128.0 * 148 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e9
+            roof = {"bound": "smem", "achieved": ach, "peak": peak, "unit": "GB/s",
+                    "frac": ach / peak, "traffic": None, "kernel": "hop_gather_kernel",
+                    "peak_source": "theoretical shared-memory bandwidth 128 B/clk/SM x 148 SMs x max SM clock"}
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None,
+                "dtype": "f64 (stage 1) / f32 (stage 2 hop)" if variant_used == "gather"
+                         else "f64 (stage 1) / f16x2-limb f32-accum (stage 2 hop)",
+                "data": "synthetic (seeded block-keyed Philox AWGN, host-generated)",
+                "config": _config(args, cfg, code, sph),
+                "evals_per_s": evals / (ms_max / 1000.0),
+                "kernel_ms_per_step": {"stage1_scl": kms[0] / args.steps, "stage2_hop": kms[1] / args.steps,
+                                       "finalize": kms[2] / args.steps, "frame_epilogue": kms[3] / args.steps},
+                "roofline": roof,
+                "fer": float(ctr[1]) / max(1, int(ctr[0])), "p_act": float(ctr[2]) / max(1, int(ctr[0])),
+                "avg_iters": float(ctr[3]) / max(1, int(ctr[2]) * A),
+                "near_tie_frames": int(ctr[5]),
+                "clocks": clocks.summary(),
+                "gpu_launches": int(4 * args.steps),
+                "e2e": e2e}
+        if not args.no_cpu:
+            threads = os.cpu_count() or 1
+            r, fr, dt = cpu_oracle_rate(cfg, code, sph, sigma, y, args.cpu_seconds, threads)
+            line["cpu_baseline"] = {"value": r, "unit": UNIT, "cores": threads, "kind": "port",
+                                    "sample": f"first {fr} frames of the same workload, {dt:.1f}s, oracle/oracle.c "
+                                              f"(float64 restatement of feclab two_stage_decode), {threads} threads"}
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,13 +1,464 @@
-// Stage 2, tensor-core variant (tcgen05) -- placeholder until the kernel lands.
+// Stage 2, tensor-core variant: MP-WSD hop as a tcgen05 contraction.
+//
+// For a tile of M = 128 trajectory rows and all patterns p of P:
+//     S[r, p] = Σ_i t[r, i] · P[p, i],   t = x ⊙ y,   ΔED = 4 S
+// (decoders.py:329-336, 353-357).  P is exact fp16 0/1 (B operand, K-major);
+// t is split t = t_hi + t_lo into two fp16 limbs (A operand, K-major) so the
+// fp32 TMEM accumulator carries ~22 significant bits of t.  The epilogue keeps
+// per row the running argmin (ties -> lowest pattern index, decoders.py:391)
+// and the runner-up, and after a full scan of P applies the best move if it
+// strictly improves (decoders.py:395-398), then refills finished rows from the
+// stage-2 work queue (active-trajectory compaction).
+//
+// CTA = 6 warps, persistent (one CTA per SM):
+//   warp 0      producer: cp.async.bulk (TMA engine) of 32 KB pre-swizzled P
+//               tile images into a STAGES-deep mbarrier ring
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 2..5  epilogue: tcgen05.ld of the fp32 tile, argmin, moves, refills
+// TMEM: 2 accumulators x 256 fp32 columns (double buffer, 512 columns).
+// Shared memory: A_hi/A_lo [KB][128 rows x 64 fp16] SWIZZLE_128B, B ring.
 #pragma once
+#include <cuda_fp16.h>
+
+#include <vector>
+
 #include "common.cuh"
+
+namespace tc {
+
+constexpr int ROWS = 128;        // UMMA M
+constexpr int NT_COLS = 256;     // UMMA N (patterns per tile)
+constexpr int KBLK = 64;         // fp16 elements per 128-byte swizzle row
+constexpr int B_STAGE_BYTES = NT_COLS * KBLK * 2;    // 32 KB
+constexpr int A_KBLK_BYTES = ROWS * KBLK * 2;        // 16 KB
+constexpr int THREADS = 192;
+constexpr int EPI_THREADS = 128;
+
+__host__ __device__ constexpr int stages_for(int kb) { return kb >= 4 ? 3 : 4; }
+
+__host__ __device__ constexpr size_t smem_bytes(int kb) {
+    return 1024 /*align slack*/ + (size_t)2 * kb * A_KBLK_BYTES + (size_t)stages_for(kb) * B_STAGE_BYTES + 256;
+}
+
+// ---------------------------------------------------------------------------
+// PTX wrappers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(bar), "r"(parity)
+            : "memory");
+    } while (!ok);
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void tc_mma_f16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                           uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void epi_bar_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+__device__ __forceinline__ int epi_bar_or(int pred) {
+    int r;
+    asm volatile(
+        "{\n\t.reg .pred p, q;\n\t"
+        "setp.ne.s32 p, %1, 0;\n\t"
+        "bar.red.or.pred q, 2, 128, p;\n\t"
+        "selp.s32 %0, 1, 0, q;\n\t}"
+        : "=r"(r)
+        : "r"(pred)
+        : "memory");
+    return r;
+}
+
+#define TC_LD32(taddr, v)                                                                                   \
+    asm volatile(                                                                                           \
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"     \
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                           \
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),   \
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),          \
+          "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),        \
+          "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),        \
+          "=r"(v[29]), "=r"(v[30]), "=r"(v[31])                                                             \
+        : "r"(taddr))
+
+// K-major SWIZZLE_128B smem descriptor (sm100 format: version 1 at bit 46,
+// layout type 2 at bits 61-63, SBO = 1024 B between 8-row groups).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t addr) {
+    return (uint64_t)((addr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+           ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+
+// byte offset of fp16 element (row, col) inside one [rows x 64] SW128 K-block
+__host__ __device__ __forceinline__ uint32_t sw128_off(int row, int col) {
+    return (uint32_t)(row * 128 + ((((col >> 3) ^ (row & 7)) & 7) << 4) + ((col & 7) << 1));
+}
+
+struct Params {
+    int n, nw, A, T, np, ntiles;
+    const float* y;
+    S2Dev s2;
+    const uint32_t* pbits;       // np x nw
+    const uint8_t* btiles;       // [ntiles][KB][256 x 64 fp16] swizzled images
+    float tie_rel;
+};
+
+// ---------------------------------------------------------------------------
+template <int KB, int NW>
+__global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
+    constexpr int STAGES = stages_for(KB);
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* sm = reinterpret_cast<unsigned char*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    unsigned char* a_hi = sm;
+    unsigned char* a_lo = sm + KB * A_KBLK_BYTES;
+    unsigned char* b_ring = sm + 2 * KB * A_KBLK_BYTES;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(b_ring + STAGES * B_STAGE_BYTES);
+    // barriers: full[STAGES], empty[STAGES], tfull[2], tempty[2], go
+    uint64_t* full = bars;
+    uint64_t* empty = bars + STAGES;
+    uint64_t* tfull = bars + 2 * STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint64_t* go = tempty + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(go + 1);
+    volatile int* done_flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n = prm.n, nw = prm.nw, A = prm.A, T = prm.T, np_ = prm.np, ntiles = prm.ntiles;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; s++) { mbar_init(smem_u32(&full[s]), 1); mbar_init(smem_u32(&empty[s]), 1); }
+        for (int b = 0; b < 2; b++) { mbar_init(smem_u32(&tfull[b]), 1); mbar_init(smem_u32(&tempty[b]), 4); }
+        mbar_init(smem_u32(go), 1);
+        *done_flag = 0;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ===== producer =====
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (uint32_t round = 0;; round++) {
+                mbar_wait(smem_u32(go), round & 1);
+                if (*done_flag) break;
+                for (int j = 0; j < ntiles; j++) {
+                    for (int kb = 0; kb < KB; kb++) {
+                        mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+                        const uint32_t fb = smem_u32(&full[stage]);
+                        mbar_expect_tx(fb, B_STAGE_BYTES);
+                        bulk_g2s(smem_u32(b_ring + stage * B_STAGE_BYTES),
+                                 prm.btiles + ((size_t)j * KB + kb) * B_STAGE_BYTES, B_STAGE_BYTES, fb);
+                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===== MMA issuer =====
+        if (lane == 0) {
+            const uint32_t idesc = (1u << 4) | ((uint32_t)(NT_COLS >> 3) << 17) | ((uint32_t)(ROWS >> 4) << 24);
+            int stage = 0;
+            uint32_t phase = 0;
+            uint32_t gtile = 0;
+            const uint32_t ahi = smem_u32(a_hi), alo = smem_u32(a_lo), bring = smem_u32(b_ring);
+            for (uint32_t round = 0;; round++) {
+                mbar_wait(smem_u32(go), round & 1);
+                if (*done_flag) break;
+                tc_fence_after();
+                for (int j = 0; j < ntiles; j++, gtile++) {
+                    const uint32_t buf = gtile & 1;
+                    mbar_wait(smem_u32(&tempty[buf]), ((gtile >> 1) & 1) ^ 1);
+                    tc_fence_after();
+                    const uint32_t d = tmem_base + buf * NT_COLS;
+                    for (int kb = 0; kb < KB; kb++) {
+                        mbar_wait(smem_u32(&full[stage]), phase);
+                        tc_fence_after();
+                        const uint64_t bd = sw128_desc(bring + stage * B_STAGE_BYTES);
+                        const uint64_t ah = sw128_desc(ahi + kb * A_KBLK_BYTES);
+                        const uint64_t al = sw128_desc(alo + kb * A_KBLK_BYTES);
+#pragma unroll
+                        for (int ks = 0; ks < KBLK / 16; ks++) {
+                            // +32 bytes per 16-element K step inside the 128-byte swizzle row
+                            tc_mma_f16(d, ah + 2 * ks, bd + 2 * ks, idesc, (kb | ks) != 0);
+                            tc_mma_f16(d, al + 2 * ks, bd + 2 * ks, idesc, 1u);
+                        }
+                        tc_commit(smem_u32(&empty[stage]));
+                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                    }
+                    tc_commit(smem_u32(&tfull[buf]));
+                }
+            }
+        }
+    } else {
+        // ===== epilogue: one trajectory row per thread =====
+        const int g = warp & 3;                  // TMEM lane quarter accessible to this warp
+        const int row = g * 32 + lane;
+        const uint32_t t_lane = tmem_base + ((uint32_t)(g * 32) << 16);
+        const int count = *prm.s2.count;
+        const long long ntraj = (long long)count * A;
+        uint32_t c[NW];
+        long long tr = -1;
+        int iters = 0, frame = 0;
+        float ed = 0.f;
+        uint8_t flags = 0;
+        bool active = false;
+
+        auto load_row = [&]() {
+            // fetch the next valid trajectory of the stage-2 queue
+            active = false;
+            for (;;) {
+                const long long cand = (long long)atomicAdd(prm.s2.work_next, 1);
+                if (cand >= ntraj) break;
+                const int q = (int)(cand / A), a = (int)(cand % A);
+                if (a >= prm.s2.nanchor[q]) continue;
+                tr = cand;
+                frame = prm.s2.frame[q];
+                active = true;
+                break;
+            }
+            if (!active) return;
+#pragma unroll
+            for (int w = 0; w < NW; w++) c[w] = (w < nw) ? prm.s2.anchors[(size_t)tr * nw + w] : 0u;
+            iters = 0;
+            flags = 0;
+            ed = 0.f;
+            const float* yr = prm.y + (size_t)frame * n;
+#pragma unroll
+            for (int w = 0; w < NW; w++)
+#pragma unroll 1
+            for (int qq = 0; qq < 4; qq++) {
+                const int c8 = w * 4 + qq;
+                const float4 y0 = *reinterpret_cast<const float4*>(yr + c8 * 8);
+                const float4 y1 = *reinterpret_cast<const float4*>(yr + c8 * 8 + 4);
+                const float yy[8] = {y0.x, y0.y, y0.z, y0.w, y1.x, y1.y, y1.z, y1.w};
+                const uint32_t cw = c[w];
+                uint32_t hi[4], lo[4];
+#pragma unroll
+                for (int e = 0; e < 8; e += 2) {
+                    const int i0 = c8 * 8 + e;
+                    const float x0 = ((cw >> (i0 & 31)) & 1u) ? -1.f : 1.f;
+                    const float x1 = ((cw >> ((i0 + 1) & 31)) & 1u) ? -1.f : 1.f;
+                    const float t0 = x0 * yy[e], t1 = x1 * yy[e + 1];
+                    const __half h0 = __float2half_rn(t0), h1 = __float2half_rn(t1);
+                    const __half l0 = __float2half_rn(t0 - __half2float(h0));
+                    const __half l1 = __float2half_rn(t1 - __half2float(h1));
+                    hi[e / 2] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
+                    lo[e / 2] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
+                    const float d0 = yy[e] - x0, d1 = yy[e + 1] - x1;
+                    ed = fmaf(d0, d0, ed);
+                    ed = fmaf(d1, d1, ed);
+                }
+                const int kb = c8 >> 3, col = (c8 & 7) * 8;
+                const uint32_t off = kb * A_KBLK_BYTES + sw128_off(row, col);
+                *reinterpret_cast<uint4*>(a_hi + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+                *reinterpret_cast<uint4*>(a_lo + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+            }
+        };
+        auto store_row = [&]() {
+#pragma unroll
+            for (int w = 0; w < NW; w++) if (w < nw) prm.s2.traj_cw[(size_t)tr * nw + w] = c[w];
+            prm.s2.traj_iters[tr] = iters;
+            prm.s2.traj_flags[tr] = flags;
+        };
+
+        load_row();
+        fence_proxy_async();
+        int any = epi_bar_or(active);
+        if (row == 0) {
+            *done_flag = any ? 0 : 1;
+            mbar_arrive(smem_u32(go));
+        }
+        uint32_t gtile = 0;
+        while (any) {
+            float b1 = CUDART_INF_F, b2 = CUDART_INF_F;
+            int i1 = 0;
+            for (int j = 0; j < ntiles; j++, gtile++) {
+                const uint32_t buf = gtile & 1;
+                mbar_wait(smem_u32(&tfull[buf]), (gtile >> 1) & 1);
+                tc_fence_after();
+                const int pbase = j * NT_COLS;
+                const bool tail = pbase + NT_COLS > np_;
+#pragma unroll 1
+                for (int ch = 0; ch < NT_COLS / 32; ch++) {
+                    uint32_t v[32];
+                    TC_LD32(t_lane + buf * NT_COLS + ch * 32, v);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    const int p0 = pbase + ch * 32;
+                    if (tail) {
+#pragma unroll
+                        for (int e = 0; e < 32; e++)
+                            if (p0 + e >= np_) v[e] = __float_as_uint(CUDART_INF_F);
+                    }
+                    // fast path: chunk minimum by a tree; exact scan only if it can
+                    // change the best or the runner-up
+                    float m[16];
+#pragma unroll
+                    for (int e = 0; e < 16; e++) m[e] = fminf(__uint_as_float(v[e]), __uint_as_float(v[e + 16]));
+#pragma unroll
+                    for (int e = 0; e < 8; e++) m[e] = fminf(m[e], m[e + 8]);
+#pragma unroll
+                    for (int e = 0; e < 4; e++) m[e] = fminf(m[e], m[e + 4]);
+                    const float mn = fminf(fminf(m[0], m[2]), fminf(m[1], m[3]));
+                    if (mn < b2) {
+#pragma unroll
+                        for (int e = 0; e < 32; e++) {
+                            const float s = __uint_as_float(v[e]);
+                            b2 = fminf(b2, fmaxf(b1, s));
+                            if (s < b1) { b1 = s; i1 = p0 + e; }
+                        }
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(smem_u32(&tempty[buf]));
+            }
+            // ---- end of a full scan of P: decide, move, refill
+            if (active) {
+                iters++;
+                const float thr = prm.tie_rel * ed;
+                if (4.f * (b2 - b1) < thr) flags |= 1;
+                if (fabsf(4.f * b1) < thr) flags |= 2;
+                const bool improve = b1 < 0.f;
+                if (improve) {
+                    const uint32_t* pb = prm.pbits + (size_t)i1 * nw;
+#pragma unroll
+                    for (int w = 0; w < NW; w++) {
+                        if (w >= nw) break;
+                        uint32_t bits = pb[w];
+                        c[w] ^= bits;
+                        while (bits) {
+                            const int i = w * 32 + __ffs(bits) - 1;
+                            bits &= bits - 1;
+                            const uint32_t off = (i >> 6) * A_KBLK_BYTES + sw128_off(row, i & 63);
+                            *reinterpret_cast<uint16_t*>(a_hi + off) ^= 0x8000u;
+                            *reinterpret_cast<uint16_t*>(a_lo + off) ^= 0x8000u;
+                        }
+                    }
+                    ed += 4.f * b1;
+                    if (prm.s2.traj_hops) prm.s2.traj_hops[(size_t)tr * T + iters - 1] = i1 + 1;
+                }
+                if (!improve || iters == T) {
+                    if (prm.s2.traj_hops)
+                        for (int h = iters - (improve ? 0 : 1); h < T; h++) prm.s2.traj_hops[(size_t)tr * T + h] = -1;
+                    store_row();
+                    load_row();
+                }
+            }
+            fence_proxy_async();
+            any = epi_bar_or(active);
+            if (row == 0) {
+                *done_flag = any ? 0 : 1;
+                mbar_arrive(smem_u32(go));
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+    }
+}
+
+}  // namespace tc
+
+// ---------------------------------------------------------------------------
+// host side
 
 struct TcPatterns {
     bool ready = false;
+    uint8_t* tiles = nullptr;
+    int np = 0, ntiles = 0, kb = 0;
 };
 
-inline bool tc_supported(int n, int np) { return false; }
-inline int tc_build(TcPatterns& t, const uint32_t* bits, int np, int n, int nw) { t.ready = false; return 0; }
+inline bool tc_supported(int n, int np) { return (n == 64 || n == 128 || n == 256) && np >= 1; }
+
+inline void tc_release(TcPatterns& t) {
+    if (t.tiles) cudaFree(t.tiles);
+    t.tiles = nullptr;
+    t.ready = false;
+}
+
+// P bits -> fp16 0/1 tile images [ntiles][KB][256 x 64] already in the SW128
+// shared-memory layout, so one 32 KB bulk copy fills one pipeline stage.
+inline int tc_build(TcPatterns& t, const uint32_t* bits, int np, int n, int nw) {
+    tc_release(t);
+    const int kb = n / tc::KBLK;
+    const int ntiles = (np + tc::NT_COLS - 1) / tc::NT_COLS;
+    const size_t bytes = (size_t)ntiles * kb * tc::B_STAGE_BYTES;
+    std::vector<uint16_t> img(bytes / 2, 0);
+    for (int p = 0; p < np; p++) {
+        const int j = p / tc::NT_COLS, r = p % tc::NT_COLS;
+        for (int i = 0; i < n; i++) {
+            if (!((bits[(size_t)p * nw + (i >> 5)] >> (i & 31)) & 1u)) continue;
+            const int k = i / tc::KBLK, col = i % tc::KBLK;
+            const size_t off = ((size_t)j * kb + k) * tc::B_STAGE_BYTES + tc::sw128_off(r, col);
+            img[off / 2] = 0x3C00;   // fp16 1.0
+        }
+    }
+    if (cudaMalloc(&t.tiles, bytes) != cudaSuccess) return -1;
+    if (cudaMemcpy(t.tiles, img.data(), bytes, cudaMemcpyHostToDevice) != cudaSuccess) return -1;
+    t.np = np; t.ntiles = ntiles; t.kb = kb; t.ready = true;
+    return 0;
+}
+
+template <int KB, int NW>
+inline int tc_launch_t(const TcPatterns& t, int n, int nw, int A, int T, const float* y, S2Dev s2, PatDev P,
+                       int num_sms, cudaStream_t st) {
+    tc::Params prm;
+    prm.n = n; prm.nw = nw; prm.A = A; prm.T = T; prm.np = t.np; prm.ntiles = t.ntiles;
+    prm.y = y; prm.s2 = s2; prm.pbits = P.bits; prm.btiles = t.tiles; prm.tie_rel = 1e-5f;
+    const size_t smem = tc::smem_bytes(KB);
+    if (cudaFuncSetAttribute(tc::hop_tc_kernel<KB, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return -1;
+    tc::hop_tc_kernel<KB, NW><<<num_sms, tc::THREADS, smem, st>>>(prm);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
 inline int tc_launch(const TcPatterns& t, int n, int nw, int A, int T, const float* y, S2Dev s2, PatDev P,
-                     int num_sms, cudaStream_t st) { return -1; }
-inline void tc_release(TcPatterns& t) { t.ready = false; }
+                     int num_sms, cudaStream_t st) {
+    if (!t.ready) return -1;
+    switch (n) {
+        case 64: return tc_launch_t<1, 2>(t, n, nw, A, T, y, s2, P, num_sms, st);
+        case 128: return tc_launch_t<2, 4>(t, n, nw, A, T, y, s2, P, num_sms, st);
+        case 256: return tc_launch_t<4, 8>(t, n, nw, A, T, y, s2, P, num_sms, st);
+        default: return -1;
+    }
+}

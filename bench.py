@@ -327,6 +327,7 @@ def main():
                 "fer": float(ctr[1]) / max(1, int(ctr[0])), "p_act": float(ctr[2]) / max(1, int(ctr[0])),
                 "avg_iters": float(ctr[3]) / max(1, int(ctr[2]) * A),
                 "near_tie_frames": int(ctr[5]),
+                "uncertified_frames": int(ctr[6]),
                 "clocks": clocks.summary(),
                 "gpu_launches": int(4 * args.steps),
                 "e2e": e2e}

@@ -62,13 +62,19 @@ extern "C" {
 #define MPW_CTR_ACTIVATIONS 2 /* stage == mp_wsd (simharness.py:309) */
 #define MPW_CTR_ITERATIONS 3  /* sum of iterations_used over trajectories */
 #define MPW_CTR_EVALS 4       /* pattern-metric evaluations = |P| * iterations */
-#define MPW_CTR_NEAR_TIE 5    /* frames carrying a near-tie flag */
+#define MPW_CTR_NEAR_TIE 5    /* frames carrying a near-tie report flag (bits 1|2|4) */
+#define MPW_CTR_UNRESOLVED 6  /* frames carrying MPW_FLAG_UNRESOLVED */
 #define MPW_NUM_COUNTERS 8
 
-/* per-frame flags */
-#define MPW_FLAG_TIE_ARGMIN 1 /* top-2 hop candidates within 1e-5 relative */
-#define MPW_FLAG_TIE_ACCEPT 2 /* best hop's ED change within 1e-5 relative of 0 */
-#define MPW_FLAG_TIE_FINAL 4  /* two distinct final centres within 1e-5 relative */
+/* per-frame flags.  Hop decisions are certified: fp32 (or fp16-limb tensor)
+ * scores whose top-2 gap or accept margin fall inside the error window are
+ * re-scored in float64, so bits 1|2|4 only REPORT near-ties (exact relative
+ * ED gap < 1e-5, the BASELINE north-star definition); bit 8 marks a scan in
+ * which a third candidate was also inside the window (decision not certified). */
+#define MPW_FLAG_TIE_ARGMIN 1 /* exact top-2 hop candidates within 1e-5 relative ED */
+#define MPW_FLAG_TIE_ACCEPT 2 /* exact ED change of the best hop within 1e-5 relative of 0 */
+#define MPW_FLAG_TIE_FINAL 4  /* two distinct final centres within 1e-5 relative (float64) */
+#define MPW_FLAG_UNRESOLVED 8 /* >= 3 hop candidates inside the certification window */
 
 typedef struct mpw_handle mpw_handle;
 

@@ -16,7 +16,8 @@ c_int, c_double, c_void_p, c_uint32, c_int64, c_uint64 = (
 
 MODE_CRC_GATED, MODE_ALWAYS_ON = 0, 1
 HOP_AUTO, HOP_GATHER, HOP_TENSOR = 0, 1, 2
-CTR_FRAMES, CTR_ERRORS, CTR_ACTIVATIONS, CTR_ITERATIONS, CTR_EVALS, CTR_NEAR_TIE = range(6)
+CTR_FRAMES, CTR_ERRORS, CTR_ACTIVATIONS, CTR_ITERATIONS, CTR_EVALS, CTR_NEAR_TIE, CTR_UNRESOLVED = range(7)
+FLAG_TIE_ARGMIN, FLAG_TIE_ACCEPT, FLAG_TIE_FINAL, FLAG_UNRESOLVED = 1, 2, 4, 8
 NUM_COUNTERS = 8
 
 _SIGS = {

@@ -45,6 +45,94 @@ struct S2Dev {
 
 __device__ __forceinline__ int getbit32(const uint32_t* w, int j) { return (w[j >> 5] >> (j & 31)) & 1u; }
 
+// Per-frame flags (include/mpwsd.h)
+#define MPW_F_TIE_ARGMIN 1u
+#define MPW_F_TIE_ACCEPT 2u
+#define MPW_F_TIE_FINAL 4u
+#define MPW_F_UNRESOLVED 8u
+
+// Running top-3 of a scan (values S_p, ascending; index order breaks ties
+// because patterns are visited in increasing index, decoders.py:391).
+struct Top3 {
+    float b1, b2, b3;
+    int i1, i2;
+    __device__ __forceinline__ void reset() { b1 = b2 = b3 = CUDART_INF_F; i1 = i2 = 0; }
+    __device__ __forceinline__ void push(float s, int p) {
+        if (s < b3) {
+            if (s < b2) {
+                b3 = b2;
+                if (s < b1) { b2 = b1; i2 = i1; b1 = s; i1 = p; }
+                else { b2 = s; i2 = p; }
+            } else {
+                b3 = s;
+            }
+        }
+    }
+};
+
+// Exact (float64) S_p = Σ_{i∈supp p} x_i y_i for the centre c (decoders.py:329-336).
+template <int NW>
+__device__ __forceinline__ double exact_score(const float* __restrict__ yrow, const uint32_t (&c)[NW],
+                                              const uint32_t* __restrict__ pb, int nw, int n) {
+    // y is read 32 values (8 x float4) per word, all loads issued before use,
+    // so one exact score costs ~nw L2 round trips instead of one per set bit.
+    double s = 0.0;
+
+#pragma unroll
+    for (int w = 0; w < NW; w++) {
+        if (w >= nw) break;
+        const uint32_t bits = pb[w];
+        if (!bits) continue;
+        const uint32_t cw = c[w];
+        float v[32];
+        if (n >= 32) {
+            const float4* y4 = reinterpret_cast<const float4*>(yrow + w * 32);
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+                const float4 t = y4[q];
+                v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
+            }
+        }
+#pragma unroll
+        for (int b = 0; b < 32; b++) {
+            if ((bits >> b) & 1u) {
+                const double yi = (double)(n >= 32 ? v[b] : yrow[b]);
+                s += ((cw >> b) & 1u) ? -yi : yi;
+            }
+        }
+    }
+    return s;
+}
+
+// End-of-scan decision with certification.  fp32 scores carry at most `err`
+// absolute error; any pair inside the window is re-scored in float64, so the
+// chosen pattern and the accept test match exact arithmetic unless a third
+// candidate also falls inside the window (flagged MPW_F_UNRESOLVED).
+// Near-tie report (north-star definition): exact relative gaps < tie_rel.
+template <int NW>
+__device__ __forceinline__ void certify_hop(const Top3& t, const float* __restrict__ yrow,
+                                            const uint32_t (&c)[NW], const uint32_t* __restrict__ pbits,
+                                            int nw, int n, float ed, float tie_rel, float err, int& best,
+                                            bool& improve, uint8_t& flags) {
+    const float thr = tie_rel * ed * 0.25f;          // 1e-5 relative ED gap, in S units
+    const float win = thr + 2.0f * err;
+    best = t.i1;
+    improve = t.b1 < 0.0f;
+    const bool pair = (t.b2 - t.b1) < win;
+    const bool zero = fabsf(t.b1) < win;
+    if (!pair && !zero) return;
+    double e1 = exact_score<NW>(yrow, c, pbits + (size_t)t.i1 * nw, nw, n);
+    double eb = e1;
+    if (pair) {
+        const double e2 = exact_score<NW>(yrow, c, pbits + (size_t)t.i2 * nw, nw, n);
+        if (e2 < e1 || (e2 == e1 && t.i2 < t.i1)) { best = t.i2; eb = e2; }
+        if (fabs(e2 - e1) < (double)thr) flags |= MPW_F_TIE_ARGMIN;
+        if ((t.b3 - t.b1) < win) flags |= MPW_F_UNRESOLVED;
+    }
+    improve = eb < 0.0;
+    if (fabs(eb) < (double)thr) flags |= MPW_F_TIE_ACCEPT;
+}
+
 // Polar butterfly on packed words (codebook.py:166-178): for every h, first
 // half of each 2h block ^= second half.  Bits >= n are zero so the in-word
 // steps are harmless for n < 32.

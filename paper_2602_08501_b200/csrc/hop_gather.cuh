@@ -23,6 +23,7 @@ struct HopParams {
     int sup_in_smem;       // supports + offsets cached in shared memory
     int total_sup_u4;
     float tie_rel;         // near-tie threshold (relative), 1e-5
+    float err;             // bound on |S_fp32 - S_exact| (S units)
 };
 
 __host__ __device__ inline size_t gather_warp_smem(int n) { return sizeof(float) * (size_t)(n + 1) * 32; }
@@ -78,8 +79,8 @@ __global__ void __launch_bounds__(256) hop_gather_kernel(HopParams hp) {
         uint8_t flags = 0;
         for (int h = 0; h < T; h++) {
             if (!__any_sync(MPW_FULL, active)) break;
-            float b1 = CUDART_INF_F, b2 = CUDART_INF_F;
-            int i1 = 0;
+            Top3 top;
+            top.reset();
             for (int p = 0; p < np_; p++) {
                 const int q0 = soff[p], q1 = soff[p + 1];
                 float s0 = 0.0f, s1 = 0.0f;
@@ -94,17 +95,15 @@ __global__ void __launch_bounds__(256) hop_gather_kernel(HopParams hp) {
                     s0 += t[(v.w & 0xffffu) * 32 + lane];
                     s1 += t[(v.w >> 16) * 32 + lane];
                 }
-                const float s = s0 + s1;
-                const float nb2 = fminf(b2, fmaxf(b1, s));
-                if (s < b1) { b1 = s; i1 = p; }
-                b2 = nb2;
+                top.push(s0 + s1, p);
             }
             if (active) {
                 iters++;
-                const float thr = hp.tie_rel * ed;
-                if (4.0f * (b2 - b1) < thr) flags |= 1;
-                if (fabsf(4.0f * b1) < thr) flags |= 2;
-                if (b1 < 0.0f) {
+                int i1;
+                bool improve;
+                certify_hop<NW>(top, hp.y + (size_t)f * n, c, hp.P.bits, nw, n, ed, hp.tie_rel, hp.err, i1,
+                                improve, flags);
+                if (improve) {
                     for (int qq = soff[i1]; qq < soff[i1 + 1]; qq++) {
                         const uint4 v = sup[qq];
                         const uint32_t ids[4] = {v.x, v.y, v.z, v.w};
@@ -117,7 +116,7 @@ __global__ void __launch_bounds__(256) hop_gather_kernel(HopParams hp) {
                     }
 #pragma unroll
                     for (int w = 0; w < NW; w++) if (w < nw) c[w] ^= hp.P.bits[(size_t)i1 * nw + w];
-                    ed += 4.0f * b1;
+                    ed += 4.0f * (i1 == top.i1 ? top.b1 : top.b2);
                     if (hp.s2.traj_hops) hp.s2.traj_hops[(size_t)tr * T + h] = i1 + 1;
                 } else {
                     active = false;

@@ -130,6 +130,7 @@ struct Params {
     const uint32_t* pbits;       // np x nw
     const uint8_t* btiles;       // [ntiles][KB][256 x 64 fp16] swizzled images
     float tie_rel;
+    float err;             // bound on |S_fp32 - S_exact| (S units)
 };
 
 // ---------------------------------------------------------------------------
@@ -307,8 +308,8 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
         }
         uint32_t gtile = 0;
         while (any) {
-            float b1 = CUDART_INF_F, b2 = CUDART_INF_F;
-            int i1 = 0;
+            Top3 top;
+            top.reset();
             for (int j = 0; j < ntiles; j++, gtile++) {
                 const uint32_t buf = gtile & 1;
                 mbar_wait(smem_u32(&tfull[buf]), (gtile >> 1) & 1);
@@ -336,13 +337,9 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
 #pragma unroll
                     for (int e = 0; e < 4; e++) m[e] = fminf(m[e], m[e + 4]);
                     const float mn = fminf(fminf(m[0], m[2]), fminf(m[1], m[3]));
-                    if (mn < b2) {
+                    if (mn < top.b3) {
 #pragma unroll
-                        for (int e = 0; e < 32; e++) {
-                            const float s = __uint_as_float(v[e]);
-                            b2 = fminf(b2, fmaxf(b1, s));
-                            if (s < b1) { b1 = s; i1 = p0 + e; }
-                        }
+                        for (int e = 0; e < 32; e++) top.push(__uint_as_float(v[e]), p0 + e);
                     }
                 }
                 tc_fence_before();
@@ -352,10 +349,10 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
             // ---- end of a full scan of P: decide, move, refill
             if (active) {
                 iters++;
-                const float thr = prm.tie_rel * ed;
-                if (4.f * (b2 - b1) < thr) flags |= 1;
-                if (fabsf(4.f * b1) < thr) flags |= 2;
-                const bool improve = b1 < 0.f;
+                int i1;
+                bool improve;
+                certify_hop<NW>(top, prm.y + (size_t)frame * n, c, prm.pbits, nw, n, ed, prm.tie_rel,
+                                prm.err, i1, improve, flags);
                 if (improve) {
                     const uint32_t* pb = prm.pbits + (size_t)i1 * nw;
 #pragma unroll
@@ -371,7 +368,7 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
                             *reinterpret_cast<uint16_t*>(a_lo + off) ^= 0x8000u;
                         }
                     }
-                    ed += 4.f * b1;
+                    ed += 4.f * (i1 == top.i1 ? top.b1 : top.b2);
                     if (prm.s2.traj_hops) prm.s2.traj_hops[(size_t)tr * T + iters - 1] = i1 + 1;
                 }
                 if (!improve || iters == T) {
@@ -445,6 +442,7 @@ inline int tc_launch_t(const TcPatterns& t, int n, int nw, int A, int T, const f
     tc::Params prm;
     prm.n = n; prm.nw = nw; prm.A = A; prm.T = T; prm.np = t.np; prm.ntiles = t.ntiles;
     prm.y = y; prm.s2 = s2; prm.pbits = P.bits; prm.btiles = t.tiles; prm.tie_rel = 1e-5f;
+    prm.err = 2e-3f;
     const size_t smem = tc::smem_bytes(KB);
     if (cudaFuncSetAttribute(tc::hop_tc_kernel<KB, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return -1;

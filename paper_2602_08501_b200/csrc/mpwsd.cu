@@ -195,7 +195,7 @@ struct FrameArgs {
 
 __global__ void frame_kernel(FrameArgs fa) {
     const int f = blockIdx.x * blockDim.x + threadIdx.x;
-    unsigned long long c_err = 0, c_act = 0, c_it = 0, c_tie = 0, c_fr = 0;
+    unsigned long long c_err = 0, c_act = 0, c_it = 0, c_tie = 0, c_fr = 0, c_unr = 0;
     if (f < fa.F) {
         const uint32_t* b = fa.best + (size_t)f * fa.nw;
         if (fa.msg_out && fa.k <= 64) {
@@ -216,7 +216,8 @@ __global__ void frame_kernel(FrameArgs fa) {
         }
         c_fr = 1;
         c_act = s2 ? 1 : 0;
-        c_tie = (fa.flags && fa.flags[f]) ? 1 : 0;
+        c_tie = (fa.flags && (fa.flags[f] & 7u)) ? 1 : 0;
+        c_unr = (fa.flags && (fa.flags[f] & 8u)) ? 1 : 0;
         if (fa.tx) {
             bool diff = false;
             for (int w = 0; w < fa.nw; w++) diff |= b[w] != fa.tx[(size_t)f * fa.nw + w];
@@ -231,6 +232,7 @@ __global__ void frame_kernel(FrameArgs fa) {
             c_act += __shfl_xor_sync(MPW_FULL, c_act, o);
             c_it += __shfl_xor_sync(MPW_FULL, c_it, o);
             c_tie += __shfl_xor_sync(MPW_FULL, c_tie, o);
+            c_unr += __shfl_xor_sync(MPW_FULL, c_unr, o);
         }
         if ((threadIdx.x & 31) == 0 && c_fr) {
             atomicAdd(&fa.counters[MPW_CTR_FRAMES], c_fr);
@@ -239,6 +241,7 @@ __global__ void frame_kernel(FrameArgs fa) {
             atomicAdd(&fa.counters[MPW_CTR_ITERATIONS], c_it);
             atomicAdd(&fa.counters[MPW_CTR_EVALS], c_it * (unsigned long long)fa.np);
             atomicAdd(&fa.counters[MPW_CTR_NEAR_TIE], c_tie);
+            atomicAdd(&fa.counters[MPW_CTR_UNRESOLVED], c_unr);
         }
     }
 }
@@ -355,6 +358,7 @@ int run_hops(mpw_handle* h, const float* y, int Fmax, int A, int T, int variant,
     hp.n = h->n; hp.nw = h->nw; hp.A = A; hp.T = T; hp.y = y; hp.s2 = s2; hp.P = pat_dev(h);
     hp.sup = h->sup.p; hp.soff = h->soff.p; hp.sup_in_smem = 0; hp.total_sup_u4 = h->total_sup_u4;
     hp.tie_rel = 1e-5f;
+    hp.err = 1e-3f;
     const int max_traj = Fmax * A;
     switch (h->nw) {
         case 1: return launch_gather<1>(h, hp, max_traj, st);

@@ -11,6 +11,7 @@ import pytest
 from oracle import oracle as orc
 from paper_2602_08501_b200 import configs
 from paper_2602_08501_b200.decoders import DeviceDecoder, words32_to_64, words64_to_32
+from paper_2602_08501_b200._native import FLAG_TIE_FINAL as TIE_FINAL, FLAG_UNRESOLVED as UNRESOLVED
 from tests.helpers import cfg_of, code_and_sphere, load, scl_fixtures, two_stage_fixtures
 
 pytestmark = pytest.mark.gpu
@@ -45,7 +46,7 @@ def test_scl_lists_bit_exact_vs_reference(fx):
         np.testing.assert_array_equal(pm[f, :c], g["list_pm"][f, :c])
 
 
-@pytest.mark.parametrize("variant", ["gather", "auto"])
+@pytest.mark.parametrize("variant", ["gather", "tensor"])
 @pytest.mark.parametrize("fx", two_stage_fixtures())
 def test_two_stage_vs_reference_golden(fx, variant):
     g = load(fx)
@@ -60,9 +61,9 @@ def test_two_stage_vs_reference_golden(fx, variant):
     best = words32_to_64(_np(o["best"]).view(np.uint32), n)
     flags = _np(o["flags"])
     mism = np.flatnonzero((best != g["best"]).any(axis=1))
-    assert set(mism.tolist()) <= set(np.flatnonzero(flags).tolist()), f"unflagged mismatches {mism}"
-    assert len(mism) <= max(1, len(stage) // 100)
-    ok = np.setdiff1d(np.arange(len(stage)), np.flatnonzero(flags))
+    risky = np.flatnonzero(flags & (UNRESOLVED | TIE_FINAL))
+    assert set(mism.tolist()) <= set(risky.tolist()), f"uncertified mismatches {mism}"
+    ok = np.setdiff1d(np.arange(len(stage)), risky)
     np.testing.assert_array_equal(_np(o["iters"])[ok], g["iters"][ok])
     anc = words32_to_64(_np(o["anchors"]).view(np.uint32), n)
     s2 = np.flatnonzero(stage == 1)
@@ -75,27 +76,34 @@ def test_two_stage_vs_reference_golden(fx, variant):
     np.testing.assert_array_equal(msg[ok], ref_msg[ok])
 
 
-@pytest.mark.parametrize("name", ["cfg1", "cfg3", "cfg2"])
-def test_two_stage_vs_oracle_random_frames(name):
+@pytest.mark.parametrize("variant", ["gather", "tensor"])
+@pytest.mark.parametrize("name", ["cfg1", "cfg3", "cfg2", "cfg4"])
+def test_two_stage_vs_oracle_random_frames(name, variant):
     cfg = configs.CONFIGS[name]
     code, sph = code_and_sphere(cfg)
     from paper_2602_08501_b200 import channel
     sigma = cfg.sigma(code=code)
-    F = {"cfg1": 4096, "cfg3": 2048, "cfg2": 256}[name]
+    F = {"cfg1": 4096, "cfg3": 2048, "cfg2": 256, "cfg4": 96}[name]
+    if name == "cfg4" and variant == "gather":
+        F = 32
     _, cw, y = channel.bulk_inputs(code, 11, 0, 0, F, sigma)
     o = decoder(cfg).two_stage_batch(y, sigma, cfg.list_size, cfg.num_paths, cfg.max_iterations,
-                                     cfg.activation_mode, variant="gather")
+                                     cfg.activation_mode, variant=variant)
     r = orc.two_stage_batch(y, code, sph, cfg.list_size, cfg.num_paths, cfg.max_iterations,
                             cfg.activation_mode == "crc_gated", sigma, nthreads=8)
     np.testing.assert_array_equal(_np(o["stage"]), r["stage"])
     best = words32_to_64(_np(o["best"]).view(np.uint32), code.n)
     flags = _np(o["flags"])
     mism = np.flatnonzero((best != r["best"]).any(axis=1))
-    assert set(mism.tolist()) <= set(np.flatnonzero(flags).tolist())
-    assert flags.astype(bool).mean() < 0.01
+    risky = np.flatnonzero(flags & (UNRESOLVED | TIE_FINAL))
+    assert set(mism.tolist()) <= set(risky.tolist()), f"uncertified mismatches {mism}"
+    assert len(risky) <= max(1, F // 200)
+    ok = np.setdiff1d(np.arange(F), risky)
+    np.testing.assert_array_equal(_np(o["iters"])[ok], r["iters"][ok])
 
 
-def test_mp_wsd_random_anchors_vs_oracle():
+@pytest.mark.parametrize("variant", ["gather", "tensor"])
+def test_mp_wsd_random_anchors_vs_oracle(variant):
     cfg = configs.CONFIGS["cfg1"]
     code, sph = code_and_sphere(cfg)
     rng = np.random.default_rng(5)
@@ -104,12 +112,13 @@ def test_mp_wsd_random_anchors_vs_oracle():
     msgs = rng.integers(0, 2, (F * A, code.k), dtype=np.uint8)
     anc64 = encode_batch(code, msgs).reshape(F, A, -1)
     y = rng.normal(size=(F, code.n)).astype(np.float32)
-    o = decoder(cfg).mp_wsd_batch(y, words64_to_32(anc64, code.n), T, variant="gather")
+    o = decoder(cfg).mp_wsd_batch(y, words64_to_32(anc64, code.n), T, variant=variant)
     r = orc.mpwsd_batch(y, anc64, sph, T, nthreads=8)
     best = words32_to_64(_np(o["best"]).view(np.uint32), code.n)
     flags = _np(o["flags"])
     mism = np.flatnonzero((best != r["best"]).any(axis=1))
-    assert set(mism.tolist()) <= set(np.flatnonzero(flags).tolist())
-    ok = np.flatnonzero(flags == 0)
+    risky = np.flatnonzero(flags & (UNRESOLVED | TIE_FINAL))
+    assert set(mism.tolist()) <= set(risky.tolist())
+    ok = np.setdiff1d(np.arange(F), risky)
     np.testing.assert_array_equal(_np(o["iters"])[ok], r["iters"][ok])
     np.testing.assert_array_equal(_np(o["hops"])[ok], r["hops"][ok])

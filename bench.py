@@ -201,9 +201,10 @@ def main():
 
     F = args.frames
     nb = 2
-    # rank r decodes frames [r*nb*F, (r+1)*nb*F) of the block-keyed stream
-    first = rank * nb * F
-    _, tx, y = channel.bulk_inputs(code, args.seed, 0, first, nb * F, sigma)
+    # rank r decodes its own block-aligned frame range of the block-keyed stream
+    from paper_2602_08501_b200 import shard
+    sh = shard.shard_for(rank, ws, nb * F)
+    _, tx, y = channel.bulk_inputs(code, args.seed, 0, sh.first, sh.count, sigma)
     y_dev = [torch.from_numpy(y[i * F:(i + 1) * F]).to(dev) for i in range(nb)]
     tx_dev = [torch.from_numpy(words64_to_32(tx[i * F:(i + 1) * F], code.n).view(np.int32)).to(dev)
               for i in range(nb)]

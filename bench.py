@@ -169,7 +169,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg4")
     ap.add_argument("--frames", type=int, default=1 << 17)
-    ap.add_argument("--variant", default="auto", choices=["auto", "gather", "tensor"])
+    ap.add_argument("--variant", default="auto", choices=["auto", "gather", "tensor", "tensor2"])
     ap.add_argument("--seed", type=int, default=2026)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-step-seconds", type=float, default=10.0)
@@ -266,7 +266,7 @@ def main():
         stage_h = torch.empty((F,), dtype=torch.uint8).pin_memory()
         ctr_h = torch.zeros((8,), dtype=torch.int64).pin_memory()
         mode = _native.MODE_CRC_GATED if cfg.activation_mode == "crc_gated" else _native.MODE_ALWAYS_ON
-        var = {"auto": 0, "gather": 1, "tensor": 2}[args.variant]
+        var = {"auto": 0, "gather": 1, "tensor": 2, "tensor2": 3}[args.variant]
         stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
         def host_step(i):
@@ -298,14 +298,18 @@ def main():
         peaks, peak_kind = _peaks()
         evals = int(ctr[4])
         hop_ms = float(kms[1])
-        variant_used = "tensor" if (args.variant == "tensor" or (args.variant == "auto" and dec.tensor_path_ready)) else "gather"
-        if variant_used == "tensor":
-            flop = evals / ws * 4.0 * code.n          # 2 limbs x 2N per evaluation
+        variant_used = args.variant
+        if variant_used == "auto":
+            variant_used = "tensor" if dec.tensor_path_ready else "gather"
+        if variant_used in ("tensor", "tensor2"):
+            limbs = 1 if variant_used == "tensor" else 2
+            flop = evals / ws * 2.0 * limbs * code.n  # limbs x 2N FLOP per evaluation
             ach = flop / (hop_ms / 1000.0) / 1e12
             peak = peaks["bf16_tflops"]
             roof = {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
-                    "frac": ach / peak, "traffic": None, "kernel": "hop_tc_kernel",
-                    "peak_source": f"{peak_kind} bf16_tflops (burst)"}
+                    "frac": ach / peak, "traffic": None, "kernel": f"hop_tc_kernel<LIMBS={limbs}>",
+                    "flop_per_eval": 2 * limbs * code.n,
+                    "peak_source": f"{peak_kind} bf16_tflops (burst cuBLAS 8192^3)"}
         else:
             wbar = float(sph.mean_nonzero_weight)
             byt = evals / ws * 4.0 * wbar                # smem bytes of the gather per evaluation
@@ -317,8 +321,9 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None,
-                "dtype": "f64 (stage 1) / f32 (stage 2 hop)" if variant_used == "gather"
-                         else "f64 (stage 1) / f16x2-limb f32-accum (stage 2 hop)",
+                "dtype": {"gather": "f64 (stage 1) / f32 (stage 2 hop)",
+                          "tensor": "f64 (stage 1) / f16 1-limb f32-accum screen + f64 certify (stage 2 hop)",
+                          "tensor2": "f64 (stage 1) / f16 2-limb f32-accum + f64 certify (stage 2 hop)"}[variant_used],
                 "data": "synthetic (seeded block-keyed Philox AWGN, host-generated)",
                 "config": _config(args, cfg, code, sph),
                 "evals_per_s": evals / (ms_max / 1000.0),

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <math_constants.h>
+#include <cuda_fp16.h>
 
 #define MPW_FULL 0xffffffffu
 
@@ -41,6 +42,8 @@ struct S2Dev {
     int32_t* traj_hops;    // [cap x A x T] accepted pattern index per hop (-1 = none)
     uint8_t* traj_flags;   // [cap x A] bit0 near-tie argmin, bit1 near-tie accept
     int32_t* work_next;    // [1] persistent-kernel work counter
+    float4* ebound;        // [cap] per-frame score error bounds (warp_error_bounds)
+    int wmax;              // max pattern weight of P
 };
 
 __device__ __forceinline__ int getbit32(const uint32_t* w, int j) { return (w[j >> 5] >> (j & 31)) & 1u; }
@@ -129,6 +132,139 @@ __device__ __forceinline__ void certify_hop(const Top3& t, const float* __restri
         if (fabs(e2 - e1) < (double)thr) flags |= MPW_F_TIE_ARGMIN;
         if ((t.b3 - t.b1) < win) flags |= MPW_F_UNRESOLVED;
     }
+    improve = eb < 0.0;
+    if (fabs(eb) < (double)thr) flags |= MPW_F_TIE_ACCEPT;
+}
+
+// Upper bound on the sum of the w largest of the values x[] spread over the
+// warp (lane holds x[lane + 32 j]): for any tau with #{x > tau} <= w,
+// sum_top_w <= sum_{x > tau} x + (w - #{x > tau}) * tau.  tau by bisection.
+__device__ __forceinline__ float warp_topw_bound(const float* xv, int cnt, int w) {
+    float mx = 0.0f;
+    for (int j = 0; j < cnt; j++) mx = fmaxf(mx, xv[j]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(MPW_FULL, mx, o));
+    float lo = 0.0f, hi = mx;
+    for (int it = 0; it < 12; it++) {
+        const float mid = 0.5f * (lo + hi);
+        int c = 0;
+        for (int j = 0; j < cnt; j++) c += xv[j] > mid;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(MPW_FULL, c, o);
+        if (c <= w) hi = mid; else lo = mid;
+    }
+    float s = 0.0f;
+    int c = 0;
+    for (int j = 0; j < cnt; j++) if (xv[j] > hi) { s += xv[j]; c++; }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        s += __shfl_xor_sync(MPW_FULL, s, o);
+        c += __shfl_xor_sync(MPW_FULL, c, o);
+    }
+    return (s + (float)(w - c) * hi) * 1.0001f;
+}
+
+// Per-frame score error bounds (S units) for the hop kernels, computed by one
+// warp from y: |t_i| = |y_i| and the fp16 split errors of t_i = ±y_i do not
+// depend on the sign pattern x, so one bound serves every hop of every anchor.
+//   x: 1-limb tensor (fp16(t)),  y: 2-limb tensor (fp16 hi + fp16 lo),
+//   z: fp32 gather,              w: sum of the wmax largest |y_i|.
+// Each sums the wmax largest per-element representation errors and adds
+// an fp32 accumulation bound of (terms) * 2^-23 * sum|t|.
+__device__ __forceinline__ float4 warp_error_bounds(const float* __restrict__ yrow, int n, int wmax) {
+    const int lane = threadIdx.x & 31;
+    float ay[32], e1[32], e2[32];
+    int cnt = 0;
+    for (int i = lane; i < n; i += 32, cnt++) {
+        const float y = yrow[i];
+        const float h = __half2float(__float2half_rn(y));
+        const float l = __half2float(__float2half_rn(y - h));
+        ay[cnt] = fabsf(y);
+        e1[cnt] = fabsf(y - h);
+        e2[cnt] = fabsf((y - h) - l);
+    }
+    const float A = warp_topw_bound(ay, cnt, wmax);
+    const float T1 = warp_topw_bound(e1, cnt, wmax);
+    const float T2 = warp_topw_bound(e2, cnt, wmax);
+    const float u = 1.1920929e-7f;   // 2^-23
+    return make_float4(T1 + (float)wmax * u * A, T2 + 2.0f * (float)wmax * u * A,
+                       (float)wmax * u * A, A);
+}
+
+// Running top-K (K small) of a scan; ascending values, index order breaks ties.
+template <int K>
+struct TopK {
+    float b[K];
+    int i[K];
+    __device__ __forceinline__ void reset() {
+#pragma unroll
+        for (int k = 0; k < K; k++) { b[k] = CUDART_INF_F; i[k] = 0; }
+    }
+    __device__ __forceinline__ float last() const { return b[K - 1]; }
+    __device__ __forceinline__ void push(float s, int p) {
+        if (!(s < b[K - 1])) return;
+        insert(s, p);
+    }
+    // precondition: s < b[K-1]; branch-free sorted insertion (registers only)
+    __device__ __forceinline__ void insert_inline(float s, int p) {
+#pragma unroll
+        for (int k = K - 1; k > 0; k--) {
+            const bool up = s < b[k - 1];          // s goes above slot k
+            const bool here = !up && s < b[k];     // s lands in slot k
+            const float nb = up ? b[k - 1] : (here ? s : b[k]);
+            const int ni = up ? i[k - 1] : (here ? p : i[k]);
+            b[k] = nb;
+            i[k] = ni;
+        }
+        if (s < b[0]) { b[0] = s; i[0] = p; }
+    }
+    // precondition: s < b[K-1]
+    __device__ __forceinline__ void insert(float s, int p) {
+        // insertion from the back; strict < keeps earlier indices first on ties
+#pragma unroll
+        for (int k = K - 1; k > 0; k--) {
+            if (s < b[k - 1]) { b[k] = b[k - 1]; i[k] = i[k - 1]; }
+            else { b[k] = s; i[k] = p; return; }
+        }
+        b[0] = s; i[0] = p;
+    }
+};
+
+// Certified decision from a top-K list whose scores carry at most `err_row`
+// absolute error: every candidate within 2·err (+ the report threshold) of the
+// best approximate score is re-scored in float64; the exact argmin (ties ->
+// lowest index) and the exact accept test are used.  If the K-th score is
+// also inside the window the scan is flagged MPW_F_UNRESOLVED.
+template <int K, int NW>
+__device__ __forceinline__ void certify_topk(const TopK<K>& t, const float* __restrict__ yrow,
+                                             const uint32_t (&c)[NW], const uint32_t* __restrict__ pbits,
+                                             int nw, int n, float ed, float tie_rel, float err_row, int& best,
+                                             bool& improve, float& best_approx, uint8_t& flags) {
+    const float thr = tie_rel * ed * 0.25f;
+    const float win = thr + 2.0f * err_row;
+    best = t.i[0];
+    best_approx = t.b[0];
+    improve = t.b[0] < 0.0f;
+    const bool pair = (t.b[1] - t.b[0]) < win;
+    const bool zero = fabsf(t.b[0]) < err_row + thr;
+    if (!pair && !zero) return;
+    double eb = exact_score<NW>(yrow, c, pbits + (size_t)t.i[0] * nw, nw, n);
+    double e_second = CUDART_INF;
+#pragma unroll
+    for (int k = 1; k < K - 1; k++) {
+        if (!((t.b[k] - t.b[0]) < win)) break;
+        const double e = exact_score<NW>(yrow, c, pbits + (size_t)t.i[k] * nw, nw, n);
+        if (e < eb || (e == eb && t.i[k] < best)) {
+            e_second = eb;
+            eb = e;
+            best = t.i[k];
+            best_approx = t.b[k];
+        } else if (e < e_second) {
+            e_second = e;
+        }
+    }
+    if ((t.b[K - 1] - t.b[0]) < win) flags |= MPW_F_UNRESOLVED;
+    if (e_second - eb < (double)thr) flags |= MPW_F_TIE_ARGMIN;
     improve = eb < 0.0;
     if (fabs(eb) < (double)thr) flags |= MPW_F_TIE_ACCEPT;
 }

@@ -59,6 +59,7 @@ __global__ void __launch_bounds__(256) hop_gather_kernel(HopParams hp) {
         uint32_t c[NW];
         float ed = 0.0f;
         const int f = valid ? hp.s2.frame[q] : 0;
+        const float err_row = valid ? hp.s2.ebound[q].z : 0.0f;
 #pragma unroll
         for (int w = 0; w < NW; w++) c[w] = (valid && w < nw) ? hp.s2.anchors[(size_t)tr * nw + w] : 0u;
 #pragma unroll
@@ -79,7 +80,7 @@ __global__ void __launch_bounds__(256) hop_gather_kernel(HopParams hp) {
         uint8_t flags = 0;
         for (int h = 0; h < T; h++) {
             if (!__any_sync(MPW_FULL, active)) break;
-            Top3 top;
+            TopK<4> top;
             top.reset();
             for (int p = 0; p < np_; p++) {
                 const int q0 = soff[p], q1 = soff[p + 1];
@@ -101,8 +102,9 @@ __global__ void __launch_bounds__(256) hop_gather_kernel(HopParams hp) {
                 iters++;
                 int i1;
                 bool improve;
-                certify_hop<NW>(top, hp.y + (size_t)f * n, c, hp.P.bits, nw, n, ed, hp.tie_rel, hp.err, i1,
-                                improve, flags);
+                float sb;
+                certify_topk<4, NW>(top, hp.y + (size_t)f * n, c, hp.P.bits, nw, n, ed, hp.tie_rel, err_row,
+                                    i1, improve, sb, flags);
                 if (improve) {
                     for (int qq = soff[i1]; qq < soff[i1 + 1]; qq++) {
                         const uint4 v = sup[qq];
@@ -116,7 +118,7 @@ __global__ void __launch_bounds__(256) hop_gather_kernel(HopParams hp) {
                     }
 #pragma unroll
                     for (int w = 0; w < NW; w++) if (w < nw) c[w] ^= hp.P.bits[(size_t)i1 * nw + w];
-                    ed += 4.0f * (i1 == top.i1 ? top.b1 : top.b2);
+                    ed += 4.0f * sb;
                     if (hp.s2.traj_hops) hp.s2.traj_hops[(size_t)tr * T + h] = i1 + 1;
                 } else {
                     active = false;

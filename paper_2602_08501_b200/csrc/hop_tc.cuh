@@ -34,10 +34,16 @@ constexpr int A_KBLK_BYTES = ROWS * KBLK * 2;        // 16 KB
 constexpr int THREADS = 192;
 constexpr int EPI_THREADS = 128;
 
-__host__ __device__ constexpr int stages_for(int kb) { return kb >= 4 ? 3 : 4; }
+constexpr int SMEM_LIMIT = 232448;   // 227 KB opt-in maximum per CTA
 
-__host__ __device__ constexpr size_t smem_bytes(int kb) {
-    return 1024 /*align slack*/ + (size_t)2 * kb * A_KBLK_BYTES + (size_t)stages_for(kb) * B_STAGE_BYTES + 256;
+__host__ __device__ constexpr int stages_for(int kb, int limbs) {
+    return (SMEM_LIMIT - 1024 - 256 - limbs * kb * A_KBLK_BYTES) / B_STAGE_BYTES > 6
+               ? 6
+               : (SMEM_LIMIT - 1024 - 256 - limbs * kb * A_KBLK_BYTES) / B_STAGE_BYTES;
+}
+
+__host__ __device__ constexpr size_t smem_bytes(int kb, int limbs) {
+    return 1024 /*align slack*/ + (size_t)limbs * kb * A_KBLK_BYTES + (size_t)stages_for(kb, limbs) * B_STAGE_BYTES + 256;
 }
 
 // ---------------------------------------------------------------------------
@@ -111,6 +117,20 @@ __device__ __forceinline__ int epi_bar_or(int pred) {
           "=r"(v[29]), "=r"(v[30]), "=r"(v[31])                                                             \
         : "r"(taddr))
 
+// v[e] for a runtime e without local memory: 5-level select tree (31 SEL)
+__device__ __forceinline__ float select32(const uint32_t (&v)[32], int e) {
+    uint32_t a[16];
+#pragma unroll
+    for (int k = 0; k < 16; k++) a[k] = (e & 16) ? v[k + 16] : v[k];
+#pragma unroll
+    for (int k = 0; k < 8; k++) a[k] = (e & 8) ? a[k + 8] : a[k];
+#pragma unroll
+    for (int k = 0; k < 4; k++) a[k] = (e & 4) ? a[k + 4] : a[k];
+#pragma unroll
+    for (int k = 0; k < 2; k++) a[k] = (e & 2) ? a[k + 2] : a[k];
+    return __uint_as_float((e & 1) ? a[1] : a[0]);
+}
+
 // K-major SWIZZLE_128B smem descriptor (sm100 format: version 1 at bit 46,
 // layout type 2 at bits 61-63, SBO = 1024 B between 8-row groups).
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t addr) {
@@ -134,14 +154,14 @@ struct Params {
 };
 
 // ---------------------------------------------------------------------------
-template <int KB, int NW>
+template <int KB, int NW, int LIMBS>
 __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
-    constexpr int STAGES = stages_for(KB);
+    constexpr int STAGES = stages_for(KB, LIMBS);
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* sm = reinterpret_cast<unsigned char*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     unsigned char* a_hi = sm;
-    unsigned char* a_lo = sm + KB * A_KBLK_BYTES;
-    unsigned char* b_ring = sm + 2 * KB * A_KBLK_BYTES;
+    unsigned char* a_lo = sm + KB * A_KBLK_BYTES;          // used only when LIMBS == 2
+    unsigned char* b_ring = sm + LIMBS * KB * A_KBLK_BYTES;
     uint64_t* bars = reinterpret_cast<uint64_t*>(b_ring + STAGES * B_STAGE_BYTES);
     // barriers: full[STAGES], empty[STAGES], tfull[2], tempty[2], go
     uint64_t* full = bars;
@@ -218,7 +238,7 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
                         for (int ks = 0; ks < KBLK / 16; ks++) {
                             // +32 bytes per 16-element K step inside the 128-byte swizzle row
                             tc_mma_f16(d, ah + 2 * ks, bd + 2 * ks, idesc, (kb | ks) != 0);
-                            tc_mma_f16(d, al + 2 * ks, bd + 2 * ks, idesc, 1u);
+                            if (LIMBS == 2) tc_mma_f16(d, al + 2 * ks, bd + 2 * ks, idesc, 1u);
                         }
                         tc_commit(smem_u32(&empty[stage]));
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -237,7 +257,7 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
         uint32_t c[NW];
         long long tr = -1;
         int iters = 0, frame = 0;
-        float ed = 0.f;
+        float ed = 0.f, err_row = 0.f;
         uint8_t flags = 0;
         bool active = false;
 
@@ -251,6 +271,8 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
                 if (a >= prm.s2.nanchor[q]) continue;
                 tr = cand;
                 frame = prm.s2.frame[q];
+                const float4 eb = prm.s2.ebound[q];
+                err_row = (LIMBS == 1) ? eb.x : eb.y;
                 active = true;
                 break;
             }
@@ -289,7 +311,7 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
                 const int kb = c8 >> 3, col = (c8 & 7) * 8;
                 const uint32_t off = kb * A_KBLK_BYTES + sw128_off(row, col);
                 *reinterpret_cast<uint4*>(a_hi + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-                *reinterpret_cast<uint4*>(a_lo + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+                if (LIMBS == 2) *reinterpret_cast<uint4*>(a_lo + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
             }
         };
         auto store_row = [&]() {
@@ -308,8 +330,9 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
         }
         uint32_t gtile = 0;
         while (any) {
-            Top3 top;
+            TopK<4> top;
             top.reset();
+            float lastv = CUDART_INF_F;   // register copy of top.last()
             for (int j = 0; j < ntiles; j++, gtile++) {
                 const uint32_t buf = gtile & 1;
                 mbar_wait(smem_u32(&tfull[buf]), (gtile >> 1) & 1);
@@ -329,17 +352,31 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
                     }
                     // fast path: chunk minimum by a tree; exact scan only if it can
                     // change the best or the runner-up
-                    float m[16];
+                    // min tree; level 2 keeps 8 group minima, group g = {g, g+8, g+16, g+24}
+                    float m1[16], m2[8];
 #pragma unroll
-                    for (int e = 0; e < 16; e++) m[e] = fminf(__uint_as_float(v[e]), __uint_as_float(v[e + 16]));
+                    for (int e = 0; e < 16; e++) m1[e] = fminf(__uint_as_float(v[e]), __uint_as_float(v[e + 16]));
 #pragma unroll
-                    for (int e = 0; e < 8; e++) m[e] = fminf(m[e], m[e + 8]);
+                    for (int e = 0; e < 8; e++) m2[e] = fminf(m1[e], m1[e + 8]);
+                    const float mn = fminf(fminf(fminf(m2[0], m2[1]), fminf(m2[2], m2[3])),
+                                           fminf(fminf(m2[4], m2[5]), fminf(m2[6], m2[7])));
+                    // slow path (rare per lane): mask of values below the current 4th
+                    // best, then insert them in increasing index order (ties keep the
+                    // lowest index); register values are picked by a select tree
+                    if (mn < lastv) {
+                        uint32_t hits = 0;
 #pragma unroll
-                    for (int e = 0; e < 4; e++) m[e] = fminf(m[e], m[e + 4]);
-                    const float mn = fminf(fminf(m[0], m[2]), fminf(m[1], m[3]));
-                    if (mn < top.b3) {
-#pragma unroll
-                        for (int e = 0; e < 32; e++) top.push(__uint_as_float(v[e]), p0 + e);
+                        for (int e = 0; e < 32; e++)
+                            hits |= (__uint_as_float(v[e]) < lastv ? 1u : 0u) << e;
+                        while (hits) {
+                            const int e = __ffs(hits) - 1;
+                            hits &= hits - 1;
+                            const float s = select32(v, e);
+                            if (s < lastv) {
+                                top.insert_inline(s, p0 + e);
+                                lastv = top.last();
+                            }
+                        }
                     }
                 }
                 tc_fence_before();
@@ -351,8 +388,9 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
                 iters++;
                 int i1;
                 bool improve;
-                certify_hop<NW>(top, prm.y + (size_t)frame * n, c, prm.pbits, nw, n, ed, prm.tie_rel,
-                                prm.err, i1, improve, flags);
+                float sb;
+                certify_topk<4, NW>(top, prm.y + (size_t)frame * n, c, prm.pbits, nw, n, ed, prm.tie_rel,
+                                    err_row, i1, improve, sb, flags);
                 if (improve) {
                     const uint32_t* pb = prm.pbits + (size_t)i1 * nw;
 #pragma unroll
@@ -365,10 +403,10 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
                             bits &= bits - 1;
                             const uint32_t off = (i >> 6) * A_KBLK_BYTES + sw128_off(row, i & 63);
                             *reinterpret_cast<uint16_t*>(a_hi + off) ^= 0x8000u;
-                            *reinterpret_cast<uint16_t*>(a_lo + off) ^= 0x8000u;
+                            if (LIMBS == 2) *reinterpret_cast<uint16_t*>(a_lo + off) ^= 0x8000u;
                         }
                     }
-                    ed += 4.f * (i1 == top.i1 ? top.b1 : top.b2);
+                    ed += 4.f * sb;
                     if (prm.s2.traj_hops) prm.s2.traj_hops[(size_t)tr * T + iters - 1] = i1 + 1;
                 }
                 if (!improve || iters == T) {
@@ -436,27 +474,35 @@ inline int tc_build(TcPatterns& t, const uint32_t* bits, int np, int n, int nw) 
     return 0;
 }
 
-template <int KB, int NW>
+template <int KB, int NW, int LIMBS>
 inline int tc_launch_t(const TcPatterns& t, int n, int nw, int A, int T, const float* y, S2Dev s2, PatDev P,
                        int num_sms, cudaStream_t st) {
     tc::Params prm;
     prm.n = n; prm.nw = nw; prm.A = A; prm.T = T; prm.np = t.np; prm.ntiles = t.ntiles;
     prm.y = y; prm.s2 = s2; prm.pbits = P.bits; prm.btiles = t.tiles; prm.tie_rel = 1e-5f;
     prm.err = 2e-3f;
-    const size_t smem = tc::smem_bytes(KB);
-    if (cudaFuncSetAttribute(tc::hop_tc_kernel<KB, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    const size_t smem = tc::smem_bytes(KB, LIMBS);
+    if (cudaFuncSetAttribute(tc::hop_tc_kernel<KB, NW, LIMBS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return -1;
-    tc::hop_tc_kernel<KB, NW><<<num_sms, tc::THREADS, smem, st>>>(prm);
+    tc::hop_tc_kernel<KB, NW, LIMBS><<<num_sms, tc::THREADS, smem, st>>>(prm);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
 inline int tc_launch(const TcPatterns& t, int n, int nw, int A, int T, const float* y, S2Dev s2, PatDev P,
-                     int num_sms, cudaStream_t st) {
+                     int num_sms, int limbs, cudaStream_t st) {
     if (!t.ready) return -1;
+    if (limbs == 1) {
+        switch (n) {
+            case 64: return tc_launch_t<1, 2, 1>(t, n, nw, A, T, y, s2, P, num_sms, st);
+            case 128: return tc_launch_t<2, 4, 1>(t, n, nw, A, T, y, s2, P, num_sms, st);
+            case 256: return tc_launch_t<4, 8, 1>(t, n, nw, A, T, y, s2, P, num_sms, st);
+            default: return -1;
+        }
+    }
     switch (n) {
-        case 64: return tc_launch_t<1, 2>(t, n, nw, A, T, y, s2, P, num_sms, st);
-        case 128: return tc_launch_t<2, 4>(t, n, nw, A, T, y, s2, P, num_sms, st);
-        case 256: return tc_launch_t<4, 8>(t, n, nw, A, T, y, s2, P, num_sms, st);
+        case 64: return tc_launch_t<1, 2, 2>(t, n, nw, A, T, y, s2, P, num_sms, st);
+        case 128: return tc_launch_t<2, 4, 2>(t, n, nw, A, T, y, s2, P, num_sms, st);
+        case 256: return tc_launch_t<4, 8, 2>(t, n, nw, A, T, y, s2, P, num_sms, st);
         default: return -1;
     }
 }

@@ -87,6 +87,8 @@ struct mpw_handle {
     DevBuf<int32_t> s2_count, s2_frame, s2_nanchor, traj_iters, traj_hops, work_next;
     DevBuf<uint32_t> s2_anchors, traj_cw;
     DevBuf<uint8_t> traj_flags;
+    DevBuf<float4> ebound;
+    int wmax = 0;
     // timing
     int timing = 0;
     cudaEvent_t ev[8];
@@ -247,12 +249,19 @@ __global__ void frame_kernel(FrameArgs fa) {
 }
 
 // mp_wsd API: queue = identity over the given frames
-__global__ void queue_identity_kernel(int F, int A, const int32_t* nanchor, S2Dev s2) {
-    const int q = blockIdx.x * blockDim.x + threadIdx.x;
-    if (q == 0) *s2.count = F;
+// (warp per frame: also the per-frame score error bounds the hop kernels use)
+__global__ void queue_identity_kernel(int F, int A, int n, const float* __restrict__ y,
+                                      const int32_t* nanchor, S2Dev s2) {
+    const int lane = threadIdx.x & 31;
+    const int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (q == 0 && lane == 0) *s2.count = F;
     if (q < F) {
-        s2.frame[q] = q;
-        s2.nanchor[q] = nanchor ? min(nanchor[q], A) : A;
+        const float4 eb = warp_error_bounds(y + (size_t)q * n, n, s2.wmax);
+        if (lane == 0) {
+            s2.frame[q] = q;
+            s2.nanchor[q] = nanchor ? min(nanchor[q], A) : A;
+            s2.ebound[q] = eb;
+        }
     }
 }
 
@@ -267,6 +276,7 @@ int ensure_s2(mpw_handle* h, int F, int A, int T) {
     CK(h->traj_iters.ensure(traj));
     CK(h->traj_hops.ensure(traj * T));
     CK(h->traj_flags.ensure(traj));
+    CK(h->ebound.ensure(F));
     return 0;
 }
 
@@ -276,6 +286,7 @@ S2Dev s2_dev(mpw_handle* h, const uint32_t* anchors_override) {
     s.anchors = anchors_override ? const_cast<uint32_t*>(anchors_override) : h->s2_anchors.p;
     s.traj_cw = h->traj_cw.p; s.traj_iters = h->traj_iters.p; s.traj_hops = h->traj_hops.p;
     s.traj_flags = h->traj_flags.p; s.work_next = h->work_next.p;
+    s.ebound = h->ebound.p; s.wmax = h->wmax;
     return s;
 }
 
@@ -348,9 +359,10 @@ int launch_gather(mpw_handle* h, HopParams hp, int max_traj, cudaStream_t st) {
 
 int run_hops(mpw_handle* h, const float* y, int Fmax, int A, int T, int variant, S2Dev s2, cudaStream_t st) {
     if (variant == MPW_HOP_AUTO) variant = tc_supported(h->n, h->np) && h->tcp.ready ? MPW_HOP_TENSOR : MPW_HOP_GATHER;
-    if (variant == MPW_HOP_TENSOR) {
+    if (variant == MPW_HOP_TENSOR || variant == MPW_HOP_TENSOR_2LIMB) {
         if (!h->tcp.ready) return fail(MPW_ERR_UNSUPPORTED, "tensor-core hop operand not built for this pattern set");
-        int rc = tc_launch(h->tcp, h->n, h->nw, A, T, y, s2, pat_dev(h), h->num_sms, st);
+        const int limbs = variant == MPW_HOP_TENSOR ? 1 : 2;
+        int rc = tc_launch(h->tcp, h->n, h->nw, A, T, y, s2, pat_dev(h), h->num_sms, limbs, st);
         if (rc) return fail(MPW_ERR_CUDA, "tensor-core hop launch failed: %s", cudaGetErrorString(cudaGetLastError()));
         return 0;
     }
@@ -416,7 +428,7 @@ void mpw_destroy(mpw_handle* h) {
     h->crc_h.release(); h->mix.release(); h->pbits.release(); h->poff.release(); h->soff.release();
     h->pidx.release(); h->sup.release(); h->s2_count.release(); h->s2_frame.release();
     h->s2_nanchor.release(); h->traj_iters.release(); h->traj_hops.release(); h->work_next.release();
-    h->s2_anchors.release(); h->traj_cw.release(); h->traj_flags.release();
+    h->s2_anchors.release(); h->traj_cw.release(); h->traj_flags.release(); h->ebound.release();
     tc_release(h->tcp);
     if (h->ev_init) for (int i = 0; i < 8; i++) cudaEventDestroy(h->ev[i]);
     delete h;
@@ -525,6 +537,8 @@ int mpw_set_patterns(mpw_handle* h, const uint64_t* pattern_words, int np) {
     soff[np] = (int32_t)(sup.size() / 8);
     h->np = np;
     h->total_sup_u4 = (int)(sup.size() / 8);
+    h->wmax = 0;
+    for (int p = 0; p < np; p++) h->wmax = std::max(h->wmax, off[p + 1] - off[p]);
     CK(h->pbits.ensure(bits.size())); CK(h->poff.ensure(off.size())); CK(h->soff.ensure(soff.size()));
     CK(h->pidx.ensure(std::max<size_t>(idx.size(), 1))); CK(h->sup.ensure(std::max<size_t>(sup.size() / 8, 1)));
     if (np) {
@@ -566,7 +580,7 @@ int mpw_mpwsd_batch(mpw_handle* h, const float* y, const uint32_t* anchors, cons
     if (int rc = ensure_s2(h, F, A, T)) return rc;
     S2Dev s2 = s2_dev(h, anchors);
     if (!hops) s2.traj_hops = h->traj_hops.p;
-    queue_identity_kernel<<<(F + 255) / 256, 256, 0, st>>>(F, A, n_anchor, s2);
+    queue_identity_kernel<<<(F + 7) / 8, 256, 0, st>>>(F, A, h->n, y, n_anchor, s2);
     CK(cudaGetLastError());
     if (int rc = run_hops(h, y, F, A, T, variant, s2, st)) return rc;
     FinalOut fo{best, best_ed, nullptr, iters, hops, nullptr, flags, nullptr};

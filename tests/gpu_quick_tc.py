@@ -13,13 +13,13 @@ for name, F in [("cfg1", 512), ("cfg3", 512), ("cfg2", 128), ("cfg4", 64)]:
     _, tx, y = channel.bulk_inputs(code, 3, 0, 0, F, sigma)
     dec = DeviceDecoder(code, sph)
     res = {}
-    for var in ["gather", "tensor"]:
+    for var in ["gather", "tensor", "tensor2"]:
         torch.cuda.synchronize(); t0 = time.time()
         o = dec.two_stage_batch(y, sigma, cfg.list_size, cfg.num_paths, cfg.max_iterations, "always_on", variant=var)
         torch.cuda.synchronize(); dt = time.time() - t0
         res[var] = (words32_to_64(o["best"].cpu().numpy().view(np.uint32), code.n), o["iters"].cpu().numpy(), o["flags"].cpu().numpy(), dt)
     r = orc.two_stage_batch(y, code, sph, cfg.list_size, cfg.num_paths, cfg.max_iterations, False, sigma, nthreads=8)
-    for var in ["gather", "tensor"]:
+    for var in ["gather", "tensor", "tensor2"]:
         b, it, fl, dt = res[var]
         mism = np.flatnonzero((b != r["best"]).any(1))
         unfl = [m for m in mism if fl[m] == 0]

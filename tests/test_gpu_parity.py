@@ -46,7 +46,7 @@ def test_scl_lists_bit_exact_vs_reference(fx):
         np.testing.assert_array_equal(pm[f, :c], g["list_pm"][f, :c])
 
 
-@pytest.mark.parametrize("variant", ["gather", "tensor"])
+@pytest.mark.parametrize("variant", ["gather", "tensor", "tensor2"])
 @pytest.mark.parametrize("fx", two_stage_fixtures())
 def test_two_stage_vs_reference_golden(fx, variant):
     g = load(fx)
@@ -76,7 +76,7 @@ def test_two_stage_vs_reference_golden(fx, variant):
     np.testing.assert_array_equal(msg[ok], ref_msg[ok])
 
 
-@pytest.mark.parametrize("variant", ["gather", "tensor"])
+@pytest.mark.parametrize("variant", ["gather", "tensor", "tensor2"])
 @pytest.mark.parametrize("name", ["cfg1", "cfg3", "cfg2", "cfg4"])
 def test_two_stage_vs_oracle_random_frames(name, variant):
     cfg = configs.CONFIGS[name]
@@ -102,7 +102,7 @@ def test_two_stage_vs_oracle_random_frames(name, variant):
     np.testing.assert_array_equal(_np(o["iters"])[ok], r["iters"][ok])
 
 
-@pytest.mark.parametrize("variant", ["gather", "tensor"])
+@pytest.mark.parametrize("variant", ["gather", "tensor", "tensor2"])
 def test_mp_wsd_random_anchors_vs_oracle(variant):
     cfg = configs.CONFIGS["cfg1"]
     code, sph = code_and_sphere(cfg)

@@ -35,6 +35,10 @@ constexpr int THREADS = 192;
 constexpr int EPI_THREADS = 128;
 
 constexpr int SMEM_LIMIT = 232448;   // 227 KB opt-in maximum per CTA
+#ifndef MPW_TC_TOPK
+#define MPW_TC_TOPK 6
+#endif
+constexpr int TOPK = MPW_TC_TOPK;    // candidates tracked per row for certification
 
 __host__ __device__ constexpr int stages_for(int kb, int limbs) {
     return (SMEM_LIMIT - 1024 - 256 - limbs * kb * A_KBLK_BYTES) / B_STAGE_BYTES > 6
@@ -330,7 +334,7 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
         }
         uint32_t gtile = 0;
         while (any) {
-            TopK<4> top;
+            TopK<TOPK> top;
             top.reset();
             float lastv = CUDART_INF_F;   // register copy of top.last()
             for (int j = 0; j < ntiles; j++, gtile++) {
@@ -389,7 +393,7 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
                 int i1;
                 bool improve;
                 float sb;
-                certify_topk<4, NW>(top, prm.y + (size_t)frame * n, c, prm.pbits, nw, n, ed, prm.tie_rel,
+                certify_topk<TOPK, NW>(top, prm.y + (size_t)frame * n, c, prm.pbits, nw, n, ed, prm.tie_rel,
                                     err_row, i1, improve, sb, flags);
                 if (improve) {
                     const uint32_t* pb = prm.pbits + (size_t)i1 * nw;

@@ -580,6 +580,7 @@ int mpw_mpwsd_batch(mpw_handle* h, const float* y, const uint32_t* anchors, cons
     if (int rc = ensure_s2(h, F, A, T)) return rc;
     S2Dev s2 = s2_dev(h, anchors);
     if (!hops) s2.traj_hops = h->traj_hops.p;
+    CK(cudaMemsetAsync(s2.work_next, 0, sizeof(int32_t), st));
     queue_identity_kernel<<<(F + 7) / 8, 256, 0, st>>>(F, A, h->n, y, n_anchor, s2);
     CK(cudaGetLastError());
     if (int rc = run_hops(h, y, F, A, T, variant, s2, st)) return rc;

@@ -134,6 +134,9 @@ int mpw_two_stage_batch_host(mpw_handle* h, const float* y_host, int F, double s
 /* Per-kernel CUDA-event timing of mpw_two_stage_batch: ms_out[4] =
  * {stage 1, stage 2 hops, finalize, frame epilogue}. */
 int mpw_set_timing(mpw_handle* h, int enable);
+/* Options: "scl_generic" (1 = force the warp-per-frame stage-1 kernel instead of
+ * the lane-per-path one; both are bit-exact), "timing" (same as mpw_set_timing). */
+int mpw_set_option(mpw_handle* h, const char* key, int value);
 int mpw_read_timing(mpw_handle* h, double* ms_out, long long* launches_out, int reset);
 
 int mpw_num_patterns(mpw_handle* h);

@@ -38,6 +38,7 @@ _SIGS = {
                                          c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p,
                                          c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "mpw_set_timing": (c_int, [c_void_p, c_int]),
+    "mpw_set_option": (c_int, [c_void_p, ctypes.c_char_p, c_int]),
     "mpw_read_timing": (c_int, [c_void_p, c_void_p, c_void_p, c_int]),
     "mpw_num_patterns": (c_int, [c_void_p]),
     "mpw_tensor_path_ready": (c_int, [c_void_p]),

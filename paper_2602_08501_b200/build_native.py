@@ -11,7 +11,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmpwsd.so")
 SOURCES = ["mpwsd.cu", "sphere_tools.cpp"]
-HEADERS = ["common.cuh", "scl.cuh", "hop_gather.cuh", "hop_tc.cuh"]
+HEADERS = ["common.cuh", "scl.cuh", "scl_lane.cuh", "hop_gather.cuh", "hop_tc.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-O3", "-shared", "-lpthread"]

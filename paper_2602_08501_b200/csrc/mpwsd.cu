@@ -20,6 +20,7 @@
 #include "hop_gather.cuh"
 #include "hop_tc.cuh"
 #include "scl.cuh"
+#include "scl_lane.cuh"
 
 namespace {
 
@@ -89,6 +90,7 @@ struct mpw_handle {
     DevBuf<uint8_t> traj_flags;
     DevBuf<float4> ebound;
     int wmax = 0;
+    int scl_generic = 0;            // force the warp-per-frame SCL kernel
     // timing
     int timing = 0;
     cudaEvent_t ev[8];
@@ -265,6 +267,17 @@ __global__ void queue_identity_kernel(int F, int A, int n, const float* __restri
     }
 }
 
+// per-frame score error bounds of the queued stage-2 frames (warp per entry)
+__global__ void ebound_kernel(int n, const float* __restrict__ y, S2Dev s2) {
+    const int lane = threadIdx.x & 31;
+    const int warps = gridDim.x * (blockDim.x >> 5);
+    const int count = *s2.count;
+    for (int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); q < count; q += warps) {
+        const float4 eb = warp_error_bounds(y + (size_t)s2.frame[q] * n, n, s2.wmax);
+        if (lane == 0) s2.ebound[q] = eb;
+    }
+}
+
 int ensure_s2(mpw_handle* h, int F, int A, int T) {
     const size_t traj = (size_t)F * A;
     CK(h->s2_count.ensure(1));
@@ -324,8 +337,50 @@ int launch_scl(mpw_handle* h, const float* y, const double* llr64, int F, double
     return 0;
 }
 
+template <int N, int L>
+int launch_scl_lane(mpw_handle* h, const float* y, const double* llr64, int F, double sigma, int A,
+                    int mode, SclOut out, S2Dev s2, cudaStream_t st) {
+    using Lay = SclLane<N, L>;
+    const size_t per_warp = Lay::TOTAL * Lay::FPW;
+    int wpb = (int)std::max<size_t>(1, std::min<size_t>(4, (200 * 1024) / per_warp));
+    const size_t smem = per_warp * wpb;
+    if (smem > 227 * 1024) return fail(MPW_ERR_UNSUPPORTED, "SCL lane kernel shared memory %zu B too large", smem);
+    CK(cudaFuncSetAttribute(scl_lane_kernel<N, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, scl_lane_kernel<N, L>, 32 * wpb, smem));
+    per_sm = std::max(per_sm, 1);
+    const long long frames_per_block = (long long)wpb * Lay::FPW;
+    const long long need = ((long long)F + frames_per_block - 1) / frames_per_block;
+    const int grid = (int)std::max<long long>(1, std::min<long long>(need, (long long)per_sm * h->num_sms * 8));
+    scl_lane_kernel<N, L><<<grid, 32 * wpb, smem, st>>>(code_dev(h), y, llr64, F, sigma, A, mode, out, s2);
+    CK(cudaGetLastError());
+    return 0;
+}
+
+template <int N>
+int dispatch_scl_lane(mpw_handle* h, const float* y, const double* llr64, int F, double sigma, int L, int A,
+                      int mode, SclOut out, S2Dev s2, cudaStream_t st) {
+    switch (L) {
+        case 4: return launch_scl_lane<N, 4>(h, y, llr64, F, sigma, A, mode, out, s2, st);
+        case 8: return launch_scl_lane<N, 8>(h, y, llr64, F, sigma, A, mode, out, s2, st);
+        case 16: return launch_scl_lane<N, 16>(h, y, llr64, F, sigma, A, mode, out, s2, st);
+        case 32: return launch_scl_lane<N, 32>(h, y, llr64, F, sigma, A, mode, out, s2, st);
+        default: return 1;
+    }
+}
+
 int dispatch_scl(mpw_handle* h, const float* y, const double* llr64, int F, double sigma, int L, int A,
                  int mode, SclOut out, S2Dev s2, cudaStream_t st) {
+    // lane-per-path kernel for the common shapes (power-of-two L, N in {64,128,256}),
+    // warp-per-frame kernel otherwise (or when MPW_SCL_GENERIC is set)
+    const bool pow2 = L >= 1 && (L & (L - 1)) == 0 && L <= 32;
+    if (pow2 && !h->scl_generic) {
+        int rc = 1;
+        if (h->n == 64) rc = dispatch_scl_lane<64>(h, y, llr64, F, sigma, L, A, mode, out, s2, st);
+        else if (h->n == 128) rc = dispatch_scl_lane<128>(h, y, llr64, F, sigma, L, A, mode, out, s2, st);
+        else if (h->n == 256) rc = dispatch_scl_lane<256>(h, y, llr64, F, sigma, L, A, mode, out, s2, st);
+        if (rc <= 0) return rc;
+    }
     switch (h->nw) {
         case 1: return launch_scl<1>(h, y, llr64, F, sigma, L, A, mode, out, s2, st);
         case 2: return launch_scl<2>(h, y, llr64, F, sigma, L, A, mode, out, s2, st);
@@ -612,6 +667,8 @@ int mpw_two_stage_batch(mpw_handle* h, const float* y, int F, double sigma, int 
     SclOut out{nullptr, nullptr, nullptr, nullptr, stage, best, best_ed};
     const int smode = (mode == MPW_MODE_CRC_GATED) ? 1 : 2;
     if (int rc = dispatch_scl(h, y, nullptr, F, sigma, L, A, smode, out, s2, st)) return rc;
+    ebound_kernel<<<std::max(1, std::min((F + 7) / 8, h->num_sms * 16)), 256, 0, st>>>(h->n, y, s2);
+    CK(cudaGetLastError());
     timing_mark(h, 1, st);
     if (int rc = run_hops(h, y, F, A, T, variant, s2, st)) return rc;
     timing_mark(h, 2, st);
@@ -664,6 +721,13 @@ int mpw_two_stage_batch_host(mpw_handle* h, const float* y_host, int F, double s
     if (counters_host) CK(cudaMemcpyAsync(counters_host, dctr.p, sizeof(unsigned long long) * MPW_NUM_COUNTERS, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     return 0;
+}
+
+int mpw_set_option(mpw_handle* h, const char* key, int value) {
+    if (!h || !key) return fail(MPW_ERR_ARG, "null argument");
+    if (!strcmp(key, "scl_generic")) { h->scl_generic = value ? 1 : 0; return 0; }
+    if (!strcmp(key, "timing")) { h->timing = value ? 1 : 0; return 0; }
+    return fail(MPW_ERR_ARG, "unknown option '%s'", key);
 }
 
 int mpw_set_timing(mpw_handle* h, int enable) {

@@ -311,7 +311,6 @@ __global__ void __launch_bounds__(256) scl_kernel(CodeDev code, const float* __r
 #pragma unroll
             for (int w = 0; w < NW; w++) if (w < nw) s2.anchors[o + w] = an[w];
         }
-        const float4 eb = warp_error_bounds(y + (size_t)f * n, n, s2.wmax);
-        if (lane == 0) { s2.frame[q] = f; s2.nanchor[q] = na; out.stage[f] = 1; s2.ebound[q] = eb; }
+        if (lane == 0) { s2.frame[q] = f; s2.nanchor[q] = na; out.stage[f] = 1; }
     }
 }

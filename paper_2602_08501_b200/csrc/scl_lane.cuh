@@ -1,0 +1,376 @@
+// Stage 1, specialised: lane-per-path CA-SCL for power-of-two L <= 32 and
+// N <= 256, templated on (N, L) so every loop bound and index is a constant.
+//
+// A warp holds FPW = 32 / L frames; lane = frame_in_warp * L + path.  Each
+// lane runs its own path through the whole SC schedule (the f/g loops over a
+// node's `half` elements are sequential per lane), so the per-element index
+// arithmetic of the warp-per-frame kernel disappears.  Float64 operations and
+// their order are exactly those of scl.cuh / the reference (decoders.py:173-268),
+// so lists, orders and path metrics stay bit-identical.
+//
+// Shared memory per frame:
+//   llr0[N]            channel LLRs (2y/sigma^2)
+//   llr[L][N-1]        per-path instances of levels 1..M (lazy clone via ptr)
+//   ps[L][NW+1]        partial-sum bits (row padded against bank conflicts)
+//   u[L][NW+1]         leaf decisions
+//   ptr[L][PTRW]       instance index per level (bytes)
+//   sel_src/bit/val[L] info-leaf selection scratch
+#pragma once
+#include "common.cuh"
+#include "scl.cuh"
+
+// Levels 1 and 2 are "virtual": never stored, recomputed on demand from the
+// channel LLRs and the path's own partial-sum bits with the same IEEE
+// operations (so the values are bit-identical to stored ones).  Only levels
+// 3..M are stored per path instance: N/4 - 1 doubles instead of N - 1.
+constexpr int SCL_VIRT = 2;
+
+template <int N, int L>
+struct SclLane {
+    static constexpr int M = (N >= 256) ? 8 : (N >= 128) ? 7 : (N >= 64) ? 6 : (N >= 32) ? 5 : (N >= 16) ? 4 : (N >= 8) ? 3 : (N >= 4) ? 2 : 1;
+    static constexpr int NW = N >= 32 ? N / 32 : 1;
+    static constexpr int NWP = NW + 1;
+    static constexpr int PTRW = 5;                       // 20 bytes: levels 0..19
+    static constexpr int FPW = 32 / L;
+    static constexpr int INST = N / 4 - 1;               // stored doubles per instance (levels 3..M)
+    static constexpr size_t LLR0 = 0;
+    static constexpr size_t LLR = LLR0 + 8 * (size_t)N;
+    static constexpr size_t PS = LLR + 8 * (size_t)L * INST;
+    static constexpr size_t U = PS + 4 * (size_t)L * NWP;
+    static constexpr size_t PTR = U + 4 * (size_t)L * NWP;
+    static constexpr size_t SVAL = (PTR + 4 * (size_t)L * PTRW + 7) & ~(size_t)7;
+    static constexpr size_t SSRC = SVAL + 8 * (size_t)L;
+    static constexpr size_t SBIT = SSRC + 4 * (size_t)L;
+    static constexpr size_t TOTAL = (SBIT + 4 * (size_t)L + 15) & ~(size_t)15;
+    // offset of stored level lvl (3..M) inside an instance
+    __host__ __device__ static constexpr int off(int lvl) { return N / 4 - 2 * (N >> (lvl > 0 ? lvl : 0)); }
+};
+
+// ---- node kernels with compile-time HALF (one lane = one path)
+template <int HALF>
+__device__ __forceinline__ void lane_f(const double* __restrict__ par, double* __restrict__ o) {
+#pragma unroll (HALF < 8 ? HALF : 8)
+    for (int j = 0; j < HALF; j++) o[j] = scl_f(par[j], par[j + HALF]);
+}
+
+template <int HALF>
+__device__ __forceinline__ void lane_g(const double* __restrict__ par, double* __restrict__ o,
+                                       const uint32_t* __restrict__ psrow, int lo) {
+    if constexpr (HALF >= 32) {
+#pragma unroll 1
+        for (int jw = 0; jw < HALF / 32; jw++) {
+            const uint32_t word = psrow[(lo >> 5) + jw];
+#pragma unroll 8
+            for (int b = 0; b < 32; b++) {
+                const int j = jw * 32 + b;
+                const double a = par[j], c = par[j + HALF];
+                o[j] = c + (((word >> b) & 1u) ? -a : a);
+            }
+        }
+    } else {
+        const uint32_t word = psrow[lo >> 5] >> (lo & 31);
+#pragma unroll
+        for (int j = 0; j < HALF; j++) {
+            const double a = par[j], c = par[j + HALF];
+            o[j] = c + (((word >> j) & 1u) ? -a : a);
+        }
+    }
+}
+
+// virtual level 1: LLR j of depth-1 node `n1` (decoders.py:239-252 applied to llr0)
+template <int N>
+__device__ __forceinline__ double lv1(const double* __restrict__ llr0, const uint32_t* __restrict__ psrow,
+                                      int n1, int j) {
+    const double a = llr0[j], b = llr0[j + N / 2];
+    if (n1 == 0) return scl_f(a, b);
+    const uint32_t u = (psrow[j >> 5] >> (j & 31)) & 1u;       // left sibling's level-1 bits
+    return b + (u ? -a : a);
+}
+
+// virtual level 2: LLR j of depth-2 node `n2`
+template <int N>
+__device__ __forceinline__ double lv2(const double* __restrict__ llr0, const uint32_t* __restrict__ psrow,
+                                      int n2, int j) {
+    const int n1 = n2 >> 1;
+    const double a = lv1<N>(llr0, psrow, n1, j), b = lv1<N>(llr0, psrow, n1, j + N / 4);
+    if (!(n2 & 1)) return scl_f(a, b);
+    const int pos = n1 * (N / 2) + j;                           // left sibling's level-2 bits
+    const uint32_t u = (psrow[pos >> 5] >> (pos & 31)) & 1u;
+    return b + (u ? -a : a);
+}
+
+// depth-2 node: parent = virtual level 2, child = stored level 3
+template <int N>
+__device__ __forceinline__ void lane_node_d2(bool is_g, int n2, const double* __restrict__ llr0,
+                                             const uint32_t* __restrict__ psrow, double* __restrict__ o,
+                                             int lo) {
+    constexpr int HALF = N / 8;
+    const uint32_t word = (HALF >= 32) ? 0u : (psrow[lo >> 5] >> (lo & 31));
+#pragma unroll 4
+    for (int j = 0; j < HALF; j++) {
+        const double a = lv2<N>(llr0, psrow, n2, j), c = lv2<N>(llr0, psrow, n2, j + HALF);
+        if (!is_g) {
+            o[j] = scl_f(a, c);
+        } else {
+            const int p = lo + j;
+            const uint32_t u = (HALF >= 32) ? ((psrow[p >> 5] >> (p & 31)) & 1u) : ((word >> j) & 1u);
+            o[j] = c + (u ? -a : a);
+        }
+    }
+}
+
+template <int N, int L>
+__device__ __forceinline__ void lane_node(int d, bool is_g, const double* par, double* o,
+                                          const uint32_t* psrow, int lo) {
+    // dispatch on depth so HALF = N >> (d+1) is a compile-time constant
+#define MPW_LANE_CASE(DD)                                                        \
+    case DD:                                                                     \
+        if constexpr ((N >> (DD + 1)) >= 1) {                                   \
+            if (is_g) lane_g<(N >> (DD + 1))>(par, o, psrow, lo);               \
+            else lane_f<(N >> (DD + 1))>(par, o);                               \
+        }                                                                        \
+        break;
+    switch (d) {
+        MPW_LANE_CASE(0) MPW_LANE_CASE(1) MPW_LANE_CASE(2) MPW_LANE_CASE(3)
+        MPW_LANE_CASE(4) MPW_LANE_CASE(5) MPW_LANE_CASE(6) MPW_LANE_CASE(7)
+        default: break;
+    }
+#undef MPW_LANE_CASE
+}
+
+template <int N, int L>
+__global__ void __launch_bounds__(128) scl_lane_kernel(CodeDev code, const float* __restrict__ y,
+                                                       const double* __restrict__ llr64, int F,
+                                                       double sigma, int A, int mode, SclOut out,
+                                                       S2Dev s2) {
+    using Lay = SclLane<N, L>;
+    constexpr int M = Lay::M, NW = Lay::NW, NWP = Lay::NWP, FPW = Lay::FPW;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+    const int fi = lane / L, l = lane % L, g0 = fi * L;
+    const unsigned gmask = (L == 32) ? MPW_FULL : (((1u << L) - 1u) << g0);
+    unsigned char* base = smem_raw + (size_t)(wib * FPW + fi) * Lay::TOTAL;
+    double* llr0 = reinterpret_cast<double*>(base + Lay::LLR0);
+    double* llr = reinterpret_cast<double*>(base + Lay::LLR);
+    uint32_t* ps_all = reinterpret_cast<uint32_t*>(base + Lay::PS);
+    uint32_t* u_all = reinterpret_cast<uint32_t*>(base + Lay::U);
+    uint8_t* ptr_all = base + Lay::PTR;
+    double* sel_val = reinterpret_cast<double*>(base + Lay::SVAL);
+    int32_t* sel_src = reinterpret_cast<int32_t*>(base + Lay::SSRC);
+    int32_t* sel_bit = reinterpret_cast<int32_t*>(base + Lay::SBIT);
+    uint32_t* psrow = ps_all + l * NWP;
+    uint32_t* urow = u_all + l * NWP;
+    uint8_t* ptrrow = ptr_all + l * Lay::PTRW * 4;
+    double* myllr = llr + (size_t)l * Lay::INST;
+    const double sig2 = sigma * sigma;
+
+    for (long long fb = ((long long)blockIdx.x * wpb + wib) * FPW; fb < F;
+         fb += (long long)gridDim.x * wpb * FPW) {
+        const long long f = fb + fi;
+        const bool valid = f < F;
+        // ---- init (decoders.py:204-209)
+        for (int i = l; i < N; i += L) {
+            double v = 0.0;
+            if (valid) v = llr64 ? llr64[(size_t)f * N + i] : 2.0 * (double)y[(size_t)f * N + i] / sig2;
+            llr0[i] = v;
+        }
+#pragma unroll
+        for (int w = 0; w < NWP; w++) { psrow[w] = 0u; urow[w] = 0u; }
+        double pm = (l == 0) ? 0.0 : CUDART_INF;
+        __syncwarp();
+
+        for (int phi = 0; phi < N; phi++) {
+            // descent to leaf phi: one g at depth M-1-ctz(phi), then f's.  Nodes
+            // whose child level is virtual (depth < SCL_VIRT) need no work.
+            int dstart = 0;
+            if (phi) {
+                const int t = __ffs(phi) - 1;
+                const int d = M - 1 - t;
+                const int lo = (phi >> (M - d)) << (M - d);
+                if (d == SCL_VIRT) {
+                    lane_node_d2<N>(true, phi >> (M - 2), llr0, psrow, myllr + Lay::off(3), lo);
+                    ptrrow[3] = (uint8_t)l;
+                } else if (d > SCL_VIRT) {
+                    const double* par = llr + (size_t)ptrrow[d] * Lay::INST + Lay::off(d);
+                    lane_node<N, L>(d, true, par, myllr + Lay::off(d + 1), psrow, lo);
+                    ptrrow[d + 1] = (uint8_t)l;
+                }
+                __syncwarp();
+                dstart = d + 1;
+            }
+            for (int d = dstart > SCL_VIRT ? dstart : SCL_VIRT; d < M; d++) {
+                if (d == SCL_VIRT) {
+                    lane_node_d2<N>(false, phi >> (M - 2), llr0, psrow, myllr + Lay::off(3), 0);
+                    ptrrow[3] = (uint8_t)l;
+                } else {
+                    const double* par = llr + (size_t)ptrrow[d] * Lay::INST + Lay::off(d);
+                    lane_node<N, L>(d, false, par, myllr + Lay::off(d + 1), psrow, 0);
+                    ptrrow[d + 1] = (uint8_t)l;
+                }
+                __syncwarp();
+            }
+            const double dm = myllr[Lay::INST - 1];
+            const bool frozen = (code.frozen[phi >> 5] >> (phi & 31)) & 1u;
+            if (frozen) {
+                pm = pm + fabs(dm) * (double)(dm < 0.0);                      // :216-218
+            } else {
+                // stable rank of the 2L candidates (pm_k natural, pm_k + |dm_k| flipped)
+                const double vn = pm, vf = pm + fabs(dm);
+                int rn = 0, rf = 0;
+#pragma unroll
+                for (int k = 0; k < L; k++) {
+                    const double pk = __shfl_sync(MPW_FULL, pm, g0 + k);
+                    const double dk = __shfl_sync(MPW_FULL, dm, g0 + k);
+                    const double fk = pk + fabs(dk);
+                    rn += (pk < vn) || (pk == vn && k < l);
+                    rn += (fk < vn);
+                    rf += (pk <= vf);
+                    rf += (fk < vf) || (fk == vf && k < l);
+                }
+                const int nat = dm < 0.0 ? 1 : 0;
+                if (rn < L) { sel_src[rn] = l; sel_bit[rn] = nat; sel_val[rn] = vn; }
+                if (rf < L) { sel_src[rf] = l; sel_bit[rf] = nat ^ 1; sel_val[rf] = vf; }
+                __syncwarp();
+                const int src = sel_src[l];
+                const int bit = sel_bit[l];
+                pm = sel_val[l];
+                uint32_t rps[NW], ru[NW], rp[Lay::PTRW];
+                const uint32_t* sps = ps_all + src * NWP;
+                const uint32_t* su = u_all + src * NWP;
+                const uint32_t* sp = reinterpret_cast<const uint32_t*>(ptr_all + src * Lay::PTRW * 4);
+#pragma unroll
+                for (int w = 0; w < NW; w++) { rps[w] = sps[w]; ru[w] = su[w]; }
+#pragma unroll
+                for (int w = 0; w < Lay::PTRW; w++) rp[w] = sp[w];
+                __syncwarp();
+                if (bit) {
+#pragma unroll
+                    for (int w = 0; w < NW; w++)
+                        if (w == (phi >> 5)) { rps[w] |= 1u << (phi & 31); ru[w] |= 1u << (phi & 31); }
+                }
+#pragma unroll
+                for (int w = 0; w < NW; w++) { psrow[w] = rps[w]; urow[w] = ru[w]; }
+                uint32_t* mp = reinterpret_cast<uint32_t*>(ptrrow);
+#pragma unroll
+                for (int w = 0; w < Lay::PTRW; w++) mp[w] = rp[w];
+                __syncwarp();
+            }
+            if (phi == N - 1) break;
+            const int c = __ffs(~phi) - 1;                                      // :253-259
+            for (int d = M - 1; d >= M - c; d--) {
+                const int half = N >> (d + 1);
+                const int lo = (phi >> (M - d)) << (M - d);
+                if (half >= 32) {
+                    const int hw = half >> 5, w0 = lo >> 5;
+                    for (int i = 0; i < hw; i++) psrow[w0 + i] ^= psrow[w0 + hw + i];
+                } else {
+                    const uint32_t mask = ((1u << half) - 1u) << (lo & 31);
+                    const uint32_t x = psrow[lo >> 5];
+                    psrow[lo >> 5] = x ^ ((x >> half) & mask);
+                }
+            }
+        }
+
+        // ---- list: finite paths, stable by pm (decoders.py:261-268)
+        const bool fin = isfinite(pm);
+        int rank = 0;
+#pragma unroll
+        for (int k = 0; k < L; k++) {
+            const double pk = __shfl_sync(MPW_FULL, pm, g0 + k);
+            rank += isfinite(pk) && ((pk < pm) || (pk == pm && k < l));
+        }
+        const unsigned finmask = __ballot_sync(MPW_FULL, fin) & gmask;
+        const int cnt = __popc(finmask);
+        uint32_t cw[NW], uu[NW];
+#pragma unroll
+        for (int w = 0; w < NW; w++) { uu[w] = urow[w]; cw[w] = uu[w]; }
+        polar_transform_words<NW>(cw, NW);
+
+        if (mode == 0) {
+            if (valid) {
+                if (l == 0 && out.list_n) out.list_n[f] = cnt;
+                if (fin) {
+                    const size_t o = ((size_t)f * L + rank) * NW;
+#pragma unroll
+                    for (int w = 0; w < NW; w++) {
+                        if (out.list_u) out.list_u[o + w] = uu[w];
+                        if (out.list_cw) out.list_cw[o + w] = cw[w];
+                    }
+                    if (out.list_pm) out.list_pm[(size_t)f * L + rank] = pm;
+                }
+            }
+            __syncwarp();
+            continue;
+        }
+
+        // ---- CRC gate (decoders.py:559-570) on v = u[info_set] (codebook.py:154-163, 287-297)
+        uint64_t v = 0;
+        if (code.is_ca) {
+            for (int j = 0; j < code.kp; j++) {
+                const int pos = code.info[j];
+                v |= (uint64_t)((urow[pos >> 5] >> (pos & 31)) & 1u) << j;
+            }
+        }
+        int gwin = 1 << 30;                 // lowest CRC-valid rank in this frame group
+        if (mode == 1) {
+            uint32_t syn = 0;
+            for (int j = 0; j < code.crc_deg; j++) syn |= (uint32_t)(__popcll(v & code.crc_h[j]) & 1) << j;
+            gwin = (fin && syn == 0) ? rank : (1 << 30);
+#pragma unroll
+            for (int o = 1; o < L; o <<= 1) gwin = min(gwin, __shfl_xor_sync(MPW_FULL, gwin, o));
+        }
+        const bool passed = gwin < (1 << 30);
+        __syncwarp();
+        // winner's codeword into scratch (ps rows are dead after the last leaf)
+        if (passed && fin && rank == gwin) {
+#pragma unroll
+            for (int w = 0; w < NW; w++) ps_all[w] = cw[w];
+        }
+        __syncwarp();
+        double acc = 0.0;
+        if (passed) {
+            for (int i = l; i < N; i += L) {
+                const double x = ((ps_all[i >> 5] >> (i & 31)) & 1u) ? -1.0 : 1.0;
+                const double dd = (valid ? (double)y[(size_t)f * N + i] : 0.0) - x;
+                acc += dd * dd;
+            }
+        }
+#pragma unroll
+        for (int o = 1; o < L; o <<= 1) acc += __shfl_xor_sync(MPW_FULL, acc, o);
+        // stage-2 queue slot (one atomic per failing frame), broadcast in the group
+        const int na = cnt < A ? cnt : A;
+        int q = 0;
+        if (!passed && valid && l == 0) q = atomicAdd(s2.count, 1);
+        q = __shfl_sync(MPW_FULL, q, g0);
+        if (valid) {
+            if (passed) {
+                for (int w = l; w < NW; w += L) out.best[(size_t)f * NW + w] = ps_all[w];
+                if (l == 0) { out.stage[f] = 0; out.best_ed[f] = acc; }
+            } else {
+                if (fin && rank < na) {
+                    // anchors: first A entries projected into the CRC subcode (decoders.py:572-579)
+                    uint32_t an[NW];
+                    if (code.is_ca) {
+#pragma unroll
+                        for (int w = 0; w < NW; w++) an[w] = 0u;
+                        uint64_t rem = v & ((code.k >= 64) ? ~0ull : ((1ull << code.k) - 1ull));
+                        while (rem) {
+                            const int i = __ffsll((long long)rem) - 1;
+                            rem &= rem - 1;
+#pragma unroll
+                            for (int w = 0; w < NW; w++) an[w] ^= code.gen[(size_t)i * NW + w];
+                        }
+                    } else {
+#pragma unroll
+                        for (int w = 0; w < NW; w++) an[w] = cw[w];
+                    }
+                    const size_t o = ((size_t)q * A + rank) * NW;
+#pragma unroll
+                    for (int w = 0; w < NW; w++) s2.anchors[o + w] = an[w];
+                }
+                if (l == 0) { s2.frame[q] = (int)f; s2.nanchor[q] = na; out.stage[f] = 1; }
+            }
+        }
+        __syncwarp();
+    }
+}

@@ -122,3 +122,27 @@ def test_mp_wsd_random_anchors_vs_oracle(variant):
     ok = np.setdiff1d(np.arange(F), risky)
     np.testing.assert_array_equal(_np(o["iters"])[ok], r["iters"][ok])
     np.testing.assert_array_equal(_np(o["hops"])[ok], r["hops"][ok])
+
+
+@pytest.mark.parametrize("generic", [0, 1])
+@pytest.mark.parametrize("name", ["cfg1", "cfg3", "cfg4"])
+def test_scl_kernels_agree_bit_exact(name, generic):
+    """Lane-per-path and warp-per-frame stage-1 kernels give identical lists."""
+    import ctypes
+    from paper_2602_08501_b200 import _native, channel
+    cfg = configs.CONFIGS[name]
+    code = cfg.code()
+    inner = code.inner
+    sigma = cfg.sigma(code=code)
+    _, _, y = channel.bulk_inputs(code, 21, 0, 0, 512, sigma)
+    dec = DeviceDecoder(inner)
+    _native.check(_native.lib().mpw_set_option(dec._h, b"scl_generic", generic))
+    o = dec.scl_batch(y=y, sigma=sigma, list_size=cfg.list_size)
+    llr = 2.0 * y.astype(np.float64) / (sigma * sigma)
+    for f in range(0, 512, 37):
+        u, cw, pm = orc.scl(llr[f], inner.info_set, code.n, cfg.list_size)
+        c = int(o["list_n"][f].item())
+        assert c == cw.shape[0]
+        got = words32_to_64(o["list_cw"][f, :c].cpu().numpy().view(np.uint32), code.n)
+        np.testing.assert_array_equal(got, cw)
+        np.testing.assert_array_equal(o["list_pm"][f, :c].cpu().numpy(), pm)

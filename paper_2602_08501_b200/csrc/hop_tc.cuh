@@ -31,8 +31,9 @@ constexpr int NT_COLS = 256;     // UMMA N (patterns per tile)
 constexpr int KBLK = 64;         // fp16 elements per 128-byte swizzle row
 constexpr int B_STAGE_BYTES = NT_COLS * KBLK * 2;    // 32 KB
 constexpr int A_KBLK_BYTES = ROWS * KBLK * 2;        // 16 KB
-constexpr int THREADS = 192;
-constexpr int EPI_THREADS = 128;
+constexpr int EPI_WARPS = 8;     // two per TMEM lane quarter, each scans half of a tile
+constexpr int EPI_THREADS = 32 * EPI_WARPS;
+constexpr int THREADS = 64 + EPI_THREADS;
 
 constexpr int SMEM_LIMIT = 232448;   // 227 KB opt-in maximum per CTA
 #ifndef MPW_TC_TOPK
@@ -96,13 +97,13 @@ __device__ __forceinline__ void tc_mma_f16(uint32_t d_tmem, uint64_t adesc, uint
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ void epi_bar_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+__device__ __forceinline__ void epi_bar_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 __device__ __forceinline__ int epi_bar_or(int pred) {
     int r;
     asm volatile(
         "{\n\t.reg .pred p, q;\n\t"
         "setp.ne.s32 p, %1, 0;\n\t"
-        "bar.red.or.pred q, 2, 128, p;\n\t"
+        "bar.red.or.pred q, 2, 256, p;\n\t"
         "selp.s32 %0, 1, 0, q;\n\t}"
         : "=r"(r)
         : "r"(pred)
@@ -181,7 +182,7 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; s++) { mbar_init(smem_u32(&full[s]), 1); mbar_init(smem_u32(&empty[s]), 1); }
-        for (int b = 0; b < 2; b++) { mbar_init(smem_u32(&tfull[b]), 1); mbar_init(smem_u32(&tempty[b]), 4); }
+        for (int b = 0; b < 2; b++) { mbar_init(smem_u32(&tfull[b]), 1); mbar_init(smem_u32(&tempty[b]), EPI_WARPS); }
         mbar_init(smem_u32(go), 1);
         *done_flag = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -252,9 +253,17 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
             }
         }
     } else {
-        // ===== epilogue: one trajectory row per thread =====
+        // ===== epilogue: two threads per trajectory row =====
+        // warp w in 2..9 reads TMEM lane quarter w % 4; warps 2..5 (primary) scan
+        // columns [0,128) of every tile and own the row state, warps 6..9
+        // (secondary) scan columns [128,256) and hand their top-K over at the end
+        // of each round through the (then idle) B ring.
         const int g = warp & 3;                  // TMEM lane quarter accessible to this warp
         const int row = g * 32 + lane;
+        const bool primary = warp < 6;
+        const int ch0 = primary ? 0 : (NT_COLS / 32) / 2;
+        float* xv = reinterpret_cast<float*>(b_ring);                      // [128][TOPK]
+        int* xi = reinterpret_cast<int*>(b_ring + ROWS * TOPK * sizeof(float));
         const uint32_t t_lane = tmem_base + ((uint32_t)(g * 32) << 16);
         const int count = *prm.s2.count;
         const long long ntraj = (long long)count * A;
@@ -325,10 +334,10 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
             prm.s2.traj_flags[tr] = flags;
         };
 
-        load_row();
+        if (primary) load_row();
         fence_proxy_async();
         int any = epi_bar_or(active);
-        if (row == 0) {
+        if (primary && row == 0) {
             *done_flag = any ? 0 : 1;
             mbar_arrive(smem_u32(go));
         }
@@ -344,7 +353,7 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
                 const int pbase = j * NT_COLS;
                 const bool tail = pbase + NT_COLS > np_;
 #pragma unroll 1
-                for (int ch = 0; ch < NT_COLS / 32; ch++) {
+                for (int ch = ch0; ch < ch0 + (NT_COLS / 32) / 2; ch++) {
                     uint32_t v[32];
                     TC_LD32(t_lane + buf * NT_COLS + ch * 32, v);
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
@@ -387,7 +396,24 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
                 __syncwarp();
                 if (lane == 0) mbar_arrive(smem_u32(&tempty[buf]));
             }
-            // ---- end of a full scan of P: decide, move, refill
+            // ---- end of a full scan of P: merge the two column halves, then
+            // decide, move, refill (the MMA of the round is complete, so the B
+            // ring is idle and serves as the exchange buffer)
+            if (!primary) {
+#pragma unroll
+                for (int k = 0; k < TOPK; k++) { xv[row * TOPK + k] = top.b[k]; xi[row * TOPK + k] = top.i[k]; }
+            }
+            epi_bar_sync();
+            if (primary) {
+#pragma unroll
+                for (int k = 0; k < TOPK; k++) {
+                    const float s = xv[row * TOPK + k];
+                    if (s < lastv) {
+                        top.insert_inline(s, xi[row * TOPK + k]);
+                        lastv = top.last();
+                    }
+                }
+            }
             if (active) {
                 iters++;
                 int i1;
@@ -422,7 +448,7 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
             }
             fence_proxy_async();
             any = epi_bar_or(active);
-            if (row == 0) {
+            if (primary && row == 0) {
                 *done_flag = any ? 0 : 1;
                 mbar_arrive(smem_u32(go));
             }

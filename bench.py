@@ -47,6 +47,20 @@ def _peaks():
             "sm_max_mhz": 1965.0}, "fallback"
 
 
+def _ncu_traffic(key):
+    """DRAM bytes (read + write) per launch of the dominant kernel from one
+    committed `ncu --set full` capture of the same command
+    (profiles/ncu_traffic.json), or None when no capture exists."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        e = d.get(key)
+        return None if e is None else {"bytes": e["bytes"], "source": e["source"]}
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 class ClockSampler:
     """nvidia-smi clocks and throttle reasons during the timed region."""
 
@@ -307,7 +321,8 @@ def main():
             ach = flop / (hop_ms / 1000.0) / 1e12
             peak = peaks["bf16_tflops"]
             roof = {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
-                    "frac": ach / peak, "traffic": None, "kernel": f"hop_tc_kernel<LIMBS={limbs}>",
+                    "frac": ach / peak, "traffic": _ncu_traffic(f"hop_tc_{limbs}limb_{args.frames}"),
+                    "kernel": f"hop_tc_kernel<LIMBS={limbs}>",
                     "flop_per_eval": 2 * limbs * code.n,
                     "peak_source": f"{peak_kind} bf16_tflops (burst cuBLAS 8192^3)"}
         else:
@@ -335,7 +350,8 @@ def main():
                 "near_tie_frames": int(ctr[5]),
                 "uncertified_frames": int(ctr[6]),
                 "clocks": clocks.summary(),
-                "gpu_launches": int(4 * args.steps),
+                # per step: scl, ebound, hop, finalize, frame (memsets are not kernels)
+                "gpu_launches": int(5 * args.steps),
                 "e2e": e2e}
         if not args.no_cpu:
             threads = os.cpu_count() or 1

@@ -20,6 +20,7 @@
 #pragma once
 #include <cuda_fp16.h>
 
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -122,6 +123,12 @@ __device__ __forceinline__ int epi_bar_or(int pred) {
           "=r"(v[29]), "=r"(v[30]), "=r"(v[31])                                                             \
         : "r"(taddr))
 
+__device__ __forceinline__ float fmin3(float a, float b, float c) {
+    float r;
+    asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+
 // v[e] for a runtime e without local memory: 5-level select tree (31 SEL)
 __device__ __forceinline__ float select32(const uint32_t (&v)[32], int e) {
     uint32_t a[16];
@@ -156,6 +163,7 @@ struct Params {
     const uint8_t* btiles;       // [ntiles][KB][256 x 64 fp16] swizzled images
     float tie_rel;
     float err;             // bound on |S_fp32 - S_exact| (S units)
+    int experiment;        // profiling knob: 1 skip epilogue math, 2 skip TMEM loads, 4 force T scans
 };
 
 // ---------------------------------------------------------------------------
@@ -342,40 +350,43 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
             mbar_arrive(smem_u32(go));
         }
         uint32_t gtile = 0;
+        const bool dbg_on = (prm.experiment & 8) && blockIdx.x == 0 && primary && row == 0;
+        long long t_scan = 0, t_round = 0, t_mark = 0, t_scan0 = 0, n_rounds = 0;
         while (any) {
+            if (dbg_on) t_scan0 = clock64();
             TopK<TOPK> top;
             top.reset();
-            float lastv = CUDART_INF_F;   // register copy of top.last()
+            // insertion threshold: the K-th best, but never above best + window --
+            // candidates outside the certification window of the running best can
+            // never be needed (running best >= final best)
+            const float wadd = 2.0f * err_row + prm.tie_rel * ed * 0.25f;
+            float lastv = CUDART_INF_F;   // min(top.last(), top.b[0] + wadd)
             for (int j = 0; j < ntiles; j++, gtile++) {
                 const uint32_t buf = gtile & 1;
                 mbar_wait(smem_u32(&tfull[buf]), (gtile >> 1) & 1);
                 tc_fence_after();
                 const int pbase = j * NT_COLS;
                 const bool tail = pbase + NT_COLS > np_;
-#pragma unroll 1
-                for (int ch = ch0; ch < ch0 + (NT_COLS / 32) / 2; ch++) {
-                    uint32_t v[32];
-                    TC_LD32(t_lane + buf * NT_COLS + ch * 32, v);
-                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                    const int p0 = pbase + ch * 32;
+                // per-chunk reduction: min tree, then (rarely) exact top-K insertion
+                auto process = [&](uint32_t (&v)[32], int p0) {
                     if (tail) {
 #pragma unroll
                         for (int e = 0; e < 32; e++)
                             if (p0 + e >= np_) v[e] = __float_as_uint(CUDART_INF_F);
                     }
-                    // fast path: chunk minimum by a tree; exact scan only if it can
-                    // change the best or the runner-up
-                    // min tree; level 2 keeps 8 group minima, group g = {g, g+8, g+16, g+24}
-                    float m1[16], m2[8];
+                    // chunk minimum with 3-input FMNMX3: 16 instructions for 32 values
+                    float m3[11];
 #pragma unroll
-                    for (int e = 0; e < 16; e++) m1[e] = fminf(__uint_as_float(v[e]), __uint_as_float(v[e + 16]));
-#pragma unroll
-                    for (int e = 0; e < 8; e++) m2[e] = fminf(m1[e], m1[e + 8]);
-                    const float mn = fminf(fminf(fminf(m2[0], m2[1]), fminf(m2[2], m2[3])),
-                                           fminf(fminf(m2[4], m2[5]), fminf(m2[6], m2[7])));
-                    // slow path (rare per lane): mask of values below the current 4th
-                    // best, then insert them in increasing index order (ties keep the
-                    // lowest index); register values are picked by a select tree
+                    for (int e = 0; e < 10; e++)
+                        m3[e] = fmin3(__uint_as_float(v[3 * e]), __uint_as_float(v[3 * e + 1]),
+                                      __uint_as_float(v[3 * e + 2]));
+                    m3[10] = fminf(__uint_as_float(v[30]), __uint_as_float(v[31]));
+                    const float q0 = fmin3(m3[0], m3[1], m3[2]), q1 = fmin3(m3[3], m3[4], m3[5]);
+                    const float q2 = fmin3(m3[6], m3[7], m3[8]), q3 = fminf(m3[9], m3[10]);
+                    const float mn = fminf(fmin3(q0, q1, q2), q3);
+                    // slow path (rare per lane): mask of values below the current K-th
+                    // best, inserted in increasing index order (ties keep the lowest
+                    // index); register values are picked by a select tree
                     if (mn < lastv) {
                         uint32_t hits = 0;
 #pragma unroll
@@ -384,18 +395,39 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
                         while (hits) {
                             const int e = __ffs(hits) - 1;
                             hits &= hits - 1;
-                            const float s = select32(v, e);
-                            if (s < lastv) {
-                                top.insert_inline(s, p0 + e);
-                                lastv = top.last();
+                            const float sv = select32(v, e);
+                            if (sv < lastv) {
+                                top.insert_inline(sv, p0 + e);
+                                lastv = fminf(top.last(), top.b[0] + wadd);
                             }
                         }
                     }
+                };
+                // TMEM loads double-buffered: chunk k+1 is in flight while chunk k reduces
+                constexpr int NCH = (NT_COLS / 32) / 2;
+                const uint32_t tbase = t_lane + buf * NT_COLS + ch0 * 32;
+                uint32_t va[32], vb[32];
+                if (prm.experiment & 2) {
+#pragma unroll
+                    for (int e = 0; e < 32; e++) { va[e] = __float_as_uint(1.0f); vb[e] = va[e]; }
+                } else {
+                    TC_LD32(tbase, va);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                }
+#pragma unroll
+                for (int k = 0; k < NCH; k++) {
+                    uint32_t (&cur)[32] = (k & 1) ? vb : va;
+                    uint32_t (&nxt)[32] = (k & 1) ? va : vb;
+                    if (k + 1 < NCH && !(prm.experiment & 2)) TC_LD32(tbase + (k + 1) * 32, nxt);
+                    if (!(prm.experiment & 1)) process(cur, pbase + (ch0 + k) * 32);
+                    if (k + 1 < NCH && !(prm.experiment & 2))
+                        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                 }
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(smem_u32(&tempty[buf]));
             }
+            if (dbg_on) { t_mark = clock64(); t_scan += t_mark - t_scan0; }
             // ---- end of a full scan of P: merge the two column halves, then
             // decide, move, refill (the MMA of the round is complete, so the B
             // ring is idle and serves as the exchange buffer)
@@ -410,7 +442,7 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
                     const float s = xv[row * TOPK + k];
                     if (s < lastv) {
                         top.insert_inline(s, xi[row * TOPK + k]);
-                        lastv = top.last();
+                        lastv = fminf(top.last(), top.b[0] + wadd);
                     }
                 }
             }
@@ -439,7 +471,7 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
                     ed += 4.f * sb;
                     if (prm.s2.traj_hops) prm.s2.traj_hops[(size_t)tr * T + iters - 1] = i1 + 1;
                 }
-                if (!improve || iters == T) {
+                if ((!improve && !(prm.experiment & 4)) || iters == T) {
                     if (prm.s2.traj_hops)
                         for (int h = iters - (improve ? 0 : 1); h < T; h++) prm.s2.traj_hops[(size_t)tr * T + h] = -1;
                     store_row();
@@ -448,11 +480,13 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
             }
             fence_proxy_async();
             any = epi_bar_or(active);
+            if (dbg_on) { t_round += clock64() - t_mark; n_rounds++; }
             if (primary && row == 0) {
                 *done_flag = any ? 0 : 1;
                 mbar_arrive(smem_u32(go));
             }
         }
+        if (dbg_on) printf("[hop_tc dbg] rounds=%lld scan_cycles=%lld roundend_cycles=%lld\n", n_rounds, t_scan, t_round);
     }
     tc_fence_before();
     __syncthreads();
@@ -466,6 +500,11 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
 
 // ---------------------------------------------------------------------------
 // host side
+
+inline int tc_experiment() {
+    const char* e = getenv("MPW_TC_EXPERIMENT");
+    return e ? atoi(e) : 0;
+}
 
 struct TcPatterns {
     bool ready = false;
@@ -511,6 +550,7 @@ inline int tc_launch_t(const TcPatterns& t, int n, int nw, int A, int T, const f
     prm.n = n; prm.nw = nw; prm.A = A; prm.T = T; prm.np = t.np; prm.ntiles = t.ntiles;
     prm.y = y; prm.s2 = s2; prm.pbits = P.bits; prm.btiles = t.tiles; prm.tie_rel = 1e-5f;
     prm.err = 2e-3f;
+    prm.experiment = tc_experiment();
     const size_t smem = tc::smem_bytes(KB, LIMBS);
     if (cudaFuncSetAttribute(tc::hop_tc_kernel<KB, NW, LIMBS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return -1;

@@ -126,7 +126,41 @@ def gen_scl(name, frames, seed=7):
     print(f"scl_{name}: {frames} frames")
 
 
+DEMO_CFG = """
+code_family = ca_polar
+code_n = 64
+code_k = 16
+snr_db_grid = 0.0, 1.0, 2.0, 3.0, 4.0
+stage1 = scl
+scl_list_size = 4
+wsd_radius_index = {r}
+wsd_num_paths = {paths}
+activation_mode = crc_gated
+max_trials = 4000
+min_block_errors = 100
+seed = 99
+"""
+
+
+def gen_sweeps():
+    """The reference's own run_sweep on its desk-scale demo configuration
+    (demos/bler_sweep_small.py), written with its own write_csv."""
+    from feclab.simharness import parse_config, run_sweep, write_csv
+    code = fcb.build_ca_polar_code(64, 16)
+    for r, paths, name in ((2, 4, "sweep_two_stage.csv"), (0, 1, "sweep_stage1.csv")):
+        cfg_text = DEMO_CFG.format(r=r, paths=paths)
+        with open(os.path.join(HERE, name.replace(".csv", ".cfg")), "w") as fh:
+            fh.write(cfg_text.lstrip())
+        t0 = time.time()
+        recs = run_sweep(parse_config(cfg_text), sphere=build_sphere(code, r))
+        write_csv(recs, os.path.join(HERE, name))
+        print(f"{name}: {time.time() - t0:.1f}s")
+
+
 if __name__ == "__main__":
+    if "--sweeps" in sys.argv:
+        gen_sweeps()
+        sys.exit(0)
     for nm, fr in (("cfg1", 64), ("cfg2", 16), ("cfg3", 32), ("cfg4", 8)):
         gen_scl(nm, fr)
     gen_two_stage("cfg1", 400)

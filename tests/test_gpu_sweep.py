@@ -1,0 +1,23 @@
+"""The batched GPU sweep reproduces the reference's own run_sweep CSVs byte
+for byte (golden CSVs made by tests/golden/make_golden.py --sweeps, which the
+reference writes identically to its shipped demos/sweep_*.csv)."""
+import os
+
+import pytest
+
+from paper_2602_08501_b200 import sweep
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.mark.parametrize("name", ["sweep_two_stage", "sweep_stage1"])
+def test_gpu_sweep_csv_matches_reference_bytes(name, tmp_path):
+    cfg = sweep.load_config(os.path.join(GOLDEN, name + ".cfg"))
+    recs = sweep.run_sweep(cfg, batch=4096)
+    out = tmp_path / (name + ".csv")
+    sweep.write_csv(recs, out)
+    with open(os.path.join(GOLDEN, name + ".csv"), "rb") as fh:
+        want = fh.read()
+    assert out.read_bytes() == want
+    assert all(r.uncertified_frames == 0 for r in recs)

@@ -139,6 +139,15 @@ int mpw_set_timing(mpw_handle* h, int enable);
 int mpw_set_option(mpw_handle* h, const char* key, int value);
 int mpw_read_timing(mpw_handle* h, double* ms_out, long long* launches_out, int reset);
 
+/* Device-side channel generator for bulk sweeps: frames [first_frame,
+ * first_frame + F) of the counter-based Philox4x32-10 stream (seed, snr_idx):
+ * uniform message bits, codeword through the code's generator, BPSK + AWGN
+ * (float64 Box-Muller, rounded to float32).  Outputs (device): y F x n,
+ * tx F x nw (may be NULL), msg F (k <= 64, may be NULL).  Mirrors
+ * paper_2602_08501_b200.channel.keyed_inputs_host. */
+int mpw_channel_batch(mpw_handle* h, uint64_t seed, int snr_idx, long long first_frame, int F,
+                      double sigma, float* y, uint32_t* tx, uint64_t* msg, void* stream);
+
 int mpw_num_patterns(mpw_handle* h);
 int mpw_tensor_path_ready(mpw_handle* h);
 

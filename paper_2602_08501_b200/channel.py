@@ -89,3 +89,64 @@ def bulk_inputs(code, seed: int, snr_idx: int, first_frame: int, frames: int, si
     cw = np.concatenate([p[1] for p in parts])
     y = np.concatenate([p[2] for p in parts])
     return msgs, cw, y
+
+
+# ---------------------------------------------------------------------------
+# Counter-based keyed stream shared with the device generator (csrc/channel.cuh)
+
+_PH_M0, _PH_M1 = np.uint64(0xD2511F53), np.uint64(0xCD9E8D57)
+_PH_W0, _PH_W1 = np.uint32(0x9E3779B9), np.uint32(0xBB67AE85)
+_PH_TAG = np.uint32(0x4D505753)
+_U32 = np.uint64(0xFFFFFFFF)
+
+
+def philox4x32_10(c0, c1, c2, c3, k0, k1):
+    """Vectorised Philox4x32-10 (Random123 constants); uint32 arrays in/out."""
+    c0, c1, c2, c3 = (np.asarray(x, dtype=np.uint32) for x in (c0, c1, c2, c3))
+    k0 = np.uint32(k0)
+    k1 = np.uint32(k1)
+    with np.errstate(over="ignore"):
+        for _ in range(10):
+            p0 = _PH_M0 * c0.astype(np.uint64)
+            p1 = _PH_M1 * c2.astype(np.uint64)
+            hi0, lo0 = (p0 >> np.uint64(32)).astype(np.uint32), (p0 & _U32).astype(np.uint32)
+            hi1, lo1 = (p1 >> np.uint64(32)).astype(np.uint32), (p1 & _U32).astype(np.uint32)
+            c0, c1, c2, c3 = hi1 ^ c1 ^ k0, lo1, hi0 ^ c3 ^ k1, lo0
+            k0 = np.uint32(k0 + _PH_W0)
+            k1 = np.uint32(k1 + _PH_W1)
+    return c0, c1, c2, c3
+
+
+def keyed_inputs_host(code, seed: int, snr_idx: int, first_frame: int, frames: int, sigma: float):
+    """numpy mirror of mpw_channel_batch: (msg_words uint64 [F], codeword words
+    uint64 [F, W64], y float32 [F, N]).  The device computes log / sincospi
+    in float64 with its own libm, so a y value can differ by 1 float32 ulp in
+    rare cases (rounding ties after ~1e-16 relative differences)."""
+    n, k = code.n, code.k
+    g = np.arange(first_frame, first_frame + frames, dtype=np.uint64)
+    glo = (g & _U32).astype(np.uint32)
+    ghi = (g >> np.uint64(32)).astype(np.uint32)
+    k0 = np.uint32(seed & 0xFFFFFFFF)
+    with np.errstate(over="ignore"):
+        k1 = np.uint32((seed >> 32) & 0xFFFFFFFF) ^ np.uint32((snr_idx * 0x9E3779B9) & 0xFFFFFFFF)
+    z = np.zeros_like(glo)
+    m0, m1, m2, m3 = philox4x32_10(glo, ghi, z, np.full_like(glo, _PH_TAG), k0, k1)
+    words = np.stack([m0, m1, m2, m3], axis=1).view("<u4")
+    msg_bits = np.unpackbits(words.view(np.uint8), axis=1, bitorder="little")[:, :k]
+    msg = (msg_bits.astype(np.uint64) << np.arange(k, dtype=np.uint64)).sum(axis=1, dtype=np.uint64) \
+        if k <= 64 else None
+    cw = encode_batch(code, msg_bits)
+    x = modulate_words(cw, n)
+    nz = np.zeros((frames, n), dtype=np.float64)
+    for c in range((n + 3) // 4):
+        r0, r1, r2, r3 = philox4x32_10(glo, ghi, np.full_like(glo, 1 + c), np.full_like(glo, _PH_TAG), k0, k1)
+        for h, (a, b) in enumerate(((r0, r1), (r2, r3))):
+            u1 = (a.astype(np.float64) + 0.5) * 2.3283064365386963e-10
+            u2 = (b.astype(np.float64) + 0.5) * 2.3283064365386963e-10
+            rad = np.sqrt(-2.0 * np.log(u1))
+            ang = 2.0 * np.pi * u2
+            for q, val in ((4 * c + 2 * h, rad * np.cos(ang)), (4 * c + 2 * h + 1, rad * np.sin(ang))):
+                if q < n:
+                    nz[:, q] = val
+    y = (x + sigma * nz).astype(np.float32)
+    return msg, cw, y

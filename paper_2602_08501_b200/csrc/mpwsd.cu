@@ -21,6 +21,7 @@
 #include "hop_tc.cuh"
 #include "scl.cuh"
 #include "scl_lane.cuh"
+#include "channel.cuh"
 
 namespace {
 
@@ -720,6 +721,21 @@ int mpw_two_stage_batch_host(mpw_handle* h, const float* y_host, int F, double s
     if (flags_host) CK(cudaMemcpyAsync(flags_host, dflags.p, F, cudaMemcpyDeviceToHost, st));
     if (counters_host) CK(cudaMemcpyAsync(counters_host, dctr.p, sizeof(unsigned long long) * MPW_NUM_COUNTERS, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    return 0;
+}
+
+int mpw_channel_batch(mpw_handle* h, uint64_t seed, int snr_idx, long long first_frame, int F, double sigma,
+                      float* y, uint32_t* tx, uint64_t* msg, void* stream) {
+    if (!h || !y || F < 0 || first_frame < 0 || !(sigma > 0)) return fail(MPW_ERR_ARG, "bad arguments");
+    if (!h->has_code) return fail(MPW_ERR_STATE, "no code set");
+    if (F == 0) return 0;
+    if (set_device(h)) return MPW_ERR_CUDA;
+    ChannelArgs a;
+    a.code = code_dev(h); a.seed = seed; a.snr_idx = (uint32_t)snr_idx; a.first_frame = first_frame;
+    a.F = F; a.sigma = sigma; a.y = y; a.tx = tx; a.msg = msg;
+    const int grid = std::max(1, std::min((F + 7) / 8, h->num_sms * 32));
+    channel_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(a);
+    CK(cudaGetLastError());
     return 0;
 }
 

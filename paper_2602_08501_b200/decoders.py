@@ -606,3 +606,19 @@ def _as_candidates(entries: list) -> CandidateList:
     lst = CandidateList.__new__(CandidateList)
     lst.entries = entries
     return lst
+
+
+def device_channel(dec: DeviceDecoder, seed: int, snr_idx: int, first_frame: int, frames: int,
+                   sigma: float, stream=None):
+    """Device-resident inputs from the counter-based generator (mpw_channel_batch):
+    returns (y float32 [F,N], tx int32 words [F,nw], msg int64 [F]) on dec.device."""
+    torch = _torch()
+    d = dec.device
+    y = torch.empty((frames, dec.n), dtype=torch.float32, device=d)
+    tx = torch.empty((frames, dec.nw), dtype=torch.int32, device=d)
+    msg = torch.empty((frames,), dtype=torch.int64, device=d)
+    rc = _native.lib().mpw_channel_batch(dec._h, ctypes.c_uint64(seed), int(snr_idx), int(first_frame),
+                                         int(frames), float(sigma), _ptr(y), _ptr(tx), _ptr(msg),
+                                         dec._stream(stream))
+    _native.value_error_check(rc, "mpw_channel_batch")
+    return y, tx, msg

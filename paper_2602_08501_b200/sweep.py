@@ -233,9 +233,17 @@ def _scan_cost(n, sphere_size, support_total, m):
     return (m_eff, gain, sort, n + m_eff)
 
 
-def run_sweep(cfg: ExperimentConfig, sphere=None, batch: int = 8192, device=None, variant="auto"):
-    """simharness.run_sweep (decoder_kind='two_stage') over the GPU path."""
-    from .decoders import DeviceDecoder, default_filter_size, words32_to_64
+def run_sweep(cfg: ExperimentConfig, sphere=None, batch: int = 8192, device=None, variant="auto",
+              input_mode: str = "trial", on_batch=None):
+    """simharness.run_sweep (decoder_kind='two_stage') over the GPU path.
+
+    input_mode 'trial' reproduces the reference's per-trial streams (host
+    numpy, byte-identical CSVs); 'device' draws the counter-based stream on
+    the GPU (mpw_channel_batch) for 10^6-10^7-trial points; `on_batch(snr_idx,
+    first_trial, y, tx, outputs)` sees every device batch (oracle subsamples)."""
+    from .decoders import DeviceDecoder, default_filter_size, device_channel, words32_to_64
+    if input_mode not in ("trial", "device"):
+        raise ConfigError(f"unknown input mode {input_mode!r}")
     from .patterns import enumerate_sphere
     from .sphere import load_sphere
 
@@ -262,11 +270,18 @@ def run_sweep(cfg: ExperimentConfig, sphere=None, batch: int = 8192, device=None
         t0 = 0
         while not done:
             cnt = min(batch, cfg.max_trials - t0)
-            _, tx, y = trial_inputs(code, cfg.seed, snr_idx, range(t0, t0 + cnt), sigma)
-            y32 = y.astype(np.float32)
-            o = dec.two_stage_batch(y32, sigma, L, A, T, cfg.activation_mode, variant=variant)
-            best = words32_to_64(o["best"].cpu().numpy().view(np.uint32), n)
-            err = (best != tx).any(axis=1)
+            if input_mode == "trial":
+                _, tx, y = trial_inputs(code, cfg.seed, snr_idx, range(t0, t0 + cnt), sigma)
+                y32 = y.astype(np.float32)
+                o = dec.two_stage_batch(y32, sigma, L, A, T, cfg.activation_mode, variant=variant)
+                best = words32_to_64(o["best"].cpu().numpy().view(np.uint32), n)
+                err = (best != tx).any(axis=1)
+            else:   # device-resident counter-based inputs (mpw_channel_batch)
+                yd, txd, _ = device_channel(dec, cfg.seed, snr_idx, t0, cnt, sigma)
+                o = dec.two_stage_batch(yd, sigma, L, A, T, cfg.activation_mode, variant=variant)
+                err = (o["best"] != txd).any(dim=1).cpu().numpy()
+                if on_batch is not None:
+                    on_batch(snr_idx, t0, yd, txd, o)
             stage = o["stage"].cpu().numpy()
             iters = o["iters"].cpu().numpy()
             flags = o["flags"].cpu().numpy()

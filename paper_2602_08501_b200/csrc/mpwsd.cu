@@ -614,7 +614,9 @@ int mpw_set_patterns(mpw_handle* h, const uint64_t* pattern_words, int np) {
 
 int mpw_scl_batch(mpw_handle* h, const float* y, const double* llr, int F, double sigma, int L,
                   int32_t* list_n, uint32_t* list_u, uint32_t* list_cw, double* list_pm, void* stream) {
-    if (!h || (!y && !llr) || F < 0) return fail(MPW_ERR_ARG, "bad arguments");
+    if (!h || F < 0) return fail(MPW_ERR_ARG, "bad arguments");
+    if (F == 0) return 0;
+    if (!y && !llr) return fail(MPW_ERR_ARG, "bad arguments");
     if (!h->has_code) return fail(MPW_ERR_STATE, "no code set");
     if (L < 1 || L > SCL_MAX_L) return fail(MPW_ERR_UNSUPPORTED, "list size %d outside [1,%d]", L, SCL_MAX_L);
     if (F == 0) return 0;
@@ -628,7 +630,9 @@ int mpw_scl_batch(mpw_handle* h, const float* y, const double* llr, int F, doubl
 int mpw_mpwsd_batch(mpw_handle* h, const float* y, const uint32_t* anchors, const int32_t* n_anchor,
                     int F, int A, int T, int variant, uint32_t* best, double* best_ed,
                     int32_t* iters, int32_t* hops, uint8_t* flags, void* stream) {
-    if (!h || !y || !anchors || !best || !best_ed || F < 0 || A < 1 || T < 1) return fail(MPW_ERR_ARG, "bad arguments");
+    if (!h || F < 0 || A < 1 || T < 1) return fail(MPW_ERR_ARG, "bad arguments");
+    if (F == 0) return 0;
+    if (!y || !anchors || !best || !best_ed) return fail(MPW_ERR_ARG, "bad arguments");
     if (!h->has_pat) return fail(MPW_ERR_STATE, "no pattern set");
     if (F == 0) return 0;
     if (set_device(h)) return MPW_ERR_CUDA;
@@ -648,7 +652,9 @@ int mpw_two_stage_batch(mpw_handle* h, const float* y, int F, double sigma, int 
                         int mode, int variant, const uint32_t* tx_cw, uint32_t* best, uint64_t* best_msg,
                         double* best_ed, uint8_t* stage, int32_t* iters, int32_t* hops,
                         uint32_t* anchors_out, uint8_t* flags, unsigned long long* counters, void* stream) {
-    if (!h || !y || !best || !best_ed || !stage || F < 0 || A < 1 || T < 1) return fail(MPW_ERR_ARG, "bad arguments");
+    if (!h || F < 0 || A < 1 || T < 1) return fail(MPW_ERR_ARG, "bad arguments");
+    if (F == 0) return 0;
+    if (!y || !best || !best_ed || !stage) return fail(MPW_ERR_ARG, "bad arguments");
     if (!h->has_code || !h->has_pat) return fail(MPW_ERR_STATE, "code and pattern set must be set first");
     if (L < 1 || L > SCL_MAX_L) return fail(MPW_ERR_UNSUPPORTED, "list size %d outside [1,%d]", L, SCL_MAX_L);
     if (mode != MPW_MODE_CRC_GATED && mode != MPW_MODE_ALWAYS_ON) return fail(MPW_ERR_ARG, "unknown activation mode %d", mode);
@@ -690,7 +696,9 @@ int mpw_two_stage_batch_host(mpw_handle* h, const float* y_host, int F, double s
                              int mode, int variant, const uint32_t* tx_host, uint32_t* best_host,
                              uint64_t* msg_host, double* ed_host, uint8_t* stage_host, int32_t* iters_host,
                              uint8_t* flags_host, unsigned long long* counters_host, void* stream) {
-    if (!h || !y_host || F < 0) return fail(MPW_ERR_ARG, "bad arguments");
+    if (!h || F < 0) return fail(MPW_ERR_ARG, "bad arguments");
+    if (F == 0) return 0;
+    if (!y_host) return fail(MPW_ERR_ARG, "bad arguments");
     if (F == 0) return 0;
     if (set_device(h)) return MPW_ERR_CUDA;
     cudaStream_t st = (cudaStream_t)stream;
@@ -726,7 +734,9 @@ int mpw_two_stage_batch_host(mpw_handle* h, const float* y_host, int F, double s
 
 int mpw_channel_batch(mpw_handle* h, uint64_t seed, int snr_idx, long long first_frame, int F, double sigma,
                       float* y, uint32_t* tx, uint64_t* msg, void* stream) {
-    if (!h || !y || F < 0 || first_frame < 0 || !(sigma > 0)) return fail(MPW_ERR_ARG, "bad arguments");
+    if (!h || F < 0 || first_frame < 0 || !(sigma > 0)) return fail(MPW_ERR_ARG, "bad arguments");
+    if (F == 0) return 0;
+    if (!y) return fail(MPW_ERR_ARG, "bad arguments");
     if (!h->has_code) return fail(MPW_ERR_STATE, "no code set");
     if (F == 0) return 0;
     if (set_device(h)) return MPW_ERR_CUDA;

@@ -154,6 +154,14 @@ int mpw_tensor_path_ready(mpw_handle* h);
 /* Host-side pattern-set generation (off the timed path). */
 int64_t mpw_enumerate_lowweight(const uint64_t* gen, int k, int n, int cap, int64_t* spectrum,
                                 uint64_t* out, int64_t out_cap, int nthreads);
+/* Same on the GPU (exhaustive, k <= 40) for the code set on `h`: the reference's
+ * enumerate_spectrum / build_sphere (wsphere.py:115-208).  spectrum[n+1]
+ * (host, may be NULL) gets the full weight distribution A_w; out (host,
+ * out_cap x ceil(n/64) words) the codewords with 1 <= weight <= cap, in no
+ * particular order (the caller sorts into CWS1 member order).  Returns the
+ * number of such codewords (may exceed out_cap: only out_cap are written). */
+int64_t mpw_enumerate_lowweight_gpu(mpw_handle* h, int cap, int64_t* spectrum, uint64_t* out,
+                                    int64_t out_cap);
 int64_t mpw_collect_lowweight(const uint64_t* gen, int k, int n, int cap, int64_t iterations,
                               uint64_t seed, int p_max, uint64_t* out, int64_t out_cap,
                               int nthreads);

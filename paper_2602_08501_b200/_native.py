@@ -45,6 +45,7 @@ _SIGS = {
                                   c_void_p, c_void_p, c_void_p, c_void_p]),
     "mpw_tensor_path_ready": (c_int, [c_void_p]),
     "mpw_enumerate_lowweight": (c_int64, [c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_int64, c_int]),
+    "mpw_enumerate_lowweight_gpu": (c_int64, [c_void_p, c_int, c_void_p, c_void_p, c_int64]),
     "mpw_collect_lowweight": (c_int64, [c_void_p, c_int, c_int, c_int, c_int64, c_uint64, c_int,
                                         c_void_p, c_int64, c_int]),
 }

@@ -22,6 +22,7 @@
 #include "scl.cuh"
 #include "scl_lane.cuh"
 #include "channel.cuh"
+#include "enum.cuh"
 
 namespace {
 
@@ -738,7 +739,6 @@ int mpw_channel_batch(mpw_handle* h, uint64_t seed, int snr_idx, long long first
     if (F == 0) return 0;
     if (!y) return fail(MPW_ERR_ARG, "bad arguments");
     if (!h->has_code) return fail(MPW_ERR_STATE, "no code set");
-    if (F == 0) return 0;
     if (set_device(h)) return MPW_ERR_CUDA;
     ChannelArgs a;
     a.code = code_dev(h); a.seed = seed; a.snr_idx = (uint32_t)snr_idx; a.first_frame = first_frame;
@@ -747,6 +747,83 @@ int mpw_channel_batch(mpw_handle* h, uint64_t seed, int snr_idx, long long first
     channel_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(a);
     CK(cudaGetLastError());
     return 0;
+}
+
+extern "C++" {
+namespace {
+template <int NW>
+cudaError_t launch_enum(const mpw_handle* h, int lb, const uint32_t* table, int cap, unsigned long long* spec,
+                        uint32_t* out, unsigned long long* cnt, long long out_cap) {
+    const size_t smem = ((size_t)NW << lb) * 4 + (size_t)(h->n + 1) * 4;
+    cudaError_t e = cudaFuncSetAttribute(enum_kernel<NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const long long nhigh = 1ll << (h->k - lb);
+    const long long want = (nhigh + 255) / 256;
+    const int grid = (int)std::max(1ll, std::min<long long>(want, (long long)h->num_sms * 8));
+    enum_kernel<NW><<<grid, 256, smem>>>(h->gen.p, h->k, h->n, lb, table, nhigh, cap, spec, out, cnt, out_cap);
+    return cudaGetLastError();
+}
+}  // namespace
+}  // extern "C++"
+
+int64_t mpw_enumerate_lowweight_gpu(mpw_handle* h, int cap, int64_t* spectrum, uint64_t* out, int64_t out_cap) {
+    if (!h || cap < 0 || out_cap < 0 || (out_cap > 0 && !out)) return fail(MPW_ERR_ARG, "bad arguments");
+    if (!h->has_code) return fail(MPW_ERR_STATE, "no code set");
+    if (h->k > 40) return fail(MPW_ERR_UNSUPPORTED, "exhaustive enumeration needs k <= 40 (k=%d)", h->k);
+    const int nw = h->nw;
+    if (nw != 1 && nw != 2 && nw != 4 && nw != 8) return fail(MPW_ERR_UNSUPPORTED, "n=%d", h->n);
+    if (set_device(h)) return MPW_ERR_CUDA;
+    const int lb = std::min(h->k, ENUM_LB);
+    // doubling table of the low lb generator rows (wsphere.py:115-121)
+    std::vector<uint32_t> gen((size_t)h->k * nw);
+    CK(cudaMemcpy(gen.data(), h->gen.p, gen.size() * 4, cudaMemcpyDeviceToHost));
+    std::vector<uint32_t> table((size_t)nw << lb, 0u);
+    for (int e = 1; e < (1 << lb); e++) {
+        const int b = __builtin_ctz(e);
+        for (int w = 0; w < nw; w++) table[(size_t)e * nw + w] = table[(size_t)(e & (e - 1)) * nw + w] ^ gen[(size_t)b * nw + w];
+    }
+    DevBuf<uint32_t> dtab, dout;
+    DevBuf<unsigned long long> dspec, dcnt;
+    const long long dcap = std::max<long long>(out_cap, 1);
+    auto cleanup = [&]() { dtab.release(); dout.release(); dspec.release(); dcnt.release(); };
+    cudaError_t e = cudaSuccess;
+    if ((e = dtab.ensure(table.size())) != cudaSuccess || (e = dout.ensure((size_t)dcap * nw)) != cudaSuccess ||
+        (e = dspec.ensure(h->n + 1)) != cudaSuccess || (e = dcnt.ensure(1)) != cudaSuccess) {
+        cleanup();
+        return fail(MPW_ERR_CUDA, "allocation: %s", cudaGetErrorString(e));
+    }
+    cudaMemcpy(dtab.p, table.data(), table.size() * 4, cudaMemcpyHostToDevice);
+    cudaMemset(dspec.p, 0, (h->n + 1) * sizeof(unsigned long long));
+    cudaMemset(dcnt.p, 0, sizeof(unsigned long long));
+    switch (nw) {
+        case 1: e = launch_enum<1>(h, lb, dtab.p, cap, dspec.p, dout.p, dcnt.p, out_cap); break;
+        case 2: e = launch_enum<2>(h, lb, dtab.p, cap, dspec.p, dout.p, dcnt.p, out_cap); break;
+        case 4: e = launch_enum<4>(h, lb, dtab.p, cap, dspec.p, dout.p, dcnt.p, out_cap); break;
+        default: e = launch_enum<8>(h, lb, dtab.p, cap, dspec.p, dout.p, dcnt.p, out_cap); break;
+    }
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    unsigned long long cnt = 0;
+    std::vector<unsigned long long> spec(h->n + 1);
+    if (e == cudaSuccess) e = cudaMemcpy(&cnt, dcnt.p, sizeof(cnt), cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(spec.data(), dspec.p, spec.size() * 8, cudaMemcpyDeviceToHost);
+    std::vector<uint32_t> words;
+    const long long got = std::min<long long>((long long)cnt, out_cap);
+    if (e == cudaSuccess && got > 0) {
+        words.resize((size_t)got * nw);
+        e = cudaMemcpy(words.data(), dout.p, words.size() * 4, cudaMemcpyDeviceToHost);
+    }
+    cleanup();
+    if (e != cudaSuccess) return fail(MPW_ERR_CUDA, "enumeration: %s", cudaGetErrorString(e));
+    if (spectrum)
+        for (int i = 0; i <= h->n; i++) spectrum[i] = (int64_t)spec[i];
+    const int w64 = (h->n + 63) / 64;
+    for (long long r = 0; r < got; r++)
+        for (int w = 0; w < w64; w++) {
+            const uint64_t lo = words[(size_t)r * nw + 2 * w];
+            const uint64_t hi = 2 * w + 1 < nw ? words[(size_t)r * nw + 2 * w + 1] : 0u;
+            out[(size_t)r * w64 + w] = lo | (hi << 32);
+        }
+    return (int64_t)cnt;
 }
 
 int mpw_set_option(mpw_handle* h, const char* key, int value) {

@@ -230,6 +230,23 @@ class DeviceDecoder:
         self.sphere = sphere
         self.patterns64 = pats
 
+    def enumerate_lowweight(self, cap: int):
+        """Exhaustive GPU walk of all 2^K codewords (mpw_enumerate_lowweight_gpu):
+        (weight spectrum A_0..A_n, uint64 words of every codeword with
+        1 <= weight <= cap, unordered)."""
+        lib = _native.lib()
+        spec = np.zeros(self.n + 1, np.int64)
+        total = lib.mpw_enumerate_lowweight_gpu(self._h, 0, spec.ctypes.data, None, 0)
+        if total < 0:
+            _native.value_error_check(int(total), "mpw_enumerate_lowweight_gpu")
+        want = int(spec[1:cap + 1].sum()) if cap > 0 else 0
+        out = np.zeros((max(want, 1), (self.n + 63) // 64), np.uint64)
+        if want:
+            got = lib.mpw_enumerate_lowweight_gpu(self._h, int(cap), None, out.ctypes.data, want)
+            if got != want:
+                raise RuntimeError(f"GPU enumeration count mismatch ({got} != {want})")
+        return spec, out[:want]
+
     @property
     def tensor_path_ready(self) -> bool:
         return bool(_native.lib().mpw_tensor_path_ready(self._h))

@@ -3,6 +3,8 @@
 
 * `enumerate_sphere(code, r)`: exhaustive 2^K walk, the reference's
   `build_sphere` (wsphere.py:175-208) -- same members, same CWS1 order.
+* `enumerate_sphere_gpu(code, r)`: the same walk on the device
+  (csrc/enum.cuh, K <= 40).
 * `collect_sphere(code, cap, ...)`: seeded information-set search for K > 30
   (BASELINE config 4), where the reference's enumeration budget
   (ENUM_DIM_LIMIT = 30, wsphere.py:28) refuses.
@@ -45,6 +47,32 @@ def enumerate_sphere(code, radius_index: int, threads: int = 0):
         if got != total:
             raise RuntimeError("enumeration count mismatch")
     return sphere_from_members(code.n, code.k, radius_index, out[:total])
+
+
+def enumerate_sphere_gpu(code, radius_index: int, device=None):
+    """`enumerate_sphere` on the GPU (csrc/enum.cuh): same members, same CWS1
+    order (sorted on the host), for K <= 40."""
+    from .decoders import DeviceDecoder
+    dec = DeviceDecoder(code, device=device)
+    try:
+        spec, _ = dec.enumerate_lowweight(0)
+        shells = [w for w in range(1, code.n + 1) if spec[w]]
+        if radius_index < 0 or radius_index > len(shells):
+            raise ValueError(f"radius index {radius_index} exceeds the {len(shells)} available shells")
+        cap = shells[radius_index - 1] if radius_index > 0 else 0
+        _, words = dec.enumerate_lowweight(cap)
+    finally:
+        dec.close()
+    return sphere_from_members(code.n, code.k, radius_index, words)
+
+
+def weight_spectrum_gpu(code, device=None) -> np.ndarray:
+    from .decoders import DeviceDecoder
+    dec = DeviceDecoder(code, device=device)
+    try:
+        return dec.enumerate_lowweight(0)[0]
+    finally:
+        dec.close()
 
 
 def collect_sphere(code, weight_cap: int, iterations: int = 50000, seed: int = 20260208,

@@ -233,6 +233,55 @@ def _scan_cost(n, sphere_size, support_total, m):
     return (m_eff, gain, sort, n + m_eff)
 
 
+def run_sweep_ml(cfg: ExperimentConfig, batch: int = 8192, device=None, variant="auto"):
+    """simharness.run_sweep(decoder_kind='ml'): exact ML on the same trial
+    streams (decoders.py:140-167).  ML = one hop from the zero codeword over
+    P = every nonzero codeword (the reference's criterion 3 identity), so it
+    runs on the same tensor-core scan; ties (measure zero) go to the lowest
+    member index instead of the lowest message index."""
+    from .decoders import DeviceDecoder, words32_to_64
+    from .patterns import enumerate_sphere, weight_spectrum
+    code = build_code(cfg)
+    if code.k > 26:
+        raise ConfigError(f"K = {code.k} exceeds the ML enumeration budget of 26")
+    spec = weight_spectrum(code)
+    sphere = enumerate_sphere(code, int((spec[1:] > 0).sum()))
+    dec = DeviceDecoder(code, sphere, device=device)
+    n, nw = code.n, max(1, code.n // 32)
+    records = []
+    for snr_idx, snr_db in enumerate(cfg.snr_db_grid):
+        sigma = _sigma(cfg, snr_db)
+        trials = errors = 0
+        t0 = 0
+        done = False
+        while not done:
+            cnt = min(batch, cfg.max_trials - t0)
+            _, tx, y = trial_inputs(code, cfg.seed, snr_idx, range(t0, t0 + cnt), sigma)
+            anchors = np.zeros((cnt, 1, nw), np.uint32)
+            o = dec.mp_wsd_batch(y.astype(np.float32), anchors, 1, variant=variant)
+            best = words32_to_64(o["best"].cpu().numpy().view(np.uint32), n)
+            err = (best != tx).any(axis=1)
+            i = 0
+            while i < cnt:
+                if not (trials < cfg.max_trials and errors < cfg.min_block_errors):
+                    done = True
+                    break
+                j = min(i + BATCH, cnt, cfg.max_trials - t0)
+                trials += j - i
+                errors += int(err[i:j].sum())
+                i = j
+            t0 += cnt
+            if t0 >= cfg.max_trials or not (trials < cfg.max_trials and errors < cfg.min_block_errors):
+                done = True
+        lo, hi = wilson_interval(errors, trials)
+        records.append(SweepRecord(
+            code_label=code.label(), stage1_label="ml", wsd_r=0, wsd_m=0, wsd_j=0, num_paths=0,
+            snr_db=snr_db, trials=trials, block_errors=errors, bler=errors / trials, bler_lo=lo,
+            bler_hi=hi, activation_rate=0.0, ed_units_mean=float(1 << code.k), avg_iterations=0.0,
+            seed=cfg.seed))
+    return records
+
+
 def run_sweep(cfg: ExperimentConfig, sphere=None, batch: int = 8192, device=None, variant="auto",
               input_mode: str = "trial", on_batch=None):
     """simharness.run_sweep (decoder_kind='two_stage') over the GPU path.

@@ -155,6 +155,11 @@ def gen_sweeps():
         recs = run_sweep(parse_config(cfg_text), sphere=build_sphere(code, r))
         write_csv(recs, os.path.join(HERE, name))
         print(f"{name}: {time.time() - t0:.1f}s")
+    # exact-ML curves on the same trial streams (decoder_kind='ml', demos/sweep_ml.csv)
+    t0 = time.time()
+    recs = run_sweep(parse_config(DEMO_CFG.format(r=2, paths=4)), decoder_kind="ml")
+    write_csv(recs, os.path.join(HERE, "sweep_ml.csv"))
+    print(f"sweep_ml.csv: {time.time() - t0:.1f}s")
 
 
 if __name__ == "__main__":

@@ -21,3 +21,14 @@ def test_gpu_sweep_csv_matches_reference_bytes(name, tmp_path):
         want = fh.read()
     assert out.read_bytes() == want
     assert all(r.uncertified_frames == 0 for r in recs)
+
+
+def test_gpu_ml_sweep_csv_matches_reference_bytes(tmp_path):
+    """decoder_kind='ml' (reference mltruth) on the same streams: the GPU's
+    full-codebook scan reproduces demos/sweep_ml.csv."""
+    cfg = sweep.load_config(os.path.join(GOLDEN, "sweep_two_stage.cfg"))
+    recs = sweep.run_sweep_ml(cfg, batch=4096)
+    out = tmp_path / "ml.csv"
+    sweep.write_csv(recs, out)
+    with open(os.path.join(GOLDEN, "sweep_ml.csv"), "rb") as fh:
+        assert out.read_bytes() == fh.read()

@@ -76,6 +76,7 @@ extern "C" {
 #define MPW_FLAG_TIE_ACCEPT 2 /* exact ED change of the best hop within 1e-5 relative of 0 */
 #define MPW_FLAG_TIE_FINAL 4  /* two distinct final centres within 1e-5 relative (float64) */
 #define MPW_FLAG_UNRESOLVED 8 /* >= 3 hop candidates inside the certification window */
+#define MPW_FLAG_TIE_STAGE1 16 /* OSD: list order decided by candidates within the rounding bound */
 
 typedef struct mpw_handle mpw_handle;
 
@@ -122,6 +123,28 @@ int mpw_two_stage_batch(mpw_handle* h, const float* y, int F, double sigma, int 
                         uint64_t* best_msg, double* best_ed, uint8_t* stage, int32_t* iters,
                         int32_t* hops, uint32_t* anchors_out, uint8_t* flags,
                         unsigned long long* counters, void* stream);
+
+/* Two-stage decode with order-k OSD as stage 1 (decoders.py:274-317, 555-556;
+ * the paper's RM initialiser).  list_cap <= 0 means no cap.  OSD candidates
+ * are codewords of the code itself: in crc_gated mode the first (minimum-ED)
+ * entry passes the gate; in always_on mode the first A entries are the
+ * anchors, unprojected (decoders.py:573-576).  Outputs as mpw_two_stage_batch;
+ * flags gain MPW_FLAG_TIE_STAGE1 when two OSD candidates that decide the
+ * list order are within the float64 rounding bound. */
+int mpw_two_stage_osd_batch(mpw_handle* h, const float* y, int F, int order, int list_cap, int A,
+                            int T, int mode, int variant, const uint32_t* tx_cw, uint32_t* best,
+                            uint64_t* best_msg, double* best_ed, uint8_t* stage, int32_t* iters,
+                            int32_t* hops, uint32_t* anchors_out, uint8_t* flags,
+                            unsigned long long* counters, void* stream);
+
+/* Order-k OSD list (decoders.py:274-317) for F frames (device buffers):
+ * list_n[F], list_cw[F x M x nw], list_ed[F x M] in ascending squared-ED
+ * order, ties to the lower candidate index, M = min(list_cap, C) (list_cap <= 0:
+ * M = C = sum_{w<=order} C(k, w)).  flags[F] (may be NULL): MPW_FLAG_TIE_STAGE1
+ * when adjacent entries within the first M + 1 are closer than the rounding
+ * bound.  k <= 63, order <= 16, n in {32, 64, 128, 256}. */
+int mpw_osd_batch(mpw_handle* h, const float* y, int F, int order, int list_cap, int32_t* list_n,
+                  uint32_t* list_cw, double* list_ed, uint8_t* flags, void* stream);
 
 /* Same with HOST buffers; H2D/D2H copies are made on `stream` and the call
  * returns after the results are on the host. */

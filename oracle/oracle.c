@@ -40,6 +40,8 @@ typedef struct {
     int num_paths;             /* A */
     int max_iter;              /* T */
     int gated;                 /* activation_mode == crc_gated */
+    int osd_order;             /* >= 0: OsdStage(order, cap) instead of SclStage(L) */
+    int osd_cap;               /* list_cap, <= 0: None */
 } orc_params_t;
 
 static inline int getbit(const uint64_t *w, int j) { return (int)((w[j >> 6] >> (j & 63)) & 1u); }
@@ -373,6 +375,118 @@ static void mp_wsd_one(hop_ws_t *h, const double *y, const uint64_t *anchors, in
 }
 
 /* ------------------------------------------------------------------------ */
+/* osd_decode (decoders.py:274-317).                                         */
+
+typedef struct { double key; int idx; } osd_ent_t;
+
+static int osd_ent_cmp(const void *a, const void *b) {
+    const osd_ent_t *x = (const osd_ent_t *)a, *y = (const osd_ent_t *)b;
+    if (x->key < y->key) return -1;
+    if (x->key > y->key) return 1;
+    return (x->idx > y->idx) - (x->idx < y->idx);     /* stable: ties by position */
+}
+
+static long long osd_count(int k, int order) {
+    long long c = 0, b = 1;
+    for (int w = 0; w <= order && w <= k; w++) { c += b; b = b * (k - w) / (w + 1); }
+    return c;
+}
+
+/* Sorted candidate list: words (C x w64) and squared EDs in ascending order.
+ * Returns C, or -1 if the generator is rank deficient (:289-290). */
+static long long osd_one(const orc_code_t *c, const double *y, int order, uint64_t **words_out,
+                         double **ed_out) {
+    const int n = c->n, k = c->k, w64 = c->w64;
+    /* column_order = argsort(-|y|, stable) (:287) */
+    osd_ent_t *col = malloc(sizeof(osd_ent_t) * (size_t)n);
+    for (int i = 0; i < n; i++) { col[i].key = -fabs(y[i]); col[i].idx = i; }
+    qsort(col, (size_t)n, sizeof(osd_ent_t), osd_ent_cmp);
+    /* row_reduce in that column order (binlin.py:209-247) */
+    uint64_t *work = malloc(sizeof(uint64_t) * (size_t)k * w64), *tmp = malloc(sizeof(uint64_t) * w64);
+    memcpy(work, c->gen, sizeof(uint64_t) * (size_t)k * w64);
+    int *piv = malloc(sizeof(int) * (size_t)k);
+    int rank = 0;
+    for (int t = 0; t < n && rank < k; t++) {
+        const int cc = col[t].idx;
+        int p = -1;
+        for (int r = rank; r < k; r++) if (getbit(work + (size_t)r * w64, cc)) { p = r; break; }
+        if (p < 0) continue;
+        if (p != rank) {
+            memcpy(tmp, work + (size_t)rank * w64, sizeof(uint64_t) * w64);
+            memcpy(work + (size_t)rank * w64, work + (size_t)p * w64, sizeof(uint64_t) * w64);
+            memcpy(work + (size_t)p * w64, tmp, sizeof(uint64_t) * w64);
+        }
+        for (int r = 0; r < k; r++)
+            if (r != rank && getbit(work + (size_t)r * w64, cc))
+                for (int w = 0; w < w64; w++) work[(size_t)r * w64 + w] ^= work[(size_t)rank * w64 + w];
+        piv[rank++] = cc;
+    }
+    free(col);
+    if (rank != k) { free(work); free(tmp); free(piv); return -1; }
+    /* base = XOR of basis rows with y[pivot] < 0 (:294-299) */
+    uint64_t *base = calloc((size_t)w64, sizeof(uint64_t));
+    for (int r = 0; r < k; r++)
+        if (y[piv[r]] < 0)
+            for (int w = 0; w < w64; w++) base[w] ^= work[(size_t)r * w64 + w];
+    /* candidates in itertools.combinations order, weight 0..order (:301-306, :320-323) */
+    const long long C = osd_count(k, order);
+    uint64_t *words = malloc(sizeof(uint64_t) * (size_t)C * w64);
+    long long q = 0;
+    int comb[64];
+    for (int w = 0; w <= order && w <= k; w++) {
+        for (int i = 0; i < w; i++) comb[i] = i;
+        for (;;) {
+            uint64_t *o = words + (size_t)q * w64;
+            memcpy(o, base, sizeof(uint64_t) * w64);
+            for (int i = 0; i < w; i++)
+                for (int x = 0; x < w64; x++) o[x] ^= work[(size_t)comb[i] * w64 + x];
+            q++;
+            int i = w - 1;
+            while (i >= 0 && comb[i] == k - w + i) i--;
+            if (i < 0) break;
+            comb[i]++;
+            for (int j = i + 1; j < w; j++) comb[j] = comb[j - 1] + 1;
+        }
+    }
+    /* squared EDs and stable argsort (:310-313) */
+    osd_ent_t *ent = malloc(sizeof(osd_ent_t) * (size_t)C);
+    for (long long i = 0; i < C; i++) { ent[i].key = sqdist(y, words + (size_t)i * w64, n); ent[i].idx = (int)i; }
+    qsort(ent, (size_t)C, sizeof(osd_ent_t), osd_ent_cmp);
+    uint64_t *sw = malloc(sizeof(uint64_t) * (size_t)C * w64);
+    double *se = malloc(sizeof(double) * (size_t)C);
+    for (long long i = 0; i < C; i++) {
+        memcpy(sw + (size_t)i * w64, words + (size_t)ent[i].idx * w64, sizeof(uint64_t) * w64);
+        se[i] = ent[i].key;
+    }
+    free(ent); free(words); free(base); free(work); free(tmp); free(piv);
+    *words_out = sw; *ed_out = se;
+    return C;
+}
+
+typedef struct {
+    const orc_code_t *code; const float *y32; int order, cap, f0, f1;
+    int32_t *list_n; uint64_t *list_cw; double *list_ed;
+} osd_job_t;
+
+static void *osd_worker(void *arg) {
+    osd_job_t *jb = (osd_job_t *)arg;
+    const int n = jb->code->n, w64 = jb->code->w64;
+    double *y = malloc(sizeof(double) * n);
+    for (int f = jb->f0; f < jb->f1; f++) {
+        for (int i = 0; i < n; i++) y[i] = (double)jb->y32[(size_t)f * n + i];
+        uint64_t *cw; double *ed;
+        long long C = osd_one(jb->code, y, jb->order, &cw, &ed);
+        long long m = C < jb->cap ? C : jb->cap;
+        jb->list_n[f] = (int32_t)m;
+        memcpy(jb->list_cw + (size_t)f * jb->cap * w64, cw, sizeof(uint64_t) * (size_t)m * w64);
+        memcpy(jb->list_ed + (size_t)f * jb->cap, ed, sizeof(double) * (size_t)m);
+        free(cw); free(ed);
+    }
+    free(y);
+    return NULL;
+}
+
+/* ------------------------------------------------------------------------ */
 /* two_stage_decode (decoders.py:520-583) over a batch, threaded by frame.   */
 
 typedef struct {
@@ -399,6 +513,37 @@ static void *two_stage_worker(void *arg) {
         for (int i = 0; i < n; i++) {
             y[i] = (double)jb->y32[(size_t)f * n + i];
             llr[i] = 2.0 * y[i] / (jb->sigma * jb->sigma);             /* :550 */
+        }
+        if (p->osd_order >= 0) {                                        /* :555-556 */
+            uint64_t *ow; double *oe;
+            long long C = osd_one(c, y, p->osd_order, &ow, &oe);
+            long long m = (p->osd_cap > 0 && p->osd_cap < C) ? p->osd_cap : C;
+            int done1 = 0;
+            if (p->gated) {                                             /* :559-570 */
+                uint8_t bits[1024];
+                for (long long r = 0; r < m && !done1; r++) {
+                    for (int i = 0; i < n; i++) bits[i] = (uint8_t)getbit(ow + (size_t)r * w64, i);
+                    polar_transform_u8(bits, n);                       /* precoded_of_codeword */
+                    for (int j = 0; j < c->kp; j++) v[j] = bits[c->info_set[j]];
+                    if (crc_ok(v, c->kp, c->crc_deg, c->crc_poly)) {
+                        memcpy(jb->best + (size_t)f * w64, ow + (size_t)r * w64, sizeof(uint64_t) * w64);
+                        jb->best_ed[f] = sqdist(y, ow + (size_t)r * w64, n);
+                        jb->stage[f] = 0; jb->n_anchor[f] = 0;
+                        done1 = 1;
+                    }
+                }
+            }
+            if (!done1) {
+                int na = m < A ? (int)m : A;                             /* :572-576, in subcode */
+                memcpy(anc, ow, sizeof(uint64_t) * (size_t)na * w64);
+                if (jb->anchors_out)
+                    memcpy(jb->anchors_out + (size_t)f * A * w64, anc, sizeof(uint64_t) * (size_t)na * w64);
+                mp_wsd_one(&hw, y, anc, na, T, jb->best + (size_t)f * w64, &jb->best_ed[f],
+                           jb->iters + (size_t)f * A, jb->hops ? jb->hops + (size_t)f * A * T : NULL, NULL);
+                jb->stage[f] = 1; jb->n_anchor[f] = na;
+            }
+            free(ow); free(oe);
+            continue;
         }
         int cnt = scl_one(&ws, llr, c->info_set, c->kp, u, cw, pm, w64);
         if (jb->list_n) {
@@ -518,3 +663,21 @@ int orc_scl(const double *llrs, int n, const int32_t *info_set, int kp, int L,
 }
 
 int orc_crc_ok(const uint8_t *v, int len, int deg, uint32_t poly) { return crc_ok(v, len, deg, poly); }
+
+/* osd_decode over a batch: list_cw F x cap x w64, list_ed F x cap (cap >= 1). */
+int orc_osd_batch(const orc_code_t *code, const float *y32, int F, int order, int cap, int nthreads,
+                  int32_t *list_n, uint64_t *list_cw, double *list_ed) {
+    if (order < 0 || cap < 1 || code->k > 64) return -1;
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > 256) nthreads = 256;
+    if (nthreads > F) nthreads = F > 0 ? F : 1;
+    osd_job_t jobs[256];
+    for (int t = 0; t < nthreads; t++) {
+        osd_job_t *j = &jobs[t];
+        j->code = code; j->y32 = y32; j->order = order; j->cap = cap;
+        j->f0 = (int)((long long)F * t / nthreads); j->f1 = (int)((long long)F * (t + 1) / nthreads);
+        j->list_n = list_n; j->list_cw = list_cw; j->list_ed = list_ed;
+    }
+    run_threads(osd_worker, jobs, sizeof(osd_job_t), nthreads);
+    return 0;
+}

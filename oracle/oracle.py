@@ -37,6 +37,7 @@ def lib():
         _lib.orc_two_stage_batch.restype = ctypes.c_int
         _lib.orc_mpwsd_batch.restype = ctypes.c_int
         _lib.orc_scl.restype = ctypes.c_int
+        _lib.orc_osd_batch.restype = ctypes.c_int
     return _lib
 
 
@@ -52,7 +53,8 @@ class _Sphere(ctypes.Structure):
 
 class _Params(ctypes.Structure):
     _fields_ = [("list_size", ctypes.c_int), ("num_paths", ctypes.c_int),
-                ("max_iter", ctypes.c_int), ("gated", ctypes.c_int)]
+                ("max_iter", ctypes.c_int), ("gated", ctypes.c_int),
+                ("osd_order", ctypes.c_int), ("osd_cap", ctypes.c_int)]
 
 
 def _ptr(a):
@@ -78,11 +80,14 @@ class OracleCode:
             self.crc_poly = 0
             self.crc_deg = 0
             self.is_ca = 0
-        else:
-            raise ValueError("oracle SCL path needs a polar or CRC-polar code")
+        else:           # e.g. RM: OSD stage 1 only (no info set, no gate)
+            inner = None
+            self.crc_poly = 0
+            self.crc_deg = 0
+            self.is_ca = 0
         self.n = int(code.n)
         self.k = int(code.k)
-        self.info = np.ascontiguousarray(inner.info_set, dtype=np.int32)
+        self.info = np.ascontiguousarray(inner.info_set if inner is not None else [], dtype=np.int32)
         self.gen = np.ascontiguousarray(code.generator.words, dtype=np.uint64)
         self.w64 = self.gen.shape[1]
         self.struct = _Code(self.n, self.k, int(self.info.size), self.w64, self.info.ctypes.data,
@@ -99,13 +104,15 @@ class OracleSphere:
 
 def two_stage_batch(y32, code, sphere, list_size, num_paths, max_iter, gated, sigma,
                     nthreads=1, filter_size=None, want_lists=False, want_hops=False,
-                    want_anchors=False):
-    """Returns a dict of per-frame arrays (stage 0 = stage1_crc_pass, 1 = mp_wsd)."""
+                    want_anchors=False, osd_order=None, osd_cap=None):
+    """Returns a dict of per-frame arrays (stage 0 = stage1_crc_pass, 1 = mp_wsd).
+    osd_order set: stage 1 is OsdStage(osd_order, osd_cap) (decoders.py:555-556)."""
     y32 = np.ascontiguousarray(y32, dtype=np.float32)
     F, n = y32.shape
     oc = OracleCode(code)
     os_ = OracleSphere(sphere, filter_size)
-    prm = _Params(int(list_size), int(num_paths), int(max_iter), int(bool(gated)))
+    prm = _Params(int(list_size), int(num_paths), int(max_iter), int(bool(gated)),
+                  -1 if osd_order is None else int(osd_order), int(osd_cap or 0))
     w64 = oc.w64
     A, T, L = int(num_paths), int(max_iter), int(list_size)
     out = dict(stage=np.zeros(F, np.uint8), best=np.zeros((F, w64), np.uint64),
@@ -152,6 +159,24 @@ def mpwsd_batch(y32, anchors, sphere, max_iter, nthreads=1, filter_size=None):
                           ctypes.c_int(nthreads), _ptr(best), _ptr(best_ed), _ptr(iters),
                           _ptr(hops), _ptr(traj_ed))
     return dict(best=best, best_ed=best_ed, iters=iters, hops=hops, traj_ed=traj_ed)
+
+
+def osd_batch(y32, code, order, list_cap=None, nthreads=1):
+    """osd_decode (decoders.py:274-317) per frame: (list_n, list_cw, list_ed)."""
+    y32 = np.ascontiguousarray(y32, dtype=np.float32)
+    F, n = y32.shape
+    oc = OracleCode(code)
+    C = sum(math.comb(oc.k, w) for w in range(min(order, oc.k) + 1))
+    cap = C if list_cap is None else min(int(list_cap), C)
+    list_n = np.zeros(F, np.int32)
+    list_cw = np.zeros((F, cap, oc.w64), np.uint64)
+    list_ed = np.zeros((F, cap), np.float64)
+    rc = lib().orc_osd_batch(ctypes.byref(oc.struct), _ptr(y32), ctypes.c_int(F), ctypes.c_int(order),
+                             ctypes.c_int(cap), ctypes.c_int(nthreads), _ptr(list_n), _ptr(list_cw),
+                             _ptr(list_ed))
+    if rc != 0:
+        raise ValueError("oracle OSD rejected the arguments")
+    return list_n, list_cw, list_ed
 
 
 def scl(llrs, info_set, n, list_size):

@@ -18,6 +18,7 @@ MODE_CRC_GATED, MODE_ALWAYS_ON = 0, 1
 HOP_AUTO, HOP_GATHER, HOP_TENSOR, HOP_TENSOR_2LIMB = 0, 1, 2, 3
 CTR_FRAMES, CTR_ERRORS, CTR_ACTIVATIONS, CTR_ITERATIONS, CTR_EVALS, CTR_NEAR_TIE, CTR_UNRESOLVED = range(7)
 FLAG_TIE_ARGMIN, FLAG_TIE_ACCEPT, FLAG_TIE_FINAL, FLAG_UNRESOLVED = 1, 2, 4, 8
+FLAG_TIE_STAGE1 = 16
 NUM_COUNTERS = 8
 
 _SIGS = {
@@ -45,6 +46,11 @@ _SIGS = {
                                   c_void_p, c_void_p, c_void_p, c_void_p]),
     "mpw_tensor_path_ready": (c_int, [c_void_p]),
     "mpw_enumerate_lowweight": (c_int64, [c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_int64, c_int]),
+    "mpw_two_stage_osd_batch": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
+                                        c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                        c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "mpw_osd_batch": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p,
+                              c_void_p, c_void_p]),
     "mpw_enumerate_lowweight_gpu": (c_int64, [c_void_p, c_int, c_void_p, c_void_p, c_int64]),
     "mpw_collect_lowweight": (c_int64, [c_void_p, c_int, c_int, c_int, c_int64, c_uint64, c_int,
                                         c_void_p, c_int64, c_int]),

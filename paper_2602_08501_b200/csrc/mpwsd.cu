@@ -23,6 +23,9 @@
 #include "scl_lane.cuh"
 #include "channel.cuh"
 #include "enum.cuh"
+#include "osd.cuh"
+
+#include <cub/device/device_segmented_sort.cuh>
 
 namespace {
 
@@ -91,6 +94,7 @@ struct mpw_handle {
     DevBuf<uint32_t> s2_anchors, traj_cw;
     DevBuf<uint8_t> traj_flags;
     DevBuf<float4> ebound;
+    DevBuf<uint8_t> s1_flags;       // OSD stage-1 near-tie flags
     int wmax = 0;
     int scl_generic = 0;            // force the warp-per-frame SCL kernel
     // timing
@@ -195,6 +199,7 @@ struct FrameArgs {
     int F, A, T, nw, k, np;
     const uint32_t* best; const uint8_t* stage; const uint32_t* tx;
     int32_t* iters; int32_t* hops; uint8_t* flags; uint64_t* msg_out;
+    const uint8_t* s1flags;         // per-frame stage-1 near-tie flags (OSD), may be null
     unsigned long long* counters;
     const int32_t* pivots; const uint64_t* mix;
 };
@@ -220,9 +225,10 @@ __global__ void frame_kernel(FrameArgs fa) {
         } else if (fa.iters) {
             for (int a = 0; a < fa.A; a++) c_it += (unsigned long long)fa.iters[(size_t)f * fa.A + a];
         }
+        if (fa.flags && fa.s1flags) fa.flags[f] |= fa.s1flags[f];
         c_fr = 1;
         c_act = s2 ? 1 : 0;
-        c_tie = (fa.flags && (fa.flags[f] & 7u)) ? 1 : 0;
+        c_tie = (fa.flags && (fa.flags[f] & 23u)) ? 1 : 0;
         c_unr = (fa.flags && (fa.flags[f] & 8u)) ? 1 : 0;
         if (fa.tx) {
             bool diff = false;
@@ -373,6 +379,7 @@ int dispatch_scl_lane(mpw_handle* h, const float* y, const double* llr64, int F,
 
 int dispatch_scl(mpw_handle* h, const float* y, const double* llr64, int F, double sigma, int L, int A,
                  int mode, SclOut out, S2Dev s2, cudaStream_t st) {
+    if (h->n & (h->n - 1)) return fail(MPW_ERR_UNSUPPORTED, "SCL needs a power-of-two length (n=%d)", h->n);
     // lane-per-path kernel for the common shapes (power-of-two L, N in {64,128,256}),
     // warp-per-frame kernel otherwise (or when MPW_SCL_GENERIC is set)
     const bool pow2 = L >= 1 && (L & (L - 1)) == 0 && L <= 32;
@@ -485,7 +492,7 @@ void mpw_destroy(mpw_handle* h) {
     h->crc_h.release(); h->mix.release(); h->pbits.release(); h->poff.release(); h->soff.release();
     h->pidx.release(); h->sup.release(); h->s2_count.release(); h->s2_frame.release();
     h->s2_nanchor.release(); h->traj_iters.release(); h->traj_hops.release(); h->work_next.release();
-    h->s2_anchors.release(); h->traj_cw.release(); h->traj_flags.release(); h->ebound.release();
+    h->s2_anchors.release(); h->traj_cw.release(); h->traj_flags.release(); h->ebound.release(); h->s1_flags.release();
     tc_release(h->tcp);
     if (h->ev_init) for (int i = 0; i < 8; i++) cudaEventDestroy(h->ev[i]);
     delete h;
@@ -494,7 +501,7 @@ void mpw_destroy(mpw_handle* h) {
 int mpw_set_code(mpw_handle* h, int n, int k, int kp, const int32_t* info_set, const uint64_t* gen_words,
                  int is_ca, int crc_deg, uint32_t crc_poly) {
     if (!h || !info_set || !gen_words) return fail(MPW_ERR_ARG, "null argument");
-    if (n < 2 || (n & (n - 1)) || n > 1024) return fail(MPW_ERR_ARG, "n=%d must be a power of two in [2,1024]", n);
+    if (n < 2 || n > 1024) return fail(MPW_ERR_ARG, "n=%d must be in [2,1024]", n);
     if (k < 1 || kp < k || kp > n) return fail(MPW_ERR_ARG, "bad dimensions k=%d kp=%d", k, kp);
     if (k > 64) return fail(MPW_ERR_UNSUPPORTED, "k=%d > 64 is not supported on the device path", k);
     if (is_ca && (crc_deg < 1 || crc_deg > 32 || kp != k + crc_deg || kp > 64))
@@ -503,7 +510,7 @@ int mpw_set_code(mpw_handle* h, int n, int k, int kp, const int32_t* info_set, c
         if (info_set[i] < 0 || info_set[i] >= n || (i && info_set[i] <= info_set[i - 1]))
             return fail(MPW_ERR_ARG, "info set must be ascending in [0,n)");
     if (set_device(h)) return MPW_ERR_CUDA;
-    const int w64 = (n + 63) / 64, nw = std::max(1, n / 32);
+    const int w64 = (n + 63) / 64, nw = (n + 31) / 32;
     h->n = n; h->m = __builtin_ctz(n); h->nw = nw; h->k = k; h->kp = kp; h->is_ca = is_ca; h->crc_deg = crc_deg;
     // frozen mask
     std::vector<uint32_t> frozen(nw, 0);
@@ -649,20 +656,63 @@ int mpw_mpwsd_batch(mpw_handle* h, const float* y, const uint32_t* anchors, cons
     return finalize(h, y, F, A, T, s2, fo, st);
 }
 
-int mpw_two_stage_batch(mpw_handle* h, const float* y, int F, double sigma, int L, int A, int T,
-                        int mode, int variant, const uint32_t* tx_cw, uint32_t* best, uint64_t* best_msg,
-                        double* best_ed, uint8_t* stage, int32_t* iters, int32_t* hops,
-                        uint32_t* anchors_out, uint8_t* flags, unsigned long long* counters, void* stream) {
-    if (!h || F < 0 || A < 1 || T < 1) return fail(MPW_ERR_ARG, "bad arguments");
-    if (F == 0) return 0;
-    if (!y || !best || !best_ed || !stage) return fail(MPW_ERR_ARG, "bad arguments");
-    if (!h->has_code || !h->has_pat) return fail(MPW_ERR_STATE, "code and pattern set must be set first");
-    if (L < 1 || L > SCL_MAX_L) return fail(MPW_ERR_UNSUPPORTED, "list size %d outside [1,%d]", L, SCL_MAX_L);
+extern "C++" {
+namespace {
+
+struct Stage1 {
+    int osd;                 // 0: CA-SCL (list size L), 1: OSD (order, list cap)
+    double sigma;
+    int L, order, cap;
+};
+
+long long osd_candidates(int K, int order) {
+    long long c = 0, b = 1;
+    for (int w = 0; w <= order && w <= K; w++) {
+        c += b;
+        b = b * (K - w) / (w + 1);
+    }
+    return c;
+}
+
+template <int NW>
+int launch_osd_nw(mpw_handle* h, const OsdArgs& a, cudaStream_t st) {
+    const size_t smem = osd_smem_bytes(h->n, NW);
+    CK(cudaFuncSetAttribute(osd_kernel<NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 1;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, osd_kernel<NW>, 32 * OSD_WARPS, smem));
+    const int grid = std::max(1, std::min((a.F + OSD_WARPS - 1) / OSD_WARPS, h->num_sms * std::max(per_sm, 1)));
+    osd_kernel<NW><<<grid, 32 * OSD_WARPS, smem, st>>>(a);
+    CK(cudaGetLastError());
+    return 0;
+}
+
+int launch_osd(mpw_handle* h, const OsdArgs& a, cudaStream_t st) {
+    switch (h->nw) {
+        case 1: return launch_osd_nw<1>(h, a, st);
+        case 2: return launch_osd_nw<2>(h, a, st);
+        case 4: return launch_osd_nw<4>(h, a, st);
+        case 8: return launch_osd_nw<8>(h, a, st);
+    }
+    return fail(MPW_ERR_UNSUPPORTED, "OSD needs n in {32, 64, 128, 256}");
+}
+
+int osd_check(mpw_handle* h, int order) {
+    if (order < 0) return fail(MPW_ERR_ARG, "order must be >= 0");
+    if (h->k > OSD_MAX_K || order > OSD_MAX_ORDER)
+        return fail(MPW_ERR_UNSUPPORTED, "OSD supports k <= %d and order <= %d", OSD_MAX_K, OSD_MAX_ORDER);
+    if (h->nw != 1 && h->nw != 2 && h->nw != 4 && h->nw != 8)
+        return fail(MPW_ERR_UNSUPPORTED, "OSD needs n in {32, 64, 128, 256}");
+    if (osd_candidates(h->k, order) > (1ll << 31) - 1) return fail(MPW_ERR_UNSUPPORTED, "too many OSD candidates");
+    return 0;
+}
+
+int two_stage_impl(mpw_handle* h, const float* y, int F, const Stage1& s1, int A, int T, int mode, int variant,
+                   const uint32_t* tx_cw, uint32_t* best, uint64_t* best_msg, double* best_ed, uint8_t* stage,
+                   int32_t* iters, int32_t* hops, uint32_t* anchors_out, uint8_t* flags,
+                   unsigned long long* counters, cudaStream_t st) {
     if (mode != MPW_MODE_CRC_GATED && mode != MPW_MODE_ALWAYS_ON) return fail(MPW_ERR_ARG, "unknown activation mode %d", mode);
     if (mode == MPW_MODE_CRC_GATED && !h->is_ca) return fail(MPW_ERR_ARG, "crc_gated mode requires a CRC-concatenated code");
-    if (F == 0) return 0;
     if (set_device(h)) return MPW_ERR_CUDA;
-    cudaStream_t st = (cudaStream_t)stream;
     if (int rc = ensure_s2(h, F, A, T)) return rc;
     S2Dev s2 = s2_dev(h, nullptr);
     if (h->timing && !h->ev_init) {
@@ -674,7 +724,21 @@ int mpw_two_stage_batch(mpw_handle* h, const float* y, int F, double sigma, int 
     timing_mark(h, 0, st);
     SclOut out{nullptr, nullptr, nullptr, nullptr, stage, best, best_ed};
     const int smode = (mode == MPW_MODE_CRC_GATED) ? 1 : 2;
-    if (int rc = dispatch_scl(h, y, nullptr, F, sigma, L, A, smode, out, s2, st)) return rc;
+    const uint8_t* s1flags = nullptr;
+    if (!s1.osd) {
+        if (int rc = dispatch_scl(h, y, nullptr, F, s1.sigma, s1.L, A, smode, out, s2, st)) return rc;
+    } else {
+        CK(h->s1_flags.ensure(F));
+        OsdArgs a{};
+        a.code = code_dev(h); a.y = y; a.F = F; a.order = s1.order; a.mode = smode;
+        a.C = osd_candidates(h->k, s1.order);
+        long long M = smode == 1 ? 1 : A;
+        if (s1.cap > 0) M = std::min<long long>(M, s1.cap);
+        a.M = (int)std::min<long long>(M, a.C);
+        a.s1flags = h->s1_flags.p; a.out = out; a.s2 = s2; a.A = A;
+        if (int rc = launch_osd(h, a, st)) return rc;
+        s1flags = h->s1_flags.p;
+    }
     ebound_kernel<<<std::max(1, std::min((F + 7) / 8, h->num_sms * 16)), 256, 0, st>>>(h->n, y, s2);
     CK(cudaGetLastError());
     timing_mark(h, 1, st);
@@ -686,11 +750,118 @@ int mpw_two_stage_batch(mpw_handle* h, const float* y, int F, double sigma, int 
     FrameArgs fa;
     fa.F = F; fa.A = A; fa.T = T; fa.nw = h->nw; fa.k = h->k; fa.np = h->np;
     fa.best = best; fa.stage = stage; fa.tx = tx_cw; fa.iters = iters; fa.hops = hops; fa.flags = flags;
-    fa.msg_out = best_msg; fa.counters = counters; fa.pivots = h->pivots.p; fa.mix = h->mix.p;
+    fa.msg_out = best_msg; fa.s1flags = s1flags; fa.counters = counters; fa.pivots = h->pivots.p; fa.mix = h->mix.p;
     frame_kernel<<<(F + 255) / 256, 256, 0, st>>>(fa);
     CK(cudaGetLastError());
     timing_mark(h, 4, st);
     return timing_close(h);
+}
+
+}  // namespace
+}  // extern "C++"
+
+int mpw_two_stage_batch(mpw_handle* h, const float* y, int F, double sigma, int L, int A, int T,
+                        int mode, int variant, const uint32_t* tx_cw, uint32_t* best, uint64_t* best_msg,
+                        double* best_ed, uint8_t* stage, int32_t* iters, int32_t* hops,
+                        uint32_t* anchors_out, uint8_t* flags, unsigned long long* counters, void* stream) {
+    if (!h || F < 0 || A < 1 || T < 1) return fail(MPW_ERR_ARG, "bad arguments");
+    if (F == 0) return 0;
+    if (!y || !best || !best_ed || !stage) return fail(MPW_ERR_ARG, "bad arguments");
+    if (!h->has_code || !h->has_pat) return fail(MPW_ERR_STATE, "code and pattern set must be set first");
+    if (L < 1 || L > SCL_MAX_L) return fail(MPW_ERR_UNSUPPORTED, "list size %d outside [1,%d]", L, SCL_MAX_L);
+    Stage1 s1{0, sigma, L, 0, 0};
+    return two_stage_impl(h, y, F, s1, A, T, mode, variant, tx_cw, best, best_msg, best_ed, stage, iters, hops,
+                          anchors_out, flags, counters, (cudaStream_t)stream);
+}
+
+int mpw_two_stage_osd_batch(mpw_handle* h, const float* y, int F, int order, int list_cap, int A, int T,
+                            int mode, int variant, const uint32_t* tx_cw, uint32_t* best, uint64_t* best_msg,
+                            double* best_ed, uint8_t* stage, int32_t* iters, int32_t* hops,
+                            uint32_t* anchors_out, uint8_t* flags, unsigned long long* counters, void* stream) {
+    if (!h || F < 0 || A < 1 || T < 1) return fail(MPW_ERR_ARG, "bad arguments");
+    if (F == 0) return 0;
+    if (!y || !best || !best_ed || !stage) return fail(MPW_ERR_ARG, "bad arguments");
+    if (!h->has_code || !h->has_pat) return fail(MPW_ERR_STATE, "code and pattern set must be set first");
+    if (int rc = osd_check(h, order)) return rc;
+    if (A > OSD_MAX_KEEP - 1) return fail(MPW_ERR_UNSUPPORTED, "num_paths %d > %d", A, OSD_MAX_KEEP - 1);
+    Stage1 s1{1, 1.0, 0, order, list_cap};
+    return two_stage_impl(h, y, F, s1, A, T, mode, variant, tx_cw, best, best_msg, best_ed, stage, iters, hops,
+                          anchors_out, flags, counters, (cudaStream_t)stream);
+}
+
+extern "C++" {
+namespace {
+__global__ void osd_iota_kernel(int32_t* v, int32_t* offs, long long C, int F) {
+    const long long total = C * F;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x)
+        v[i] = (int32_t)(i % C);
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t <= F) offs[t] = (int32_t)(C * t);
+}
+
+template <int NW>
+int osd_full_list(mpw_handle* h, OsdArgs a, cudaStream_t st) {
+    const size_t total = (size_t)a.F * (size_t)a.C;
+    DevBuf<double> keys, keys_out;
+    DevBuf<int32_t> vals, vals_out, offs;
+    DevBuf<uint32_t> basis;
+    DevBuf<unsigned char> temp;
+    auto cleanup = [&]() { keys.release(); keys_out.release(); vals.release(); vals_out.release(); offs.release();
+                           basis.release(); temp.release(); };
+    cudaError_t e;
+    if ((e = keys.ensure(total)) || (e = keys_out.ensure(total)) || (e = vals.ensure(total)) ||
+        (e = vals_out.ensure(total)) || (e = offs.ensure(a.F + 1)) ||
+        (e = basis.ensure((size_t)a.F * (h->k + 1) * NW))) {
+        cleanup();
+        return fail(MPW_ERR_CUDA, "allocation: %s", cudaGetErrorString(e));
+    }
+    a.keys = keys.p; a.basis = basis.p;
+    if (int rc = launch_osd_nw<NW>(h, a, st)) { cleanup(); return rc; }
+    osd_iota_kernel<<<std::max(1, std::min<int>((int)((total + 255) / 256), h->num_sms * 8)), 256, 0, st>>>(
+        vals.p, offs.p, a.C, a.F);
+    if (a.F + 1 > h->num_sms * 8 * 256) { cleanup(); return fail(MPW_ERR_UNSUPPORTED, "batch too large"); }
+    size_t tb = 0;
+    e = cub::DeviceSegmentedSort::StableSortPairs(nullptr, tb, keys.p, keys_out.p, vals.p, vals_out.p, (int)total,
+                                                   a.F, offs.p, offs.p + 1, st);
+    if (e == cudaSuccess) e = temp.ensure(tb);
+    if (e == cudaSuccess)
+        e = cub::DeviceSegmentedSort::StableSortPairs(temp.p, tb, keys.p, keys_out.p, vals.p, vals_out.p,
+                                                       (int)total, a.F, offs.p, offs.p + 1, st);
+    if (e == cudaSuccess) {
+        const int grid = std::max(1, std::min((a.F + OSD_WARPS - 1) / OSD_WARPS, h->num_sms * 4));
+        osd_materialize_kernel<NW><<<grid, 32 * OSD_WARPS, 0, st>>>(a, vals_out.p, keys_out.p);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);    // scratch is freed below
+    cleanup();
+    if (e != cudaSuccess) return fail(MPW_ERR_CUDA, "OSD full list: %s", cudaGetErrorString(e));
+    return 0;
+}
+}  // namespace
+}  // extern "C++"
+
+int mpw_osd_batch(mpw_handle* h, const float* y, int F, int order, int list_cap, int32_t* list_n,
+                  uint32_t* list_cw, double* list_ed, uint8_t* flags, void* stream) {
+    if (!h || F < 0) return fail(MPW_ERR_ARG, "bad arguments");
+    if (F == 0) return 0;
+    if (!y || !list_n || !list_cw || !list_ed) return fail(MPW_ERR_ARG, "bad arguments");
+    if (!h->has_code) return fail(MPW_ERR_STATE, "no code set");
+    if (int rc = osd_check(h, order)) return rc;
+    if (set_device(h)) return MPW_ERR_CUDA;
+    cudaStream_t st = (cudaStream_t)stream;
+    OsdArgs a{};
+    a.code = code_dev(h); a.y = y; a.F = F; a.order = order; a.mode = 0;
+    a.C = osd_candidates(h->k, order);
+    a.M = (int)(list_cap > 0 ? std::min<long long>(list_cap, a.C) : a.C);
+    a.list_n = list_n; a.list_cw = list_cw; a.list_ed = list_ed; a.s1flags = flags;
+    if (a.M + 1 <= OSD_MAX_KEEP) return launch_osd(h, a, st);
+    if ((long long)F * a.C > (1ll << 28)) return fail(MPW_ERR_UNSUPPORTED, "full OSD lists limited to F*C <= 2^28");
+    switch (h->nw) {
+        case 1: return osd_full_list<1>(h, a, st);
+        case 2: return osd_full_list<2>(h, a, st);
+        case 4: return osd_full_list<4>(h, a, st);
+        default: return osd_full_list<8>(h, a, st);
+    }
 }
 
 int mpw_two_stage_batch_host(mpw_handle* h, const float* y_host, int F, double sigma, int L, int A, int T,

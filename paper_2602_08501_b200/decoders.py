@@ -173,10 +173,10 @@ def _ptr(t):
 
 
 def words64_to_32(words64: np.ndarray, n: int) -> np.ndarray:
-    """uint64 reference layout [..., ceil(n/64)] -> uint32 device layout [..., max(1, n/32)]."""
+    """uint64 reference layout [..., ceil(n/64)] -> uint32 device layout [..., ceil(n/32)]."""
     w = np.ascontiguousarray(words64, dtype=np.uint64)
     w32 = w.view("<u4").reshape(w.shape[:-1] + (2 * w.shape[-1],))
-    nw = max(1, n // 32)
+    nw = (n + 31) // 32
     return np.ascontiguousarray(w32[..., :nw])
 
 
@@ -210,7 +210,7 @@ class DeviceDecoder:
         self.code = code
         (self.n, self.k, self.kp, self.info, gen, self.is_ca, self.crc_deg, self.crc_poly,
          self.scl_ok) = _code_tables(code)
-        self.nw = max(1, self.n // 32)
+        self.nw = (self.n + 31) // 32
         _native.value_error_check(lib.mpw_set_code(
             h, self.n, self.k, self.kp, self.info.ctypes.data, gen.ctypes.data, self.is_ca,
             self.crc_deg, ctypes.c_uint32(self.crc_poly)), "mpw_set_code")
@@ -296,6 +296,57 @@ class DeviceDecoder:
         _native.value_error_check(rc, "mpw_two_stage_batch")
         return o
 
+    def two_stage_osd_batch(self, y, order: int, list_cap, num_paths: int, max_iterations: int,
+                            activation_mode: str = "always_on", variant: str = "auto", tx_words=None,
+                            want_hops: bool = False, want_anchors: bool = False, counters=None,
+                            stream=None, out=None):
+        """two_stage_batch with OsdStage(order, list_cap) as stage 1
+        (mpw_two_stage_osd_batch; decoders.py:555-556)."""
+        torch = _torch()
+        if activation_mode not in ("crc_gated", "always_on"):
+            raise ValueError(f"unknown activation mode {activation_mode!r}")
+        if activation_mode == "crc_gated" and not self.is_ca:
+            raise ValueError("crc_gated mode requires a CRC-concatenated code")
+        if order < 0:
+            raise ValueError("order must be >= 0")
+        yd = _dev_tensor(y, torch.float32, self.device)
+        F = int(yd.shape[0])
+        A, T = int(num_paths), int(max_iterations)
+        o = out if out is not None else self.alloc_outputs(F, A, T, want_hops, want_anchors)
+        txd = None if tx_words is None else _dev_tensor(tx_words, torch.int32, self.device)
+        ctr = counters if counters is not None else o.get("counters")
+        rc = _native.lib().mpw_two_stage_osd_batch(
+            self._h, _ptr(yd), F, int(order), int(list_cap or 0), A, T,
+            _native.MODE_CRC_GATED if activation_mode == "crc_gated" else _native.MODE_ALWAYS_ON,
+            _HOP[variant], _ptr(txd), _ptr(o["best"]), _ptr(o["best_msg"]), _ptr(o["best_ed"]),
+            _ptr(o["stage"]), _ptr(o["iters"]), _ptr(o.get("hops")), _ptr(o.get("anchors")),
+            _ptr(o["flags"]), _ptr(ctr), self._stream(stream))
+        _native.value_error_check(rc, "mpw_two_stage_osd_batch")
+        return o
+
+    def osd_batch(self, y, order: int, list_cap=None, stream=None):
+        """Order-k OSD lists (mpw_osd_batch): dict(list_n [F], list_cw [F, M, nw]
+        int32 words, list_ed [F, M] float64, flags [F])."""
+        torch = _torch()
+        if order < 0:
+            raise ValueError("order must be >= 0")
+        yd = _dev_tensor(y, torch.float32, self.device)
+        F = int(yd.shape[0])
+        C = osd_candidate_count(order, self.k)
+        M = C if list_cap is None else max(0, min(int(list_cap), C))
+        d = self.device
+        o = dict(list_n=torch.zeros((F,), dtype=torch.int32, device=d),
+                 list_cw=torch.zeros((F, max(M, 1), self.nw), dtype=torch.int32, device=d),
+                 list_ed=torch.zeros((F, max(M, 1)), dtype=torch.float64, device=d),
+                 flags=torch.zeros((F,), dtype=torch.uint8, device=d))
+        if M == 0:
+            return o
+        rc = _native.lib().mpw_osd_batch(self._h, _ptr(yd), F, int(order), int(M), _ptr(o["list_n"]),
+                                         _ptr(o["list_cw"]), _ptr(o["list_ed"]), _ptr(o["flags"]),
+                                         self._stream(stream))
+        _native.value_error_check(rc, "mpw_osd_batch")
+        return o
+
     def alloc_outputs(self, F, A, T, want_hops=False, want_anchors=False):
         torch = _torch()
         d = self.device
@@ -378,7 +429,16 @@ _cache: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
 _code_only: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
 
 
+_code_only = weakref.WeakKeyDictionary()
+
+
 def get_decoder(code, sphere) -> DeviceDecoder:
+    if sphere is None:                  # stage-1 only (OSD lists, ML)
+        dec = _code_only.get(code)
+        if dec is None:
+            dec = DeviceDecoder(code, None)
+            _code_only[code] = dec
+        return dec
     per = _cache.get(sphere)
     if per is None:
         per = weakref.WeakKeyDictionary()
@@ -561,6 +621,95 @@ def scl_decode(llrs, code, list_size, counters=None) -> CandidateList:
     return CandidateList([(BitVector(n, cw[i]), float(pm[i])) for i in range(cnt)])
 
 
+ML_DIM_LIMIT = 26
+_ml_spheres = weakref.WeakKeyDictionary()
+
+
+def ml_decode(y, code, counters=None):
+    """decoders.py:140-167 on the device: the exact argmin of ||y - x(c)||^2
+    over all 2^K codewords, as one hop from the zero codeword over P = every
+    nonzero codeword (GPU-enumerated, csrc/enum.cuh) -- the reference's
+    criterion-3 identity.  Returns (codeword, squared_ed).  Exact ties (measure
+    zero) go to the lowest member index rather than the lowest message index."""
+    if code.k > ML_DIM_LIMIT:
+        raise ValueError(f"K = {code.k} exceeds the ML enumeration budget of {ML_DIM_LIMIT}")
+    y = np.asarray(y, dtype=np.float64)
+    n = int(code.n)
+    if y.shape != (n,):
+        raise ValueError(f"expected {n} channel values, got {y.shape}")
+    sph = _ml_spheres.get(code)
+    if sph is None:
+        from .patterns import enumerate_sphere_gpu, weight_spectrum_gpu
+        spec = weight_spectrum_gpu(code)
+        sph = enumerate_sphere_gpu(code, int((spec[1:] > 0).sum()))
+        _ml_spheres[code] = sph
+    dec = get_decoder(code, sph)
+    o = dec.mp_wsd_batch(y.astype(np.float32)[None, :], np.zeros((1, 1, dec.nw), np.uint32), 1)
+    best64 = words32_to_64(o["best"].cpu().numpy().view(np.uint32), n)[0]
+    if counters is not None:
+        counters.ed_evaluations += 1 << int(code.k)
+    return BitVector(n, best64), _sqdist(y, best64, n)
+
+
+def osd_candidate_count(order: int, k: int) -> int:
+    """sum_{w <= order} C(K, w) (decoders.py:301-308; complexity.c_osd)."""
+    return sum(math.comb(int(k), w) for w in range(min(int(order), int(k)) + 1))
+
+
+def osd_decode(y, code, order_k: int, list_cap=None, counters=None) -> CandidateList:
+    """decoders.py:274-317 on the device (mpw_osd_batch): the `list_cap`
+    best order-k OSD re-encodings by squared ED, ties to the lower candidate."""
+    if order_k < 0:
+        raise ValueError("order must be >= 0")
+    if counters is None:
+        counters = OpCounter()
+    y = np.asarray(y, dtype=np.float64)
+    n = int(code.n)
+    if y.shape != (n,):
+        raise ValueError(f"expected {n} channel values, got {y.shape}")
+    dec = get_decoder(code, None)
+    o = dec.osd_batch(y.astype(np.float32)[None, :], order_k, list_cap)
+    counters.osd_reencodes += osd_candidate_count(order_k, code.k)
+    cnt = int(o["list_n"][0])
+    words = words32_to_64(o["list_cw"][0, :cnt].cpu().numpy().view(np.uint32), n)
+    eds = o["list_ed"][0, :cnt].cpu().numpy()
+    return CandidateList([(BitVector(n, words[i]), float(eds[i])) for i in range(cnt)])
+
+
+def _two_stage_osd(y, code, stage1, params, sphere, counters) -> DecodeResult:
+    """two_stage_decode with OsdStage (decoders.py:555-556, 559-581): the OSD
+    list is in the subcode, so gate winners and anchors are used as-is."""
+    n = int(code.n)
+    dec = get_decoder(code, sphere)
+    A, T = params.num_paths, params.max_iterations
+    o = dec.two_stage_osd_batch(y.astype(np.float32)[None, :], stage1.order, stage1.list_cap, A, T,
+                                params.activation_mode, want_hops=True, want_anchors=True)
+    h = {k: v.cpu().numpy() for k, v in o.items()}
+    counters.osd_reencodes += osd_candidate_count(stage1.order, code.k)
+    best64 = words32_to_64(h["best"][0].view(np.uint32), n)[0]
+    if h["stage"][0] == 0:
+        return DecodeResult(best_codeword=BitVector(n, best64),
+                            best_message=BitVector(int(code.k), dec.message_of_words(best64)),
+                            squared_ed=_sqdist(y, best64, n), stage="stage1_crc_pass",
+                            traces=[], counters=counters, near_tie=bool(h["flags"][0]))
+    iters = h["iters"][0]
+    na = int((iters > 0).sum())
+    anc64 = words32_to_64(h["anchors"][0, :na].view(np.uint32), n)
+    m = params.resolve_filter_size(sphere)
+    counters.ed_evaluations += na
+    traces = _traces_from_hops(y, sphere, anc64, iters[:na], h["hops"][0], n)
+    for t in traces:
+        for _ in range(t.iterations_used):
+            _step_counters(counters, sphere, m, n)
+    finals = [t.squared_eds[-1] for t in traces]
+    best_k = int(np.argmin(finals))
+    bc = traces[best_k].centers[-1]
+    return DecodeResult(best_codeword=bc,
+                        best_message=BitVector(int(code.k), dec.message_of_words(np.asarray(bc.words))),
+                        squared_ed=finals[best_k], stage="mp_wsd", traces=traces,
+                        counters=counters, near_tie=bool(h["flags"][0]))
+
+
 def two_stage_decode(y, code, stage1, params, sphere, sigma=1.0, counters=None) -> DecodeResult:
     """decoders.py:520-583 on the device."""
     if counters is None:
@@ -570,7 +719,7 @@ def two_stage_decode(y, code, stage1, params, sphere, sigma=1.0, counters=None) 
     if gated and code.kind != "crc_concatenated":
         raise ValueError("crc_gated mode requires a CRC-concatenated code")
     if isinstance(stage1, OsdStage) or type(stage1).__name__ == "OsdStage":
-        raise ValueError("OSD stage 1 is outside the accelerated path (SURVEY.md §8f)")
+        return _two_stage_osd(y, code, stage1, params, sphere, counters)
     if not hasattr(stage1, "list_size"):
         raise ValueError(f"unknown stage-1 spec {stage1!r}")
     if not (code.kind == "polar" or (code.kind == "crc_concatenated"
@@ -614,6 +763,10 @@ def two_stage_decode_batch(Y, code, stage1, params, sphere, sigma=1.0, tx_words=
     DeviceDecoder.two_stage_batch (stage, best, best_msg, best_ed, iters,
     flags, counters)."""
     dec = get_decoder(code, sphere)
+    if isinstance(stage1, OsdStage) or type(stage1).__name__ == "OsdStage":
+        return dec.two_stage_osd_batch(Y, stage1.order, stage1.list_cap, params.num_paths,
+                                       params.max_iterations, params.activation_mode,
+                                       variant=variant, tx_words=tx_words)
     return dec.two_stage_batch(Y, sigma, stage1.list_size, params.num_paths,
                                params.max_iterations, params.activation_mode,
                                variant=variant, tx_words=tx_words)

@@ -247,7 +247,7 @@ def run_sweep_ml(cfg: ExperimentConfig, batch: int = 8192, device=None, variant=
     spec = weight_spectrum(code)
     sphere = enumerate_sphere(code, int((spec[1:] > 0).sum()))
     dec = DeviceDecoder(code, sphere, device=device)
-    n, nw = code.n, max(1, code.n // 32)
+    n, nw = code.n, (code.n + 31) // 32
     records = []
     for snr_idx, snr_db in enumerate(cfg.snr_db_grid):
         sigma = _sigma(cfg, snr_db)

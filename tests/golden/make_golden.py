@@ -23,7 +23,8 @@ sys.path.insert(0, "/root/reference/pkg/src")
 
 import feclab.codebook as fcb  # noqa: E402
 from feclab.binlin import BitMatrix, row_reduce  # noqa: E402
-from feclab.decoders import SclStage, WsdParams, scl_decode, two_stage_decode  # noqa: E402
+from feclab.decoders import (OsdStage, SclStage, WsdParams, osd_decode, scl_decode,  # noqa: E402
+                             two_stage_decode)
 from feclab.wsphere import build_sphere, load_sphere  # noqa: E402
 
 from paper_2602_08501_b200 import channel, configs  # noqa: E402
@@ -126,6 +127,72 @@ def gen_scl(name, frames, seed=7):
     print(f"scl_{name}: {frames} frames")
 
 
+def gen_osd():
+    """osd_decode lists and OSD-initialised two-stage decodes (decoders.py:274-317,
+    555-556) on the RM(128,29) polar-form code (cfg2), the demo CA(64,16) code
+    and cfg1 (full order = ML)."""
+    demo = fcb.build_ca_polar_code(64, 16)
+    cases = (("rm_o2_cap64", ref_code("cfg2"), 3.0, 2, 64, 40),
+             ("rm_o3_full", ref_code("cfg2"), 2.0, 3, None, 6),
+             ("ca64_o3_full", demo, 2.0, 3, None, 12),
+             ("cfg1_o10_cap1", ref_code("cfg1"), 1.0, 10, 1, 30))
+    for tag, code, ebno, order, cap, frames in cases:
+        sigma = channel.ebno_to_sigma(ebno, code.k / code.n)
+        _, _, y = channel.trial_inputs(code, 11, 0, range(frames), sigma)
+        y32 = y.astype(np.float32)
+        lists = [osd_decode(y32[f].astype(np.float64), code, order, cap) for f in range(frames)]
+        M = max(len(x.entries) for x in lists)
+        W = (code.n + 63) // 64
+        cw = np.zeros((frames, M, W), np.uint64)
+        ed = np.full((frames, M), np.nan)
+        cnt = np.zeros(frames, np.int32)
+        for f, lst in enumerate(lists):
+            cnt[f] = len(lst.entries)
+            for i, (c, e) in enumerate(lst.entries):
+                cw[f, i] = c.words
+                ed[f, i] = e
+        np.savez_compressed(os.path.join(HERE, f"osd_{tag}.npz"), y32=y32, list_n=cnt, list_cw=cw,
+                            list_ed=ed, order=np.int32(order), list_cap=np.int32(cap or 0),
+                            gen=np.asarray(code.generator.words))
+        print(f"osd_{tag}: {frames} frames, M={M}")
+    # OSD(2) + always-on MP-WSD r=1 on RM(128,29) (configs/rm_128_29_osd2_r1.cfg shape)
+    cfg = configs.CONFIGS["cfg2"]
+    code = ref_code("cfg2")
+    sph = ref_sphere("cfg2", code, configs.build_sphere_for(cfg, cfg.code()))
+    for tag, ebno, frames, mode, stage1, ccode, csph in (
+            ("rm_osd2_aom", 2.0, 60, "always_on", OsdStage(2, 64), code, sph),
+            ("ca64_osd1_gated", 1.0, 40, "crc_gated", OsdStage(1), demo, None)):
+        if csph is None:
+            csph = build_sphere(ccode, 2)
+        sigma = channel.ebno_to_sigma(ebno, ccode.k / ccode.n)
+        msgs, tx, y = channel.trial_inputs(ccode, 13, 0, range(frames), sigma)
+        y32 = y.astype(np.float32)
+        A, T = 4, 4
+        params = WsdParams(radius_index=csph.radius_index, max_iterations=T, num_paths=A,
+                           activation_mode=mode)
+        W = tx.shape[1]
+        out = dict(y32=y32, tx=tx, msgs=msgs, stage=np.zeros(frames, np.uint8),
+                   best=np.zeros((frames, W), np.uint64), best_msg=np.zeros((frames, ccode.k), np.uint8),
+                   squared_ed=np.zeros(frames), iters=np.zeros((frames, A), np.int32),
+                   n_anchor=np.zeros(frames, np.int32), anchors=np.zeros((frames, A, W), np.uint64),
+                   order=np.int32(stage1.order), list_cap=np.int32(stage1.list_cap or 0),
+                   num_paths=np.int32(A), max_iterations=np.int32(T), gated=np.int32(mode == "crc_gated"),
+                   radius_index=np.int32(csph.radius_index),
+                   sphere_members=np.asarray(csph.member_words))
+        for f in range(frames):
+            r = two_stage_decode(y32[f].astype(np.float64), ccode, stage1, params, csph, sigma=sigma)
+            out["stage"][f] = 0 if r.stage == "stage1_crc_pass" else 1
+            out["best"][f] = r.best_codeword.words
+            out["best_msg"][f] = r.best_message.bits()
+            out["squared_ed"][f] = r.squared_ed
+            for k, tr in enumerate(r.traces):
+                out["iters"][f, k] = tr.iterations_used
+                out["anchors"][f, k] = tr.centers[0].words
+            out["n_anchor"][f] = len(r.traces)
+        np.savez_compressed(os.path.join(HERE, f"two_stage_{tag}.npz"), **out)
+        print(f"two_stage_{tag}: {frames} frames, p_act={out['stage'].mean():.3f}")
+
+
 DEMO_CFG = """
 code_family = ca_polar
 code_n = 64
@@ -165,6 +232,9 @@ def gen_sweeps():
 if __name__ == "__main__":
     if "--sweeps" in sys.argv:
         gen_sweeps()
+        sys.exit(0)
+    if "--osd" in sys.argv:
+        gen_osd()
         sys.exit(0)
     for nm, fr in (("cfg1", 64), ("cfg2", 16), ("cfg3", 32), ("cfg4", 8)):
         gen_scl(nm, fr)

@@ -15,7 +15,7 @@ reference's own rules, so the CSV is the reference's byte for byte:
   reference's operation counts (complexity.py:47-57, decoders.py:375-389,
   :478), mean iterations per path, fixed CSV schema (:32-33, 365-376).
 
-Only the SCL stage-1 path is accelerated; `stage1 = osd` raises.
+Both stage-1 kinds run on the device: CA-SCL and order-k OSD (csrc/osd.cuh).
 Inputs are rounded to float32 (the path's dtype) before decoding.
 """
 
@@ -157,7 +157,17 @@ def build_code(cfg: ExperimentConfig):
     """simharness.py:180-205 (RM codes cannot be list-decoded by SCL)."""
     n, k = cfg.code_n, cfg.code_k
     if cfg.code_family == "rm":
-        raise ConfigError("rm family needs OSD stage 1, which is outside the accelerated path")
+        m = n.bit_length() - 1
+        if 1 << m != n:
+            raise ConfigError("rm code_n must be a power of two")
+        total = 0
+        for r in range(m + 1):
+            total += math.comb(m, r)
+            if total == k:
+                return codes.build_rm_code(m, r)
+            if total > k:
+                break
+        raise ConfigError(f"no Reed-Muller order gives K = {k} at N = {n}")
     ranked = _ranking(n, cfg.reliability_source)
     if cfg.code_family == "polar":
         return codes.build_polar_code(n, k, ranked)
@@ -296,8 +306,6 @@ def run_sweep(cfg: ExperimentConfig, sphere=None, batch: int = 8192, device=None
     from .patterns import enumerate_sphere
     from .sphere import load_sphere
 
-    if cfg.stage1 != "scl":
-        raise ConfigError("only the SCL stage 1 is accelerated")
     code = build_code(cfg)
     if sphere is None:
         sphere = load_sphere(cfg.sphere_path) if cfg.sphere_path else enumerate_sphere(code, cfg.wsd_radius_index)
@@ -306,8 +314,21 @@ def run_sweep(cfg: ExperimentConfig, sphere=None, batch: int = 8192, device=None
     support_total = int(np.bitwise_count(np.asarray(sphere.member_words, dtype=np.uint64)[1:]).sum())
     scan = _scan_cost(code.n, size, support_total, m)
     n, L, A, T = code.n, cfg.scl_list_size, cfg.wsd_num_paths, cfg.wsd_max_iterations
-    scl_ops = L * n * (n.bit_length() - 1)
+    osd = cfg.stage1 == "osd"
+    if osd:     # decoders.py:308: osd_reencodes += C; complexity.py: 3N flops each
+        stage1_flops = 3 * n * sum(math.comb(code.k, w) for w in range(min(cfg.osd_order, code.k) + 1))
+        label = f"osd{cfg.osd_order}"
+    else:       # decoders.py:181-268 node ops, 4 flops each
+        stage1_flops = 4 * L * n * (n.bit_length() - 1)
+        label = f"scl{L}"
     dec = DeviceDecoder(code, sphere, device=device)
+
+    def decode(y):
+        if osd:
+            return dec.two_stage_osd_batch(y, cfg.osd_order, cfg.stage1_list_cap, A, T,
+                                           cfg.activation_mode, variant=variant)
+        return dec.two_stage_batch(y, sigma, L, A, T, cfg.activation_mode, variant=variant)
+
     records = []
     for snr_idx, snr_db in enumerate(cfg.snr_db_grid):
         sigma = _sigma(cfg, snr_db)
@@ -321,13 +342,12 @@ def run_sweep(cfg: ExperimentConfig, sphere=None, batch: int = 8192, device=None
             cnt = min(batch, cfg.max_trials - t0)
             if input_mode == "trial":
                 _, tx, y = trial_inputs(code, cfg.seed, snr_idx, range(t0, t0 + cnt), sigma)
-                y32 = y.astype(np.float32)
-                o = dec.two_stage_batch(y32, sigma, L, A, T, cfg.activation_mode, variant=variant)
+                o = decode(y.astype(np.float32))
                 best = words32_to_64(o["best"].cpu().numpy().view(np.uint32), n)
                 err = (best != tx).any(axis=1)
             else:   # device-resident counter-based inputs (mpw_channel_batch)
                 yd, txd, _ = device_channel(dec, cfg.seed, snr_idx, t0, cnt, sigma)
-                o = dec.two_stage_batch(yd, sigma, L, A, T, cfg.activation_mode, variant=variant)
+                o = decode(yd)
                 err = (o["best"] != txd).any(dim=1).cpu().numpy()
                 if on_batch is not None:
                     on_batch(snr_idx, t0, yd, txd, o)
@@ -355,17 +375,16 @@ def run_sweep(cfg: ExperimentConfig, sphere=None, batch: int = 8192, device=None
                 gain += ns * scan[1]
                 sort += ns * scan[2]
                 misc += ns * scan[3]
-                ties += int(((flags[sl] & 7) != 0).sum())
+                ties += int(((flags[sl] & 23) != 0).sum())
                 unres += int(((flags[sl] & 8) != 0).sum())
                 i = j
             t0 += cnt
             if t0 >= cfg.max_trials or not (trials < cfg.max_trials and errors < cfg.min_block_errors):
                 done = True
-        scl_total = scl_ops * trials
-        flops = 3 * n * ed_ev + gain + sort + 4 * scl_total + misc      # complexity.py:47-57
+        flops = 3 * n * ed_ev + gain + sort + stage1_flops * trials + misc   # complexity.py:47-57
         lo, hi = wilson_interval(errors, trials)
         records.append(SweepRecord(
-            code_label=code.label(), stage1_label=f"scl{L}", wsd_r=cfg.wsd_radius_index, wsd_m=m,
+            code_label=code.label(), stage1_label=label, wsd_r=cfg.wsd_radius_index, wsd_m=m,
             wsd_j=T, num_paths=A, snr_db=snr_db, trials=trials, block_errors=errors,
             bler=errors / trials, bler_lo=lo, bler_hi=hi, activation_rate=activated / trials,
             ed_units_mean=(flops / (3.0 * n)) / trials,

@@ -209,12 +209,12 @@ seed = 99
 """
 
 
-def gen_sweeps():
+def gen_sweeps(rm_only=False):
     """The reference's own run_sweep on its desk-scale demo configuration
     (demos/bler_sweep_small.py), written with its own write_csv."""
     from feclab.simharness import parse_config, run_sweep, write_csv
     code = fcb.build_ca_polar_code(64, 16)
-    for r, paths, name in ((2, 4, "sweep_two_stage.csv"), (0, 1, "sweep_stage1.csv")):
+    for r, paths, name in (() if rm_only else ((2, 4, "sweep_two_stage.csv"), (0, 1, "sweep_stage1.csv"))):
         cfg_text = DEMO_CFG.format(r=r, paths=paths)
         with open(os.path.join(HERE, name.replace(".csv", ".cfg")), "w") as fh:
             fh.write(cfg_text.lstrip())
@@ -222,6 +222,25 @@ def gen_sweeps():
         recs = run_sweep(parse_config(cfg_text), sphere=build_sphere(code, r))
         write_csv(recs, os.path.join(HERE, name))
         print(f"{name}: {time.time() - t0:.1f}s")
+    # OSD(2) + always-on r=1 on RM(128,29): configs/rm_128_29_osd2_r1.cfg with a
+    # reduced trial budget; sphere = the reference's own CWS reader on our file
+    from paper_2602_08501_b200 import codes as mycodes
+    from paper_2602_08501_b200.patterns import enumerate_sphere
+    with open("/root/reference/pkg/configs/rm_128_29_osd2_r1.cfg") as fh:
+        rm_text = fh.read()
+    rm_text = (rm_text.replace("snr_db_grid = 1.0, 2.0, 3.0, 4.0", "snr_db_grid = 1.0, 2.5")
+               .replace("max_trials = 10000", "max_trials = 2048")
+               .replace("sphere_path = rm_128_29_r1.cws", "sphere_path = /tmp/golden_rm_r1.cws"))
+    save_sphere(enumerate_sphere(mycodes.build_rm_code(7, 2), 1), "/tmp/golden_rm_r1.cws")
+    with open(os.path.join(HERE, "sweep_rm_osd.cfg"), "w") as fh:
+        fh.write(rm_text.replace("/tmp/golden_rm_r1.cws", "rm_128_29_r1.cws"))
+    t0 = time.time()
+    rm_cfg = parse_config(rm_text)
+    recs = run_sweep(rm_cfg, sphere=load_sphere("/tmp/golden_rm_r1.cws"))
+    write_csv(recs, os.path.join(HERE, "sweep_rm_osd.csv"))
+    print(f"sweep_rm_osd.csv: {time.time() - t0:.1f}s")
+    if rm_only:
+        return
     # exact-ML curves on the same trial streams (decoder_kind='ml', demos/sweep_ml.csv)
     t0 = time.time()
     recs = run_sweep(parse_config(DEMO_CFG.format(r=2, paths=4)), decoder_kind="ml")
@@ -232,6 +251,9 @@ def gen_sweeps():
 if __name__ == "__main__":
     if "--sweeps" in sys.argv:
         gen_sweeps()
+        sys.exit(0)
+    if "--rm-sweep" in sys.argv:
+        gen_sweeps(rm_only=True)
         sys.exit(0)
     if "--osd" in sys.argv:
         gen_osd()

@@ -32,3 +32,18 @@ def test_gpu_ml_sweep_csv_matches_reference_bytes(tmp_path):
     sweep.write_csv(recs, out)
     with open(os.path.join(GOLDEN, "sweep_ml.csv"), "rb") as fh:
         assert out.read_bytes() == fh.read()
+
+
+def test_gpu_rm_osd_sweep_csv_matches_reference_bytes(tmp_path):
+    """configs/rm_128_29_osd2_r1.cfg (OSD(2) + always-on r=1 on RM(128,29)) with a
+    reduced trial budget: the reference's own run_sweep CSV, byte for byte."""
+    from paper_2602_08501_b200 import codes
+    from paper_2602_08501_b200.patterns import enumerate_sphere_gpu
+    cfg = sweep.load_config(os.path.join(GOLDEN, "sweep_rm_osd.cfg"))
+    sph = enumerate_sphere_gpu(codes.build_rm_code(7, 2), 1)
+    recs = sweep.run_sweep(cfg, sphere=sph, batch=4096)
+    assert all(r.uncertified_frames == 0 for r in recs)
+    out = tmp_path / "rm.csv"
+    sweep.write_csv(recs, out)
+    with open(os.path.join(GOLDEN, "sweep_rm_osd.csv"), "rb") as fh:
+        assert out.read_bytes() == fh.read()

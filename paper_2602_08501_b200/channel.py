@@ -36,6 +36,29 @@ def ebno_to_sigma(ebno_db: float, rate: float) -> float:
     return math.sqrt(1.0 / (2.0 * rate * 10.0 ** (ebno_db / 10.0)))
 
 
+def modulate(c) -> np.ndarray:
+    """BPSK: bit 0 -> +1, bit 1 -> -1 (channel.py:44-46)."""
+    return 1.0 - 2.0 * np.asarray(c.bits(), dtype=np.float64)
+
+
+def modulate_bits(bits) -> np.ndarray:
+    """channel.py:49-50."""
+    return 1.0 - 2.0 * np.asarray(bits, dtype=np.float64)
+
+
+def llr(y, sigma: float) -> np.ndarray:
+    """2y/sigma^2 (channel.py:83-87)."""
+    if sigma <= 0:
+        raise ValueError("sigma must be positive")
+    return 2.0 * np.asarray(y, dtype=np.float64) / (sigma * sigma)
+
+
+def squared_distance(y, x) -> float:
+    """||y - x||^2 (channel.py:90-93)."""
+    d = np.asarray(y, dtype=np.float64) - np.asarray(x, dtype=np.float64)
+    return float(d @ d)
+
+
 def _stream(seed: int, sid: int) -> np.random.Generator:
     key = np.array([seed & _MASK64, sid & _MASK64], dtype=np.uint64)
     return np.random.Generator(np.random.Philox(key=key))

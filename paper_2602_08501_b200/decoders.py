@@ -122,6 +122,12 @@ class OpCounter:
     osd_reencodes: int = 0
     misc_flops: int = 0
 
+    def __add__(self, other) -> "OpCounter":
+        out = OpCounter()
+        out.merge(self)
+        out.merge(other)
+        return out
+
     def merge(self, other) -> None:
         for f in ("ed_evaluations", "gain_additions", "sort_comparisons", "scl_node_ops",
                   "osd_reencodes", "misc_flops"):
@@ -526,6 +532,16 @@ def _traces_from_hops(y, sphere, anchors64, iters, hops, n):
                 hist.append(False)
         traces.append(TrajectoryTrace(k, centers, eds, hist, int(iters[k])))
     return traces
+
+
+def gain_metric(y, x_hat, support) -> float:
+    """decoders.py:329-336: sum over the support of -2 y_j x_hat_j (the exact
+    correlation change of flipping `support`; -Delta ED / 2)."""
+    idx = np.asarray(support, dtype=np.int64)
+    if idx.size == 0:
+        return 0.0
+    y = np.asarray(y, dtype=np.float64)
+    return float(-2.0 * np.sum(y[idx] * np.asarray(x_hat, dtype=np.float64)[idx]))
 
 
 def mp_wsd(y, init_list, sphere, params, counters=None) -> DecodeResult:

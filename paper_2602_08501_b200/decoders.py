@@ -171,6 +171,8 @@ def _dev_tensor(a, dtype, device):
     arr = np.ascontiguousarray(a)
     if arr.dtype == np.uint32 and dtype == torch.int32:
         arr = arr.view(np.int32)
+    if not arr.flags.writeable:
+        arr = arr.copy()
     return torch.from_numpy(arr).to(device=device, dtype=dtype).contiguous()
 
 

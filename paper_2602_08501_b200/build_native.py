@@ -1,38 +1,78 @@
 """Builds libmpwsd.so in-tree with nvcc for sm_100a (no JIT cache, so the
-built library travels with the repo snapshot to the GPU box)."""
+built library travels with the repo snapshot to the GPU box).  Each
+translation unit compiles in its own nvcc process (in parallel), then one
+link step produces the shared library."""
 
 from __future__ import annotations
 
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
+OBJ = os.path.join(CSRC, "build")
 LIB = os.path.join(HERE, "libmpwsd.so")
-SOURCES = ["mpwsd.cu", "sphere_tools.cpp"]
-HEADERS = ["common.cuh", "scl.cuh", "scl_lane.cuh", "hop_gather.cuh", "hop_tc.cuh"]
+SOURCES = ["mpwsd.cu", "hop_tc.cu", "scl_lane.cu", "sphere_tools.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
-         "-Xcompiler", "-fPIC", "-Xcompiler", "-O3", "-shared", "-lpthread"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+CFLAGS = [*ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3"]
+
+
+def _deps():
+    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)
+            if f.endswith((".cu", ".cuh", ".h", ".cpp"))]
+    deps.append(os.path.join(HERE, "..", "include", "mpwsd.h"))
+    return deps
 
 
 def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, s) for s in SOURCES + HEADERS]
-    deps.append(os.path.join(HERE, "..", "include", "mpwsd.h"))
-    return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
+    return any(os.path.getmtime(d) > t for d in _deps() if os.path.exists(d))
+
+
+def _obj(src: str) -> str:
+    return os.path.join(OBJ, os.path.splitext(src)[0] + ".o")
+
+
+def _obj_stale(src: str) -> bool:
+    """An object is stale when it or its dependency file is missing, or any
+    file the dependency file lists (nvcc -MD) is newer."""
+    o, d = _obj(src), _obj(src)[:-2] + ".d"
+    if not (os.path.exists(o) and os.path.exists(d)):
+        return True
+    t = os.path.getmtime(o)
+    with open(d) as fh:
+        deps = fh.read().replace("\\\n", " ").split(":", 1)[-1].split()
+    return any(not os.path.exists(f) or os.path.getmtime(f) > t for f in deps)
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
-    cmd = [NVCC, *FLAGS, "-o", LIB + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES]]
-    if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd), file=sys.stderr)
+    os.makedirs(OBJ, exist_ok=True)
+    extra = ["-Xptxas=-v"] if verbose else []
+    todo = [s for s in SOURCES if force or _obj_stale(s)]
+
+    def compile_one(src):
+        cmd = [NVCC, *CFLAGS, *extra, "-MD", "-MF", _obj(src)[:-2] + ".d", "-c", os.path.join(CSRC, src),
+               "-o", _obj(src)]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        r = subprocess.run(cmd, cwd=HERE, capture_output=True, text=True)
+        return src, r
+
+    with ThreadPoolExecutor(max_workers=max(1, len(todo))) as ex:
+        results = list(ex.map(compile_one, todo))
+    for src, r in results:
+        if verbose or r.returncode:
+            sys.stderr.write(r.stdout + r.stderr)
+        if r.returncode:
+            raise subprocess.CalledProcessError(r.returncode, f"nvcc {src}")
+    cmd = [NVCC, *ARCH, "-shared", "-o", LIB + ".tmp", *[_obj(s) for s in SOURCES], "-lpthread"]
     subprocess.run(cmd, check=True, cwd=HERE)
     os.replace(LIB + ".tmp", LIB)
     return LIB

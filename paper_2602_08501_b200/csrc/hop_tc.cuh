@@ -20,6 +20,7 @@
 #pragma once
 #include <cuda_fp16.h>
 
+#include <cstdio>
 #include <cstdlib>
 #include <vector>
 
@@ -163,7 +164,8 @@ struct Params {
     const uint8_t* btiles;       // [ntiles][KB][256 x 64 fp16] swizzled images
     float tie_rel;
     float err;             // bound on |S_fp32 - S_exact| (S units)
-    int experiment;        // profiling knob: 1 skip epilogue math, 2 skip TMEM loads, 4 force T scans
+    int experiment;        // profiling knob: 1 skip epilogue math, 2 skip TMEM loads, 4 force T scans,
+                           // 8 cycle report from CTA 0, 16 skip top-K insertion
 };
 
 // ---------------------------------------------------------------------------
@@ -351,7 +353,7 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
         }
         uint32_t gtile = 0;
         const bool dbg_on = (prm.experiment & 8) && blockIdx.x == 0 && primary && row == 0;
-        long long t_scan = 0, t_round = 0, t_mark = 0, t_scan0 = 0, n_rounds = 0;
+        long long t_scan = 0, t_round = 0, t_mark = 0, t_scan0 = 0, n_rounds = 0, t_early = 0;
         while (any) {
             if (dbg_on) t_scan0 = clock64();
             TopK<TOPK> top;
@@ -363,6 +365,7 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
             float lastv = CUDART_INF_F;   // min(top.last(), top.b[0] + wadd)
             for (int j = 0; j < ntiles; j++, gtile++) {
                 const uint32_t buf = gtile & 1;
+                if (dbg_on && j == 16) t_early += clock64() - t_scan0;
                 mbar_wait(smem_u32(&tfull[buf]), (gtile >> 1) & 1);
                 tc_fence_after();
                 const int pbase = j * NT_COLS;
@@ -387,7 +390,7 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
                     // slow path (rare per lane): mask of values below the current K-th
                     // best, inserted in increasing index order (ties keep the lowest
                     // index); register values are picked by a select tree
-                    if (mn < lastv) {
+                    if (mn < lastv && !(prm.experiment & 16)) {
                         uint32_t hits = 0;
 #pragma unroll
                         for (int e = 0; e < 32; e++)
@@ -486,7 +489,7 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
                 mbar_arrive(smem_u32(go));
             }
         }
-        if (dbg_on) printf("[hop_tc dbg] rounds=%lld scan_cycles=%lld roundend_cycles=%lld\n", n_rounds, t_scan, t_round);
+        if (dbg_on) printf("[hop_tc dbg] rounds=%lld scan_cycles=%lld roundend_cycles=%lld first16_cycles=%lld\n", n_rounds, t_scan, t_round, t_early);
     }
     tc_fence_before();
     __syncthreads();
@@ -497,82 +500,3 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
 }
 
 }  // namespace tc
-
-// ---------------------------------------------------------------------------
-// host side
-
-inline int tc_experiment() {
-    const char* e = getenv("MPW_TC_EXPERIMENT");
-    return e ? atoi(e) : 0;
-}
-
-struct TcPatterns {
-    bool ready = false;
-    uint8_t* tiles = nullptr;
-    int np = 0, ntiles = 0, kb = 0;
-};
-
-inline bool tc_supported(int n, int np) { return (n == 64 || n == 128 || n == 256) && np >= 1; }
-
-inline void tc_release(TcPatterns& t) {
-    if (t.tiles) cudaFree(t.tiles);
-    t.tiles = nullptr;
-    t.ready = false;
-}
-
-// P bits -> fp16 0/1 tile images [ntiles][KB][256 x 64] already in the SW128
-// shared-memory layout, so one 32 KB bulk copy fills one pipeline stage.
-inline int tc_build(TcPatterns& t, const uint32_t* bits, int np, int n, int nw) {
-    tc_release(t);
-    const int kb = n / tc::KBLK;
-    const int ntiles = (np + tc::NT_COLS - 1) / tc::NT_COLS;
-    const size_t bytes = (size_t)ntiles * kb * tc::B_STAGE_BYTES;
-    std::vector<uint16_t> img(bytes / 2, 0);
-    for (int p = 0; p < np; p++) {
-        const int j = p / tc::NT_COLS, r = p % tc::NT_COLS;
-        for (int i = 0; i < n; i++) {
-            if (!((bits[(size_t)p * nw + (i >> 5)] >> (i & 31)) & 1u)) continue;
-            const int k = i / tc::KBLK, col = i % tc::KBLK;
-            const size_t off = ((size_t)j * kb + k) * tc::B_STAGE_BYTES + tc::sw128_off(r, col);
-            img[off / 2] = 0x3C00;   // fp16 1.0
-        }
-    }
-    if (cudaMalloc(&t.tiles, bytes) != cudaSuccess) return -1;
-    if (cudaMemcpy(t.tiles, img.data(), bytes, cudaMemcpyHostToDevice) != cudaSuccess) return -1;
-    t.np = np; t.ntiles = ntiles; t.kb = kb; t.ready = true;
-    return 0;
-}
-
-template <int KB, int NW, int LIMBS>
-inline int tc_launch_t(const TcPatterns& t, int n, int nw, int A, int T, const float* y, S2Dev s2, PatDev P,
-                       int num_sms, cudaStream_t st) {
-    tc::Params prm;
-    prm.n = n; prm.nw = nw; prm.A = A; prm.T = T; prm.np = t.np; prm.ntiles = t.ntiles;
-    prm.y = y; prm.s2 = s2; prm.pbits = P.bits; prm.btiles = t.tiles; prm.tie_rel = 1e-5f;
-    prm.err = 2e-3f;
-    prm.experiment = tc_experiment();
-    const size_t smem = tc::smem_bytes(KB, LIMBS);
-    if (cudaFuncSetAttribute(tc::hop_tc_kernel<KB, NW, LIMBS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-        return -1;
-    tc::hop_tc_kernel<KB, NW, LIMBS><<<num_sms, tc::THREADS, smem, st>>>(prm);
-    return cudaGetLastError() == cudaSuccess ? 0 : -1;
-}
-
-inline int tc_launch(const TcPatterns& t, int n, int nw, int A, int T, const float* y, S2Dev s2, PatDev P,
-                     int num_sms, int limbs, cudaStream_t st) {
-    if (!t.ready) return -1;
-    if (limbs == 1) {
-        switch (n) {
-            case 64: return tc_launch_t<1, 2, 1>(t, n, nw, A, T, y, s2, P, num_sms, st);
-            case 128: return tc_launch_t<2, 4, 1>(t, n, nw, A, T, y, s2, P, num_sms, st);
-            case 256: return tc_launch_t<4, 8, 1>(t, n, nw, A, T, y, s2, P, num_sms, st);
-            default: return -1;
-        }
-    }
-    switch (n) {
-        case 64: return tc_launch_t<1, 2, 2>(t, n, nw, A, T, y, s2, P, num_sms, st);
-        case 128: return tc_launch_t<2, 4, 2>(t, n, nw, A, T, y, s2, P, num_sms, st);
-        case 256: return tc_launch_t<4, 8, 2>(t, n, nw, A, T, y, s2, P, num_sms, st);
-        default: return -1;
-    }
-}

@@ -1,0 +1,21 @@
+// Host API of the tensor-core hop (definitions in hop_tc.cu, a separate
+// translation unit so the kernel templates compile in parallel with the rest).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "common.cuh"
+
+struct TcPatterns {
+    bool ready = false;
+    uint8_t* tiles = nullptr;
+    int np = 0, ntiles = 0, kb = 0;
+};
+
+bool tc_supported(int n, int np);
+void tc_release(TcPatterns& t);
+// P bits -> fp16 0/1 tile images [ntiles][KB][256 x 64] already in the SW128
+// shared-memory layout, so one 32 KB bulk copy fills one pipeline stage.
+int tc_build(TcPatterns& t, const uint32_t* bits, int np, int n, int nw);
+int tc_launch(const TcPatterns& t, int n, int nw, int A, int T, const float* y, S2Dev s2, PatDev P,
+              int num_sms, int limbs, cudaStream_t st);

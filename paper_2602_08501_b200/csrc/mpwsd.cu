@@ -18,9 +18,9 @@
 #include "../../include/mpwsd.h"
 #include "common.cuh"
 #include "hop_gather.cuh"
-#include "hop_tc.cuh"
+#include "hop_tc_api.h"
 #include "scl.cuh"
-#include "scl_lane.cuh"
+#include "scl_lane_api.h"
 #include "channel.cuh"
 #include "enum.cuh"
 #include "osd.cuh"
@@ -345,38 +345,6 @@ int launch_scl(mpw_handle* h, const float* y, const double* llr64, int F, double
     return 0;
 }
 
-template <int N, int L>
-int launch_scl_lane(mpw_handle* h, const float* y, const double* llr64, int F, double sigma, int A,
-                    int mode, SclOut out, S2Dev s2, cudaStream_t st) {
-    using Lay = SclLane<N, L>;
-    const size_t per_warp = Lay::TOTAL * Lay::FPW;
-    int wpb = (int)std::max<size_t>(1, std::min<size_t>(4, (200 * 1024) / per_warp));
-    const size_t smem = per_warp * wpb;
-    if (smem > 227 * 1024) return fail(MPW_ERR_UNSUPPORTED, "SCL lane kernel shared memory %zu B too large", smem);
-    CK(cudaFuncSetAttribute(scl_lane_kernel<N, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, scl_lane_kernel<N, L>, 32 * wpb, smem));
-    per_sm = std::max(per_sm, 1);
-    const long long frames_per_block = (long long)wpb * Lay::FPW;
-    const long long need = ((long long)F + frames_per_block - 1) / frames_per_block;
-    const int grid = (int)std::max<long long>(1, std::min<long long>(need, (long long)per_sm * h->num_sms * 8));
-    scl_lane_kernel<N, L><<<grid, 32 * wpb, smem, st>>>(code_dev(h), y, llr64, F, sigma, A, mode, out, s2);
-    CK(cudaGetLastError());
-    return 0;
-}
-
-template <int N>
-int dispatch_scl_lane(mpw_handle* h, const float* y, const double* llr64, int F, double sigma, int L, int A,
-                      int mode, SclOut out, S2Dev s2, cudaStream_t st) {
-    switch (L) {
-        case 4: return launch_scl_lane<N, 4>(h, y, llr64, F, sigma, A, mode, out, s2, st);
-        case 8: return launch_scl_lane<N, 8>(h, y, llr64, F, sigma, A, mode, out, s2, st);
-        case 16: return launch_scl_lane<N, 16>(h, y, llr64, F, sigma, A, mode, out, s2, st);
-        case 32: return launch_scl_lane<N, 32>(h, y, llr64, F, sigma, A, mode, out, s2, st);
-        default: return 1;
-    }
-}
-
 int dispatch_scl(mpw_handle* h, const float* y, const double* llr64, int F, double sigma, int L, int A,
                  int mode, SclOut out, S2Dev s2, cudaStream_t st) {
     if (h->n & (h->n - 1)) return fail(MPW_ERR_UNSUPPORTED, "SCL needs a power-of-two length (n=%d)", h->n);
@@ -384,11 +352,9 @@ int dispatch_scl(mpw_handle* h, const float* y, const double* llr64, int F, doub
     // warp-per-frame kernel otherwise (or when MPW_SCL_GENERIC is set)
     const bool pow2 = L >= 1 && (L & (L - 1)) == 0 && L <= 32;
     if (pow2 && !h->scl_generic) {
-        int rc = 1;
-        if (h->n == 64) rc = dispatch_scl_lane<64>(h, y, llr64, F, sigma, L, A, mode, out, s2, st);
-        else if (h->n == 128) rc = dispatch_scl_lane<128>(h, y, llr64, F, sigma, L, A, mode, out, s2, st);
-        else if (h->n == 256) rc = dispatch_scl_lane<256>(h, y, llr64, F, sigma, L, A, mode, out, s2, st);
-        if (rc <= 0) return rc;
+        const int rc = scl_lane_launch(h->n, L, code_dev(h), y, llr64, F, sigma, A, mode, out, s2, h->num_sms, st);
+        if (rc == 0) return 0;
+        if (rc < 0) return fail(MPW_ERR_CUDA, "SCL lane kernel launch failed: %s", cudaGetErrorString((cudaError_t)-rc));
     }
     switch (h->nw) {
         case 1: return launch_scl<1>(h, y, llr64, F, sigma, L, A, mode, out, s2, st);

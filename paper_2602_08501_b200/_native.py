@@ -8,7 +8,7 @@ import os
 import re
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmpwsd.so")
+LIB_PATH = os.environ.get("MPW_LIB") or os.path.join(_HERE, "libmpwsd.so")   # MPW_LIB: A/B builds
 HEADER = os.path.join(_HERE, "..", "include", "mpwsd.h")
 
 c_int, c_double, c_void_p, c_uint32, c_int64, c_uint64 = (

@@ -52,27 +52,29 @@ static int tc_launch_t(const TcPatterns& t, int n, int nw, int A, int T, const f
     prm.err = 2e-3f;
     prm.experiment = tc_experiment();
     const size_t smem = tc::smem_bytes(KB, LIMBS);
-    if (cudaFuncSetAttribute(tc::hop_tc_kernel<KB, NW, LIMBS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-        return -1;
+    cudaError_t e = cudaFuncSetAttribute(tc::hop_tc_kernel<KB, NW, LIMBS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return -(int)e;
     tc::hop_tc_kernel<KB, NW, LIMBS><<<num_sms, tc::THREADS, smem, st>>>(prm);
-    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+    e = cudaGetLastError();
+    return e == cudaSuccess ? 0 : -(int)e;
 }
 
 int tc_launch(const TcPatterns& t, int n, int nw, int A, int T, const float* y, S2Dev s2, PatDev P,
                      int num_sms, int limbs, cudaStream_t st) {
-    if (!t.ready) return -1;
+    if (!t.ready) return 1;
     if (limbs == 1) {
         switch (n) {
             case 64: return tc_launch_t<1, 2, 1>(t, n, nw, A, T, y, s2, P, num_sms, st);
             case 128: return tc_launch_t<2, 4, 1>(t, n, nw, A, T, y, s2, P, num_sms, st);
             case 256: return tc_launch_t<4, 8, 1>(t, n, nw, A, T, y, s2, P, num_sms, st);
-            default: return -1;
+            default: return 1;
         }
     }
     switch (n) {
         case 64: return tc_launch_t<1, 2, 2>(t, n, nw, A, T, y, s2, P, num_sms, st);
         case 128: return tc_launch_t<2, 4, 2>(t, n, nw, A, T, y, s2, P, num_sms, st);
         case 256: return tc_launch_t<4, 8, 2>(t, n, nw, A, T, y, s2, P, num_sms, st);
-        default: return -1;
+        default: return 1;
     }
 }

@@ -42,15 +42,30 @@ constexpr int SMEM_LIMIT = 232448;   // 227 KB opt-in maximum per CTA
 #define MPW_TC_TOPK 6
 #endif
 constexpr int TOPK = MPW_TC_TOPK;    // candidates tracked per row for certification
+static_assert(TOPK <= 8, "top-K hand-over uses 16 TMEM columns");
+constexpr int POOL = 64;                     // prefetched stage-2 work items per CTA
+
+// One prefetched trajectory of the stage-2 queue (claimed mid-round by the
+// secondary epilogue warps, consumed by row refills at the round end).
+struct PoolEnt {
+    int tr;            // trajectory id (queue slot * A + anchor), -1 = none
+    int frame;
+    float err;         // per-frame score error bound for this limb count
+    int pad;
+};
+constexpr int POOL_BYTES = POOL * (int)sizeof(PoolEnt);
+
+__host__ __device__ constexpr int fixed_bytes(int kb, int limbs) {
+    return 1024 /*align slack*/ + limbs * kb * A_KBLK_BYTES + POOL_BYTES + 256;
+}
 
 __host__ __device__ constexpr int stages_for(int kb, int limbs) {
-    return (SMEM_LIMIT - 1024 - 256 - limbs * kb * A_KBLK_BYTES) / B_STAGE_BYTES > 6
-               ? 6
-               : (SMEM_LIMIT - 1024 - 256 - limbs * kb * A_KBLK_BYTES) / B_STAGE_BYTES;
+    return (SMEM_LIMIT - fixed_bytes(kb, limbs)) / B_STAGE_BYTES > 6 ? 6
+                                                                       : (SMEM_LIMIT - fixed_bytes(kb, limbs)) / B_STAGE_BYTES;
 }
 
 __host__ __device__ constexpr size_t smem_bytes(int kb, int limbs) {
-    return 1024 /*align slack*/ + (size_t)limbs * kb * A_KBLK_BYTES + (size_t)stages_for(kb, limbs) * B_STAGE_BYTES + 256;
+    return (size_t)fixed_bytes(kb, limbs) + (size_t)stages_for(kb, limbs) * B_STAGE_BYTES;
 }
 
 // ---------------------------------------------------------------------------
@@ -73,6 +88,31 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
             : "memory");
     } while (!ok);
 }
+__device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+// try_wait with a suspend-time hint: the thread sleeps until the phase
+// completes or ~20 us pass, so a poll loop around it does not spin
+__device__ __forceinline__ bool mbar_try_hint(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity), "r"(20000)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
@@ -100,6 +140,7 @@ __device__ __forceinline__ void tc_mma_f16(uint32_t d_tmem, uint64_t adesc, uint
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void epi_bar_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+__device__ __forceinline__ void sec_bar_sync() { asm volatile("bar.sync 3, 128;" ::: "memory"); }
 __device__ __forceinline__ int epi_bar_or(int pred) {
     int r;
     asm volatile(
@@ -123,6 +164,20 @@ __device__ __forceinline__ int epi_bar_or(int pred) {
           "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),        \
           "=r"(v[29]), "=r"(v[30]), "=r"(v[31])                                                             \
         : "r"(taddr))
+
+#define TC_LD16(taddr, v)                                                                                   \
+    asm volatile(                                                                                           \
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];" \
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),   \
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),          \
+          "=r"(v[15])                                                                                       \
+        : "r"(taddr))
+#define TC_ST16(taddr, v)                                                                                   \
+    asm volatile(                                                                                           \
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" \
+        ::"r"(taddr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), \
+          "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])      \
+        : "memory")
 
 __device__ __forceinline__ float fmin3(float a, float b, float c) {
     float r;
@@ -165,8 +220,92 @@ struct Params {
     float tie_rel;
     float err;             // bound on |S_fp32 - S_exact| (S units)
     int experiment;        // profiling knob: 1 skip epilogue math, 2 skip TMEM loads, 4 force T scans,
-                           // 8 cycle report from CTA 0, 16 skip top-K insertion
+                           // 8 cycle report from CTA 0, 16 skip top-K insertion, 32 no work pool,
+                           // 64 producer waits for the round end
 };
+
+// Certified decision (same rule and arithmetic as certify_topk in
+// common.cuh): every candidate within the window of the best approximate
+// score is re-scored in float64, summing ±y_i over its support in ascending
+// i.  Here all window candidates are scored in one pass over y, one 32-value
+// word at a time with the next word's loads in flight, so a row pays about
+// one L2 round trip instead of one per (candidate, word).
+template <int K, int NW>
+__device__ __forceinline__ void certify_window(const TopK<K>& t, const float* __restrict__ yrow,
+                                               const uint32_t (&c)[NW], const uint32_t* __restrict__ pbits,
+                                               float ed, float tie_rel, float err_row, int& best, bool& improve,
+                                               float& best_approx, uint8_t& flags) {
+    const float thr = tie_rel * ed * 0.25f;
+    const float win = thr + 2.0f * err_row;
+    best = t.i[0];
+    best_approx = t.b[0];
+    improve = t.b[0] < 0.0f;
+    const bool pair = (t.b[1] - t.b[0]) < win;
+    const bool zero = fabsf(t.b[0]) < err_row + thr;
+    if (!pair && !zero) return;
+    int ncand = 1;
+#pragma unroll
+    for (int k = 1; k < K - 1; k++)
+        if (ncand == k && (t.b[k] - t.b[0]) < win) ncand = k + 1;
+    double sc[K - 1];
+#pragma unroll
+    for (int k = 0; k < K - 1; k++) sc[k] = 0.0;
+    // y in 16-value half words: the next half's loads are in flight while the
+    // current half is converted to float64 once (sign of x folded in) and
+    // added into every window candidate whose support holds the position
+    const float4* y4 = reinterpret_cast<const float4*>(yrow);
+    float4 yb[2][4];
+#pragma unroll
+    for (int q = 0; q < 4; q++) yb[0][q] = __ldg(y4 + q);
+    uint32_t bits[K - 1];
+#pragma unroll
+    for (int hw = 0; hw < 2 * NW; hw++) {
+        const int w = hw >> 1, sh = (hw & 1) * 16;
+        if (hw + 1 < 2 * NW) {
+#pragma unroll
+            for (int q = 0; q < 4; q++) yb[(hw + 1) & 1][q] = __ldg(y4 + (hw + 1) * 4 + q);
+        }
+        if (sh == 0) {
+#pragma unroll
+            for (int k = 0; k < K - 1; k++) bits[k] = (k < ncand) ? __ldg(pbits + (size_t)t.i[k] * NW + w) : 0u;
+        }
+        const float* yv = reinterpret_cast<const float*>(yb[hw & 1]);
+        const uint32_t cw = c[w] >> sh;
+        double yd[16];
+#pragma unroll
+        for (int bb = 0; bb < 16; bb++) {
+            const double v = (double)yv[bb];
+            yd[bb] = ((cw >> bb) & 1u) ? -v : v;
+        }
+#pragma unroll
+        for (int k = 0; k < K - 1; k++) {
+            if (k >= ncand) break;
+            const uint32_t bk = bits[k] >> sh;
+#pragma unroll
+            for (int bb = 0; bb < 16; bb++)
+                if ((bk >> bb) & 1u) sc[k] += yd[bb];
+        }
+    }
+    double eb = sc[0];
+    double e_second = CUDART_INF;
+#pragma unroll
+    for (int k = 1; k < K - 1; k++) {
+        if (k >= ncand) break;
+        const double e = sc[k];
+        if (e < eb || (e == eb && t.i[k] < best)) {
+            e_second = eb;
+            eb = e;
+            best = t.i[k];
+            best_approx = t.b[k];
+        } else if (e < e_second) {
+            e_second = e;
+        }
+    }
+    if ((t.b[K - 1] - t.b[0]) < win) flags |= MPW_F_UNRESOLVED;
+    if (e_second - eb < (double)thr) flags |= MPW_F_TIE_ARGMIN;
+    improve = eb < 0.0;
+    if (fabs(eb) < (double)thr) flags |= MPW_F_TIE_ACCEPT;
+}
 
 // ---------------------------------------------------------------------------
 template <int KB, int NW, int LIMBS>
@@ -177,7 +316,8 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
     unsigned char* a_hi = sm;
     unsigned char* a_lo = sm + KB * A_KBLK_BYTES;          // used only when LIMBS == 2
     unsigned char* b_ring = sm + LIMBS * KB * A_KBLK_BYTES;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(b_ring + STAGES * B_STAGE_BYTES);
+    PoolEnt* pool = reinterpret_cast<PoolEnt*>(b_ring + STAGES * B_STAGE_BYTES);   // [POOL]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(pool + POOL);
     // barriers: full[STAGES], empty[STAGES], tfull[2], tempty[2], go
     uint64_t* full = bars;
     uint64_t* empty = bars + STAGES;
@@ -186,6 +326,8 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
     uint64_t* go = tempty + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(go + 1);
     volatile int* done_flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
+    int* pool_head = const_cast<int*>(done_flag) + 1;     // next pool index to consume
+    volatile int* pool_tail = pool_head + 1;              // pool indices < tail hold entries
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n = prm.n, nw = prm.nw, A = prm.A, T = prm.T, np_ = prm.np, ntiles = prm.ntiles;
@@ -195,6 +337,8 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
         for (int b = 0; b < 2; b++) { mbar_init(smem_u32(&tfull[b]), 1); mbar_init(smem_u32(&tempty[b]), EPI_WARPS); }
         mbar_init(smem_u32(go), 1);
         *done_flag = 0;
+        *pool_head = 0;
+        *pool_tail = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -207,23 +351,40 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
     const uint32_t tmem_base = *tmem_slot;
 
     if (warp == 0) {
-        // ===== producer =====
+        // ===== producer: streams P tiles round after round without waiting for
+        // the round end (the ring runs ahead into the next round while the
+        // epilogue decides and refills).  While it waits for a free stage it
+        // polls done_flag; once set it stops and waits for the copies it
+        // issued that the MMA will never consume.
         if (lane == 0) {
             int stage = 0;
-            uint32_t phase = 0;
-            for (uint32_t round = 0;; round++) {
-                mbar_wait(smem_u32(go), round & 1);
-                if (*done_flag) break;
-                for (int j = 0; j < ntiles; j++) {
+            uint32_t phase = 0, issued = 0;
+            bool quit = false;
+            for (uint32_t round = 0; !quit; round++) {
+                if (prm.experiment & 64) {   // profiling: no run-ahead across the round end
+                    mbar_wait(smem_u32(go), round & 1);
+                    if (*done_flag) break;
+                }
+                for (int j = 0; j < ntiles && !quit; j++) {
                     for (int kb = 0; kb < KB; kb++) {
-                        mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+                        const uint32_t eb = smem_u32(&empty[stage]);
+                        while (!mbar_try_hint(eb, phase ^ 1)) {
+                            if (*done_flag) { quit = true; break; }
+                        }
+                        if (quit) break;
                         const uint32_t fb = smem_u32(&full[stage]);
                         mbar_expect_tx(fb, B_STAGE_BYTES);
                         bulk_g2s(smem_u32(b_ring + stage * B_STAGE_BYTES),
                                  prm.btiles + ((size_t)j * KB + kb) * B_STAGE_BYTES, B_STAGE_BYTES, fb);
+                        issued++;
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
                     }
                 }
+            }
+            const uint32_t pending = issued < (uint32_t)STAGES ? issued : (uint32_t)STAGES;
+            for (uint32_t k = 0; k < pending; k++) {
+                if (stage == 0) { stage = STAGES - 1; phase ^= 1; } else stage--;
+                mbar_wait(smem_u32(&full[stage]), phase);
             }
         }
     } else if (warp == 1) {
@@ -234,17 +395,25 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
             uint32_t phase = 0;
             uint32_t gtile = 0;
             const uint32_t ahi = smem_u32(a_hi), alo = smem_u32(a_lo), bring = smem_u32(b_ring);
+            const bool dbg = (prm.experiment & 8) && blockIdx.x == 0;
+            long long w_go = 0, w_tempty = 0, w_full = 0, t0 = 0;
             for (uint32_t round = 0;; round++) {
+                if (dbg) t0 = clock64();
                 mbar_wait(smem_u32(go), round & 1);
+                if (dbg) w_go += clock64() - t0;
                 if (*done_flag) break;
                 tc_fence_after();
                 for (int j = 0; j < ntiles; j++, gtile++) {
                     const uint32_t buf = gtile & 1;
+                    if (dbg) t0 = clock64();
                     mbar_wait(smem_u32(&tempty[buf]), ((gtile >> 1) & 1) ^ 1);
+                    if (dbg) w_tempty += clock64() - t0;
                     tc_fence_after();
                     const uint32_t d = tmem_base + buf * NT_COLS;
                     for (int kb = 0; kb < KB; kb++) {
+                        if (dbg) t0 = clock64();
                         mbar_wait(smem_u32(&full[stage]), phase);
+                        if (dbg) w_full += clock64() - t0;
                         tc_fence_after();
                         const uint64_t bd = sw128_desc(bring + stage * B_STAGE_BYTES);
                         const uint64_t ah = sw128_desc(ahi + kb * A_KBLK_BYTES);
@@ -261,99 +430,173 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
                     tc_commit(smem_u32(&tfull[buf]));
                 }
             }
+            if (dbg) printf("[hop_tc mma] wait go %lld tempty %lld full %lld\n", w_go, w_tempty, w_full);
         }
     } else {
         // ===== epilogue: two threads per trajectory row =====
         // warp w in 2..9 reads TMEM lane quarter w % 4; warps 2..5 (primary) scan
         // columns [0,128) of every tile and own the row state, warps 6..9
-        // (secondary) scan columns [128,256) and hand their top-K over at the end
-        // of each round through the (then idle) B ring.
+        // (secondary) scan columns [128,256), hand their top-K over at the end
+        // of each round, and keep the CTA's pool of prefetched work items full.
         const int g = warp & 3;                  // TMEM lane quarter accessible to this warp
         const int row = g * 32 + lane;
         const bool primary = warp < 6;
+        const int sec = threadIdx.x - 64 - 128;  // secondary thread index 0..127
         const int ch0 = primary ? 0 : (NT_COLS / 32) / 2;
-        float* xv = reinterpret_cast<float*>(b_ring);                      // [128][TOPK]
-        int* xi = reinterpret_cast<int*>(b_ring + ROWS * TOPK * sizeof(float));
         const uint32_t t_lane = tmem_base + ((uint32_t)(g * 32) << 16);
         const int count = *prm.s2.count;
-        const long long ntraj = (long long)count * A;
+        const int ntraj = count * A;
         uint32_t c[NW];
-        long long tr = -1;
+        int tr = -1;
         int iters = 0, frame = 0;
         float ed = 0.f, err_row = 0.f;
         uint8_t flags = 0;
         bool active = false;
+        // pool bookkeeping (identical in every secondary thread)
+        int p_head = 0, p_tail = 0, p_fill = 0;
+        // this secondary thread's in-flight pool claim
+        int cl_tr = -1, cl_q = 0;
+        int cl_frame = 0, cl_nanc = 0;
+        float cl_err = 0.f;
+        // the pool needs three tile boundaries per round; with fewer tiles rows
+        // refill straight from the global queue
+        const int j_claim = ntiles >= 3 ? (ntiles / 2 < ntiles - 3 ? ntiles / 2 : ntiles - 3) : -1;
+        const bool use_pool = j_claim >= 0 && !(prm.experiment & 32);
 
-        auto load_row = [&]() {
-            // fetch the next valid trajectory of the stage-2 queue
-            active = false;
+        // next valid trajectory straight from the global queue (-1: exhausted)
+        auto claim_direct = [&]() -> bool {
             for (;;) {
-                const long long cand = (long long)atomicAdd(prm.s2.work_next, 1);
-                if (cand >= ntraj) break;
-                const int q = (int)(cand / A), a = (int)(cand % A);
+                const int cand = atomicAdd(prm.s2.work_next, 1);
+                if (cand >= ntraj) return false;
+                const int q = cand / A, a = cand - q * A;
                 if (a >= prm.s2.nanchor[q]) continue;
                 tr = cand;
                 frame = prm.s2.frame[q];
                 const float4 eb = prm.s2.ebound[q];
                 err_row = (LIMBS == 1) ? eb.x : eb.y;
-                active = true;
-                break;
-            }
-            if (!active) return;
 #pragma unroll
-            for (int w = 0; w < NW; w++) c[w] = (w < nw) ? prm.s2.anchors[(size_t)tr * nw + w] : 0u;
+                for (int w = 0; w < NW; w++) c[w] = prm.s2.anchors[(size_t)tr * NW + w];
+                return true;
+            }
+        };
+        // next prefetched trajectory from the CTA pool (entries published at
+        // the previous round end; tr < 0 marks a claim that found no work)
+        auto claim_pool = [&]() -> bool {
+            const int tail = *pool_tail;
+            for (;;) {
+                const int idx = atomicAdd(pool_head, 1);
+                if (idx >= tail) return false;
+                const PoolEnt& e = pool[idx % POOL];
+                if (e.tr < 0) continue;
+                tr = e.tr;
+                frame = e.frame;
+                err_row = e.err;
+#pragma unroll
+                for (int w = 0; w < NW; w++) c[w] = __ldg(prm.s2.anchors + (size_t)tr * NW + w);
+                return true;
+            }
+        };
+        // A row of the new centre: t = x ⊙ y split into fp16 limbs, canonical
+        // fp32 ED; y is read one 32-value word ahead of its use
+        auto build_row = [&]() {
             iters = 0;
             flags = 0;
             ed = 0.f;
-            const float* yr = prm.y + (size_t)frame * n;
+            const float4* y4 = reinterpret_cast<const float4*>(prm.y + (size_t)frame * n);
+            float4 yb[2][8];
 #pragma unroll
-            for (int w = 0; w < NW; w++)
-#pragma unroll 1
-            for (int qq = 0; qq < 4; qq++) {
-                const int c8 = w * 4 + qq;
-                const float4 y0 = *reinterpret_cast<const float4*>(yr + c8 * 8);
-                const float4 y1 = *reinterpret_cast<const float4*>(yr + c8 * 8 + 4);
-                const float yy[8] = {y0.x, y0.y, y0.z, y0.w, y1.x, y1.y, y1.z, y1.w};
-                const uint32_t cw = c[w];
-                uint32_t hi[4], lo[4];
+            for (int q = 0; q < 8; q++) yb[0][q] = __ldg(y4 + q);
 #pragma unroll
-                for (int e = 0; e < 8; e += 2) {
-                    const int i0 = c8 * 8 + e;
-                    const float x0 = ((cw >> (i0 & 31)) & 1u) ? -1.f : 1.f;
-                    const float x1 = ((cw >> ((i0 + 1) & 31)) & 1u) ? -1.f : 1.f;
-                    const float t0 = x0 * yy[e], t1 = x1 * yy[e + 1];
-                    const __half h0 = __float2half_rn(t0), h1 = __float2half_rn(t1);
-                    const __half l0 = __float2half_rn(t0 - __half2float(h0));
-                    const __half l1 = __float2half_rn(t1 - __half2float(h1));
-                    hi[e / 2] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
-                    lo[e / 2] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
-                    const float d0 = yy[e] - x0, d1 = yy[e + 1] - x1;
-                    ed = fmaf(d0, d0, ed);
-                    ed = fmaf(d1, d1, ed);
+            for (int w = 0; w < NW; w++) {
+                if (w + 1 < NW) {
+#pragma unroll
+                    for (int q = 0; q < 8; q++) yb[(w + 1) & 1][q] = __ldg(y4 + (w + 1) * 8 + q);
                 }
-                const int kb = c8 >> 3, col = (c8 & 7) * 8;
-                const uint32_t off = kb * A_KBLK_BYTES + sw128_off(row, col);
-                *reinterpret_cast<uint4*>(a_hi + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-                if (LIMBS == 2) *reinterpret_cast<uint4*>(a_lo + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+                const float* yw = reinterpret_cast<const float*>(yb[w & 1]);
+                const uint32_t cw = c[w];
+#pragma unroll
+                for (int qq = 0; qq < 4; qq++) {
+                    uint32_t hi[4], lo[4];
+#pragma unroll
+                    for (int e = 0; e < 8; e += 2) {
+                        const int b0 = qq * 8 + e;
+                        const float x0 = ((cw >> b0) & 1u) ? -1.f : 1.f;
+                        const float x1 = ((cw >> (b0 + 1)) & 1u) ? -1.f : 1.f;
+                        const float t0 = x0 * yw[b0], t1 = x1 * yw[b0 + 1];
+                        const __half h0 = __float2half_rn(t0), h1 = __float2half_rn(t1);
+                        hi[e / 2] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
+                        if (LIMBS == 2) {
+                            const __half l0 = __float2half_rn(t0 - __half2float(h0));
+                            const __half l1 = __float2half_rn(t1 - __half2float(h1));
+                            lo[e / 2] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
+                        }
+                        const float d0 = yw[b0] - x0, d1 = yw[b0 + 1] - x1;
+                        ed = fmaf(d0, d0, ed);
+                        ed = fmaf(d1, d1, ed);
+                    }
+                    const int c8 = w * 4 + qq;
+                    const int kb = c8 >> 3, col = (c8 & 7) * 8;
+                    const uint32_t off = kb * A_KBLK_BYTES + sw128_off(row, col);
+                    *reinterpret_cast<uint4*>(a_hi + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+                    if (LIMBS == 2) *reinterpret_cast<uint4*>(a_lo + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+                }
             }
         };
         auto store_row = [&]() {
 #pragma unroll
-            for (int w = 0; w < NW; w++) if (w < nw) prm.s2.traj_cw[(size_t)tr * nw + w] = c[w];
+            for (int w = 0; w < NW; w++) prm.s2.traj_cw[(size_t)tr * NW + w] = c[w];
             prm.s2.traj_iters[tr] = iters;
             prm.s2.traj_flags[tr] = flags;
         };
+        // pool refill by the secondaries, pipelined over three tile boundaries
+        // so no step waits on the latency of the previous one:
+        //   step 0: claim an index from the global queue (atomic)
+        //   step 1: load its queue slot (frame, anchor count, error bound)
+        //   step 2: write the pool entry and prefetch the anchor and the frame's
+        //           y row into L2
+        auto pool_step = [&](int step) {
+            if (sec >= p_fill) return;
+            if (step == 0) {
+                cl_tr = atomicAdd(prm.s2.work_next, 1);
+            } else if (step == 1) {
+                if (cl_tr < ntraj) {
+                    cl_q = cl_tr / A;
+                    cl_nanc = prm.s2.nanchor[cl_q];
+                    cl_frame = prm.s2.frame[cl_q];
+                    const float4 eb = prm.s2.ebound[cl_q];
+                    cl_err = (LIMBS == 1) ? eb.x : eb.y;
+                }
+            } else {
+                PoolEnt& e = pool[(p_tail + sec) % POOL];
+                const bool ok = cl_tr < ntraj && (cl_tr - cl_q * A) < cl_nanc;
+                e.tr = ok ? cl_tr : -1;
+                if (ok) {
+                    e.frame = cl_frame;
+                    e.err = cl_err;
+                    prefetch_l2(prm.s2.anchors + (size_t)cl_tr * NW);
+                    const char* yl = reinterpret_cast<const char*>(prm.y + (size_t)cl_frame * n);
+                    for (int o = 0; o < n * 4; o += 128) prefetch_l2(yl + o);
+                }
+            }
+        };
 
-        if (primary) load_row();
+        if (primary) {
+            active = claim_direct();
+            if (active) build_row();
+        }
         fence_proxy_async();
         int any = epi_bar_or(active);
         if (primary && row == 0) {
             *done_flag = any ? 0 : 1;
             mbar_arrive(smem_u32(go));
         }
+        p_fill = use_pool ? POOL : 0;
         uint32_t gtile = 0;
         const bool dbg_on = (prm.experiment & 8) && blockIdx.x == 0 && primary && row == 0;
+        const bool dbg_seg = (prm.experiment & 8) && blockIdx.x == 0;
         long long t_scan = 0, t_round = 0, t_mark = 0, t_scan0 = 0, n_rounds = 0, t_early = 0;
+        long long seg[6] = {0, 0, 0, 0, 0, 0}, t_seg = 0;
+#define SEG(k) if (dbg_seg) { const long long t_ = clock64(); seg[k] += t_ - t_seg; t_seg = t_; }
         while (any) {
             if (dbg_on) t_scan0 = clock64();
             TopK<TOPK> top;
@@ -429,22 +672,40 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(smem_u32(&tempty[buf]));
+                if (!primary && use_pool && j >= j_claim && j < j_claim + 3) pool_step(j - j_claim);
             }
             if (dbg_on) { t_mark = clock64(); t_scan += t_mark - t_scan0; }
+            if (dbg_seg) t_seg = clock64();
             // ---- end of a full scan of P: merge the two column halves, then
-            // decide, move, refill (the MMA of the round is complete, so the B
-            // ring is idle and serves as the exchange buffer)
+            // decide, move, refill.  The secondary half hands its top-K over
+            // through TMEM: columns [128, 144) of the last tile's accumulator,
+            // which only this secondary warp reads (the next round's MMAs
+            // start after the round end).
+            const uint32_t xaddr = t_lane + ((gtile - 1) & 1) * NT_COLS + NT_COLS / 2;
             if (!primary) {
+                uint32_t xs[16];
 #pragma unroll
-                for (int k = 0; k < TOPK; k++) { xv[row * TOPK + k] = top.b[k]; xi[row * TOPK + k] = top.i[k]; }
+                for (int k = 0; k < 8; k++) {
+                    xs[k] = k < TOPK ? __float_as_uint(top.b[k]) : 0u;
+                    xs[8 + k] = k < TOPK ? (uint32_t)top.i[k] : 0u;
+                }
+                TC_ST16(xaddr, xs);
+                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                tc_fence_before();
             }
+            SEG(0);
             epi_bar_sync();
+            SEG(1);
             if (primary) {
+                tc_fence_after();
+                uint32_t xs[16];
+                TC_LD16(xaddr, xs);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
                 for (int k = 0; k < TOPK; k++) {
-                    const float s = xv[row * TOPK + k];
+                    const float s = __uint_as_float(xs[k]);
                     if (s < lastv) {
-                        top.insert_inline(s, xi[row * TOPK + k]);
+                        top.insert_inline(s, (int)xs[8 + k]);
                         lastv = fminf(top.last(), top.b[0] + wadd);
                     }
                 }
@@ -454,35 +715,68 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
                 int i1;
                 bool improve;
                 float sb;
-                certify_topk<TOPK, NW>(top, prm.y + (size_t)frame * n, c, prm.pbits, nw, n, ed, prm.tie_rel,
-                                    err_row, i1, improve, sb, flags);
+                certify_window<TOPK, NW>(top, prm.y + (size_t)frame * n, c, prm.pbits, ed, prm.tie_rel, err_row, i1,
+                                         improve, sb, flags);
+                SEG(2);
                 if (improve) {
-                    const uint32_t* pb = prm.pbits + (size_t)i1 * nw;
+                    // flip the fp16 sign bits of the moved positions 8 at a time
+                    // (one 16-byte RMW per swizzle chunk, no per-bit loop)
+                    uint32_t pwv[NW];
 #pragma unroll
-                    for (int w = 0; w < NW; w++) {
-                        if (w >= nw) break;
-                        uint32_t bits = pb[w];
-                        c[w] ^= bits;
-                        while (bits) {
-                            const int i = w * 32 + __ffs(bits) - 1;
-                            bits &= bits - 1;
-                            const uint32_t off = (i >> 6) * A_KBLK_BYTES + sw128_off(row, i & 63);
-                            *reinterpret_cast<uint16_t*>(a_hi + off) ^= 0x8000u;
-                            if (LIMBS == 2) *reinterpret_cast<uint16_t*>(a_lo + off) ^= 0x8000u;
+                    for (int w = 0; w < NW; w++) pwv[w] = __ldg(prm.pbits + (size_t)i1 * NW + w);
+                    {
+#pragma unroll
+                        for (int w = 0; w < NW; w++) {
+                            const uint32_t bits = pwv[w];
+                            c[w] ^= bits;
+#pragma unroll
+                            for (int q = 0; q < 4; q++) {
+                                const uint32_t b8 = (bits >> (8 * q)) & 0xFFu;
+                                if (!b8) continue;
+                                const int c8 = w * 4 + q;
+                                const uint32_t off = (c8 >> 3) * A_KBLK_BYTES + sw128_off(row, (c8 & 7) * 8);
+                                uint4 m;
+                                m.x = ((b8 & 1u) << 15) | ((b8 & 2u) << 30);
+                                m.y = ((b8 & 4u) << 13) | ((b8 & 8u) << 28);
+                                m.z = ((b8 & 16u) << 11) | ((b8 & 32u) << 26);
+                                m.w = ((b8 & 64u) << 9) | ((b8 & 128u) << 24);
+                                uint4* ph = reinterpret_cast<uint4*>(a_hi + off);
+                                uint4 v = *ph;
+                                v.x ^= m.x; v.y ^= m.y; v.z ^= m.z; v.w ^= m.w;
+                                *ph = v;
+                                if (LIMBS == 2) {
+                                    uint4* pl = reinterpret_cast<uint4*>(a_lo + off);
+                                    uint4 u = *pl;
+                                    u.x ^= m.x; u.y ^= m.y; u.z ^= m.z; u.w ^= m.w;
+                                    *pl = u;
+                                }
+                            }
                         }
                     }
                     ed += 4.f * sb;
                     if (prm.s2.traj_hops) prm.s2.traj_hops[(size_t)tr * T + iters - 1] = i1 + 1;
                 }
+                SEG(3);
                 if ((!improve && !(prm.experiment & 4)) || iters == T) {
                     if (prm.s2.traj_hops)
                         for (int h = iters - (improve ? 0 : 1); h < T; h++) prm.s2.traj_hops[(size_t)tr * T + h] = -1;
                     store_row();
-                    load_row();
+                    active = claim_pool() || claim_direct();
+                    if (active) build_row();
                 }
             }
+            SEG(4);
             fence_proxy_async();
             any = epi_bar_or(active);
+            SEG(5);
+            if (!primary && use_pool) {
+                // publish this round's pool fill; consumed indices never exceed the old tail
+                const int h = *reinterpret_cast<volatile int*>(pool_head);
+                p_head = h < p_tail ? h : p_tail;
+                p_tail += p_fill;
+                p_fill = POOL - (p_tail - p_head);
+                if (sec == 0) { *pool_head = p_head; *pool_tail = p_tail; }
+            }
             if (dbg_on) { t_round += clock64() - t_mark; n_rounds++; }
             if (primary && row == 0) {
                 *done_flag = any ? 0 : 1;
@@ -490,6 +784,16 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
             }
         }
         if (dbg_on) printf("[hop_tc dbg] rounds=%lld scan_cycles=%lld roundend_cycles=%lld first16_cycles=%lld\n", n_rounds, t_scan, t_round, t_early);
+#undef SEG
+        if (dbg_seg) {
+#pragma unroll
+            for (int k = 0; k < 6; k++)
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) seg[k] = max(seg[k], __shfl_xor_sync(MPW_FULL, seg[k], o));
+            if (lane == 0)
+                printf("[hop_tc seg] warp %d: pre-merge %lld merge-wait %lld certify %lld move %lld refill %lld or-wait %lld\n",
+                       warp, seg[0], seg[1], seg[2], seg[3], seg[4], seg[5]);
+        }
     }
     tc_fence_before();
     __syncthreads();

@@ -17,5 +17,6 @@ void tc_release(TcPatterns& t);
 // P bits -> fp16 0/1 tile images [ntiles][KB][256 x 64] already in the SW128
 // shared-memory layout, so one 32 KB bulk copy fills one pipeline stage.
 int tc_build(TcPatterns& t, const uint32_t* bits, int np, int n, int nw);
+// 0 on launch, -cudaError on failure, 1 for an unsupported shape
 int tc_launch(const TcPatterns& t, int n, int nw, int A, int T, const float* y, S2Dev s2, PatDev P,
               int num_sms, int limbs, cudaStream_t st);

@@ -393,7 +393,8 @@ int run_hops(mpw_handle* h, const float* y, int Fmax, int A, int T, int variant,
         if (!h->tcp.ready) return fail(MPW_ERR_UNSUPPORTED, "tensor-core hop operand not built for this pattern set");
         const int limbs = variant == MPW_HOP_TENSOR ? 1 : 2;
         int rc = tc_launch(h->tcp, h->n, h->nw, A, T, y, s2, pat_dev(h), h->num_sms, limbs, st);
-        if (rc) return fail(MPW_ERR_CUDA, "tensor-core hop launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+        if (rc) return fail(MPW_ERR_CUDA, "tensor-core hop launch failed: %s",
+                            rc < 0 ? cudaGetErrorString((cudaError_t)-rc) : "unsupported shape");
         return 0;
     }
     HopParams hp;

@@ -1,5 +1,7 @@
 // Tensor-core hop: host side (operand images, launch).
+#include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "hop_tc.cuh"
@@ -43,7 +45,7 @@ int tc_build(TcPatterns& t, const uint32_t* bits, int np, int n, int nw) {
     return 0;
 }
 
-template <int KB, int NW, int LIMBS>
+template <int KB, int NW, int LIMBS, int MODE>
 static int tc_launch_t(const TcPatterns& t, int n, int nw, int A, int T, const float* y, S2Dev s2, PatDev P,
                        int num_sms, cudaStream_t st) {
     tc::Params prm;
@@ -51,12 +53,29 @@ static int tc_launch_t(const TcPatterns& t, int n, int nw, int A, int T, const f
     prm.y = y; prm.s2 = s2; prm.pbits = P.bits; prm.btiles = t.tiles; prm.tie_rel = 1e-5f;
     prm.err = 2e-3f;
     prm.experiment = tc_experiment();
+    static long long* trace = nullptr;
+    prm.trace = nullptr;
+    if (prm.experiment & 128) {
+        const size_t tb = sizeof(long long) * tc::TRACE_W * tc::TRACE_TILES;
+        if (!trace && cudaMallocManaged(&trace, tb) != cudaSuccess) trace = nullptr;
+        if (trace) memset(trace, 0, tb);
+        prm.trace = trace;
+    }
     const size_t smem = tc::smem_bytes(KB, LIMBS);
-    cudaError_t e = cudaFuncSetAttribute(tc::hop_tc_kernel<KB, NW, LIMBS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(tc::hop_tc_kernel<KB, NW, LIMBS, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return -(int)e;
-    tc::hop_tc_kernel<KB, NW, LIMBS><<<num_sms, tc::THREADS, smem, st>>>(prm);
+    tc::hop_tc_kernel<KB, NW, LIMBS, MODE><<<num_sms, tc::THREADS, smem, st>>>(prm);
     e = cudaGetLastError();
+    if (e == cudaSuccess && prm.trace) {
+        // profiling only: dump the trace of this launch (CTA 0), overwriting the previous one
+        cudaStreamSynchronize(st);
+        const char* path = getenv("MPW_TC_TRACE");
+        if (FILE* fh = fopen(path ? path : "gpurun_out/hop_trace.bin", "wb")) {
+            fwrite(prm.trace, sizeof(long long), (size_t)tc::TRACE_W * tc::TRACE_TILES, fh);
+            fclose(fh);
+        }
+    }
     return e == cudaSuccess ? 0 : -(int)e;
 }
 
@@ -65,16 +84,22 @@ int tc_launch(const TcPatterns& t, int n, int nw, int A, int T, const float* y, 
     if (!t.ready) return 1;
     if (limbs == 1) {
         switch (n) {
-            case 64: return tc_launch_t<1, 2, 1>(t, n, nw, A, T, y, s2, P, num_sms, st);
-            case 128: return tc_launch_t<2, 4, 1>(t, n, nw, A, T, y, s2, P, num_sms, st);
-            case 256: return tc_launch_t<4, 8, 1>(t, n, nw, A, T, y, s2, P, num_sms, st);
+            case 64: return tc_launch_t<1, 2, 1, 0>(t, n, nw, A, T, y, s2, P, num_sms, st);
+            case 128: return tc_launch_t<2, 4, 1, 0>(t, n, nw, A, T, y, s2, P, num_sms, st);
+            case 256: {
+                // profiling builds of the cfg4 shape: 128 alone = trace only, other knobs = full
+                const int x = tc_experiment();
+                if (x == 128) return tc_launch_t<4, 8, 1, 1>(t, n, nw, A, T, y, s2, P, num_sms, st);
+                if (x) return tc_launch_t<4, 8, 1, 2>(t, n, nw, A, T, y, s2, P, num_sms, st);
+                return tc_launch_t<4, 8, 1, 0>(t, n, nw, A, T, y, s2, P, num_sms, st);
+            }
             default: return 1;
         }
     }
     switch (n) {
-        case 64: return tc_launch_t<1, 2, 2>(t, n, nw, A, T, y, s2, P, num_sms, st);
-        case 128: return tc_launch_t<2, 4, 2>(t, n, nw, A, T, y, s2, P, num_sms, st);
-        case 256: return tc_launch_t<4, 8, 2>(t, n, nw, A, T, y, s2, P, num_sms, st);
+        case 64: return tc_launch_t<1, 2, 2, 0>(t, n, nw, A, T, y, s2, P, num_sms, st);
+        case 128: return tc_launch_t<2, 4, 2, 0>(t, n, nw, A, T, y, s2, P, num_sms, st);
+        case 256: return tc_launch_t<4, 8, 2, 0>(t, n, nw, A, T, y, s2, P, num_sms, st);
         default: return 1;
     }
 }

@@ -43,6 +43,7 @@ constexpr int SMEM_LIMIT = 232448;   // 227 KB opt-in maximum per CTA
 #endif
 constexpr int TOPK = MPW_TC_TOPK;    // candidates tracked per row for certification
 static_assert(TOPK <= 8, "top-K hand-over uses 16 TMEM columns");
+constexpr int TRACE_W = 18, TRACE_TILES = 1 << 16;
 constexpr int POOL = 64;                     // prefetched stage-2 work items per CTA
 
 // One prefetched trajectory of the stage-2 queue (claimed mid-round by the
@@ -185,6 +186,18 @@ __device__ __forceinline__ float fmin3(float a, float b, float c) {
     return r;
 }
 
+// minimum of 32 fp32 values with 3-input FMNMX3: 16 instructions, depth 4
+__device__ __forceinline__ float min32(const uint32_t (&v)[32]) {
+    float m3[11];
+#pragma unroll
+    for (int e = 0; e < 10; e++)
+        m3[e] = fmin3(__uint_as_float(v[3 * e]), __uint_as_float(v[3 * e + 1]), __uint_as_float(v[3 * e + 2]));
+    m3[10] = fminf(__uint_as_float(v[30]), __uint_as_float(v[31]));
+    const float q0 = fmin3(m3[0], m3[1], m3[2]), q1 = fmin3(m3[3], m3[4], m3[5]);
+    const float q2 = fmin3(m3[6], m3[7], m3[8]), q3 = fminf(m3[9], m3[10]);
+    return fminf(fmin3(q0, q1, q2), q3);
+}
+
 // v[e] for a runtime e without local memory: 5-level select tree (31 SEL)
 __device__ __forceinline__ float select32(const uint32_t (&v)[32], int e) {
     uint32_t a[16];
@@ -219,6 +232,7 @@ struct Params {
     const uint8_t* btiles;       // [ntiles][KB][256 x 64 fp16] swizzled images
     float tie_rel;
     float err;             // bound on |S_fp32 - S_exact| (S units)
+    long long* trace;      // experiment & 128: per-tile clock64 trace of CTA 0 (TRACE_W per tile)
     int experiment;        // profiling knob: 1 skip epilogue math, 2 skip TMEM loads, 4 force T scans,
                            // 8 cycle report from CTA 0, 16 skip top-K insertion, 32 no work pool,
                            // 64 producer waits for the round end
@@ -308,9 +322,14 @@ __device__ __forceinline__ void certify_window(const TopK<K>& t, const float* __
 }
 
 // ---------------------------------------------------------------------------
-template <int KB, int NW, int LIMBS>
+// MODE 0: production.  MODE 1: plus the per-tile clock trace of CTA 0
+// (Params::trace).  MODE 2: plus the profiling knobs of Params::experiment.
+template <int KB, int NW, int LIMBS, int MODE>
 __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
     constexpr int STAGES = stages_for(KB, LIMBS);
+    constexpr bool PROF = MODE == 2;
+    const int xp = PROF ? prm.experiment : 0;
+    long long* const trace = MODE >= 1 ? prm.trace : nullptr;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* sm = reinterpret_cast<unsigned char*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     unsigned char* a_hi = sm;
@@ -361,7 +380,7 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
             uint32_t phase = 0, issued = 0;
             bool quit = false;
             for (uint32_t round = 0; !quit; round++) {
-                if (prm.experiment & 64) {   // profiling: no run-ahead across the round end
+                if (xp & 64) {   // profiling: no run-ahead across the round end
                     mbar_wait(smem_u32(go), round & 1);
                     if (*done_flag) break;
                 }
@@ -395,7 +414,7 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
             uint32_t phase = 0;
             uint32_t gtile = 0;
             const uint32_t ahi = smem_u32(a_hi), alo = smem_u32(a_lo), bring = smem_u32(b_ring);
-            const bool dbg = (prm.experiment & 8) && blockIdx.x == 0;
+            const bool dbg = (xp & 8) && blockIdx.x == 0;
             long long w_go = 0, w_tempty = 0, w_full = 0, t0 = 0;
             for (uint32_t round = 0;; round++) {
                 if (dbg) t0 = clock64();
@@ -408,6 +427,8 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
                     if (dbg) t0 = clock64();
                     mbar_wait(smem_u32(&tempty[buf]), ((gtile >> 1) & 1) ^ 1);
                     if (dbg) w_tempty += clock64() - t0;
+                    const bool tr_on = trace && blockIdx.x == 0 && gtile < (uint32_t)TRACE_TILES;
+                    if (tr_on) trace[(size_t)gtile * TRACE_W] = clock64();
                     tc_fence_after();
                     const uint32_t d = tmem_base + buf * NT_COLS;
                     for (int kb = 0; kb < KB; kb++) {
@@ -428,6 +449,7 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
                     }
                     tc_commit(smem_u32(&tfull[buf]));
+                    if (tr_on) trace[(size_t)gtile * TRACE_W + 1] = clock64();
                 }
             }
             if (dbg) printf("[hop_tc mma] wait go %lld tempty %lld full %lld\n", w_go, w_tempty, w_full);
@@ -461,7 +483,7 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
         // the pool needs three tile boundaries per round; with fewer tiles rows
         // refill straight from the global queue
         const int j_claim = ntiles >= 3 ? (ntiles / 2 < ntiles - 3 ? ntiles / 2 : ntiles - 3) : -1;
-        const bool use_pool = j_claim >= 0 && !(prm.experiment & 32);
+        const bool use_pool = j_claim >= 0 && !(xp & 32);
 
         // next valid trajectory straight from the global queue (-1: exhausted)
         auto claim_direct = [&]() -> bool {
@@ -592,8 +614,8 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
         }
         p_fill = use_pool ? POOL : 0;
         uint32_t gtile = 0;
-        const bool dbg_on = (prm.experiment & 8) && blockIdx.x == 0 && primary && row == 0;
-        const bool dbg_seg = (prm.experiment & 8) && blockIdx.x == 0;
+        const bool dbg_on = (xp & 8) && blockIdx.x == 0 && primary && row == 0;
+        const bool dbg_seg = (xp & 8) && blockIdx.x == 0;
         long long t_scan = 0, t_round = 0, t_mark = 0, t_scan0 = 0, n_rounds = 0, t_early = 0;
         long long seg[6] = {0, 0, 0, 0, 0, 0}, t_seg = 0;
 #define SEG(k) if (dbg_seg) { const long long t_ = clock64(); seg[k] += t_ - t_seg; t_seg = t_; }
@@ -611,66 +633,52 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
                 if (dbg_on && j == 16) t_early += clock64() - t_scan0;
                 mbar_wait(smem_u32(&tfull[buf]), (gtile >> 1) & 1);
                 tc_fence_after();
+                const bool tr_on = trace && blockIdx.x == 0 && gtile < (uint32_t)TRACE_TILES && lane == 0;
+                if (tr_on) trace[(size_t)gtile * TRACE_W + warp] = clock64();
                 const int pbase = j * NT_COLS;
-                const bool tail = pbase + NT_COLS > np_;
-                // per-chunk reduction: min tree, then (rarely) exact top-K insertion
-                auto process = [&](uint32_t (&v)[32], int p0) {
-                    if (tail) {
+                // slow path (rare per lane once the running best settles): values
+                // below the threshold are inserted in increasing index order (ties
+                // keep the lowest index); register values are picked by a select
+                // tree.  Columns past |P| (zero pattern columns of the last tile)
+                // are skipped here, so the min trees need no tail masking.
+                auto slow = [&](const uint32_t (&v)[32], int p0) {
+                    uint32_t hits = 0;
 #pragma unroll
-                        for (int e = 0; e < 32; e++)
-                            if (p0 + e >= np_) v[e] = __float_as_uint(CUDART_INF_F);
-                    }
-                    // chunk minimum with 3-input FMNMX3: 16 instructions for 32 values
-                    float m3[11];
-#pragma unroll
-                    for (int e = 0; e < 10; e++)
-                        m3[e] = fmin3(__uint_as_float(v[3 * e]), __uint_as_float(v[3 * e + 1]),
-                                      __uint_as_float(v[3 * e + 2]));
-                    m3[10] = fminf(__uint_as_float(v[30]), __uint_as_float(v[31]));
-                    const float q0 = fmin3(m3[0], m3[1], m3[2]), q1 = fmin3(m3[3], m3[4], m3[5]);
-                    const float q2 = fmin3(m3[6], m3[7], m3[8]), q3 = fminf(m3[9], m3[10]);
-                    const float mn = fminf(fmin3(q0, q1, q2), q3);
-                    // slow path (rare per lane): mask of values below the current K-th
-                    // best, inserted in increasing index order (ties keep the lowest
-                    // index); register values are picked by a select tree
-                    if (mn < lastv && !(prm.experiment & 16)) {
-                        uint32_t hits = 0;
-#pragma unroll
-                        for (int e = 0; e < 32; e++)
-                            hits |= (__uint_as_float(v[e]) < lastv ? 1u : 0u) << e;
-                        while (hits) {
-                            const int e = __ffs(hits) - 1;
-                            hits &= hits - 1;
-                            const float sv = select32(v, e);
-                            if (sv < lastv) {
-                                top.insert_inline(sv, p0 + e);
-                                lastv = fminf(top.last(), top.b[0] + wadd);
-                            }
+                    for (int e = 0; e < 32; e++) hits |= (__uint_as_float(v[e]) < lastv ? 1u : 0u) << e;
+                    while (hits) {
+                        const int e = __ffs(hits) - 1;
+                        hits &= hits - 1;
+                        const float sv = select32(v, e);
+                        if (sv < lastv && p0 + e < np_) {
+                            top.insert_inline(sv, p0 + e);
+                            lastv = fminf(top.last(), top.b[0] + wadd);
                         }
                     }
                 };
-                // TMEM loads double-buffered: chunk k+1 is in flight while chunk k reduces
+                // two 32-column chunks per step: both TMEM loads in flight together,
+                // then two interleaved min trees
                 constexpr int NCH = (NT_COLS / 32) / 2;
                 const uint32_t tbase = t_lane + buf * NT_COLS + ch0 * 32;
                 uint32_t va[32], vb[32];
-                if (prm.experiment & 2) {
+#pragma unroll 1
+                for (int k = 0; k < NCH; k += 2) {
+                    if (PROF && (xp & 2)) {
 #pragma unroll
-                    for (int e = 0; e < 32; e++) { va[e] = __float_as_uint(1.0f); vb[e] = va[e]; }
-                } else {
-                    TC_LD32(tbase, va);
-                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                }
-#pragma unroll
-                for (int k = 0; k < NCH; k++) {
-                    uint32_t (&cur)[32] = (k & 1) ? vb : va;
-                    uint32_t (&nxt)[32] = (k & 1) ? va : vb;
-                    if (k + 1 < NCH && !(prm.experiment & 2)) TC_LD32(tbase + (k + 1) * 32, nxt);
-                    if (!(prm.experiment & 1)) process(cur, pbase + (ch0 + k) * 32);
-                    if (k + 1 < NCH && !(prm.experiment & 2))
+                        for (int e = 0; e < 32; e++) { va[e] = __float_as_uint(1.0f); vb[e] = va[e]; }
+                    } else {
+                        TC_LD32(tbase + k * 32, va);
+                        TC_LD32(tbase + (k + 1) * 32, vb);
                         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    }
+                    if (PROF && (xp & 1)) continue;
+                    const float ma = min32(va), mb = min32(vb);
+                    if (PROF && (xp & 16)) { if (ma == -12345.f || mb == -12345.f) top.b[0] = 0.f; continue; }
+                    if (ma < lastv) slow(va, pbase + (ch0 + k) * 32);
+                    if (mb < lastv) slow(vb, pbase + (ch0 + k + 1) * 32);
                 }
                 tc_fence_before();
                 __syncwarp();
+                if (tr_on) trace[(size_t)gtile * TRACE_W + 8 + warp] = clock64();
                 if (lane == 0) mbar_arrive(smem_u32(&tempty[buf]));
                 if (!primary && use_pool && j >= j_claim && j < j_claim + 3) pool_step(j - j_claim);
             }
@@ -757,7 +765,7 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
                     if (prm.s2.traj_hops) prm.s2.traj_hops[(size_t)tr * T + iters - 1] = i1 + 1;
                 }
                 SEG(3);
-                if ((!improve && !(prm.experiment & 4)) || iters == T) {
+                if ((!improve && !(xp & 4)) || iters == T) {
                     if (prm.s2.traj_hops)
                         for (int h = iters - (improve ? 0 : 1); h < T; h++) prm.s2.traj_hops[(size_t)tr * T + h] = -1;
                     store_row();

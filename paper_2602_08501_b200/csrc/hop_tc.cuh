@@ -57,7 +57,7 @@ struct PoolEnt {
 constexpr int POOL_BYTES = POOL * (int)sizeof(PoolEnt);
 
 __host__ __device__ constexpr int fixed_bytes(int kb, int limbs) {
-    return 1024 /*align slack*/ + limbs * kb * A_KBLK_BYTES + POOL_BYTES + 256;
+    return 1024 /*align slack*/ + limbs * kb * A_KBLK_BYTES + POOL_BYTES + ROWS * 4 /*row windows*/ + 256;
 }
 
 __host__ __device__ constexpr int stages_for(int kb, int limbs) {
@@ -198,6 +198,15 @@ __device__ __forceinline__ float min32(const uint32_t (&v)[32]) {
     return fminf(fmin3(q0, q1, q2), q3);
 }
 
+// c[w] for a runtime w without local memory
+template <int NW>
+__device__ __forceinline__ uint32_t select_word(const uint32_t (&c)[NW], int w) {
+    uint32_t r = c[0];
+#pragma unroll
+    for (int k = 1; k < NW; k++) r = (w == k) ? c[k] : r;
+    return r;
+}
+
 // v[e] for a runtime e without local memory: 5-level select tree (31 SEL)
 __device__ __forceinline__ float select32(const uint32_t (&v)[32], int e) {
     uint32_t a[16];
@@ -244,47 +253,125 @@ struct Params {
 // i.  Here all window candidates are scored in one pass over y, one 32-value
 // word at a time with the next word's loads in flight, so a row pays about
 // one L2 round trip instead of one per (candidate, word).
-template <int K, int NW>
+template <int K, int NW, bool YSMEM>
 __device__ __forceinline__ void certify_window(const TopK<K>& t, const float* __restrict__ yrow,
                                                const uint32_t (&c)[NW], const uint32_t* __restrict__ pbits,
                                                float ed, float tie_rel, float err_row, int& best, bool& improve,
-                                               float& best_approx, uint8_t& flags) {
+                                               float& best_approx, uint8_t& flags, uint32_t (&best_bits)[NW],
+                                               bool& have_bits) {
     const float thr = tie_rel * ed * 0.25f;
     const float win = thr + 2.0f * err_row;
     best = t.i[0];
     best_approx = t.b[0];
     improve = t.b[0] < 0.0f;
+    have_bits = false;
     const bool pair = (t.b[1] - t.b[0]) < win;
     const bool zero = fabsf(t.b[0]) < err_row + thr;
     if (!pair && !zero) return;
+    // candidate indices copied out of the top-K (the loops below must not
+    // address the top-K arrays, or they would be demoted to local memory)
+    int ci[K - 1];
+#pragma unroll
+    for (int k = 0; k < K - 1; k++) ci[k] = t.i[k];
     int ncand = 1;
 #pragma unroll
     for (int k = 1; k < K - 1; k++)
         if (ncand == k && (t.b[k] - t.b[0]) < win) ncand = k + 1;
+    // every candidate's pattern bits into L1 up front (one round trip); the
+    // per-word reads below then hit L1
+#pragma unroll
+    for (int k = 0; k < K - 1; k++)
+        if (k < ncand) asm volatile("prefetch.global.L1 [%0];" ::"l"(pbits + (size_t)ci[k] * NW));
+    const float4* y4 = reinterpret_cast<const float4*>(yrow);
+    // pass 1, fp32: S_k = sum over supp p_k of x_i y_i with the recursive-
+    // summation bound |fl(S_k) - S_k| <= gamma_63 * sum|y| (<= 64 terms).  If
+    // every decision below is separated by more than that bound it equals the
+    // exact one; otherwise pass 2 recomputes the sums in float64.
+    {
+        float s32[K - 1];
+#pragma unroll
+        for (int k = 0; k < K - 1; k++) s32[k] = 0.f;
+        float ay = 0.f;
+        uint32_t bw[K - 1];
+#pragma unroll 1
+        for (int hw = 0; hw < 2 * NW; hw++) {
+            const int w = hw >> 1, sh = (hw & 1) * 16;
+            if (sh == 0) {
+#pragma unroll
+                for (int k = 0; k < K - 1; k++) bw[k] = (k < ncand) ? __ldg(pbits + (size_t)ci[k] * NW + w) : 0u;
+            }
+            float4 yq[4];
+#pragma unroll
+            for (int q = 0; q < 4; q++) yq[q] = YSMEM ? y4[hw * 4 + q] : __ldg(y4 + hw * 4 + q);
+            const float* yv = reinterpret_cast<const float*>(yq);
+            const uint32_t cw = select_word<NW>(c, w) >> sh;
+            float tv[16];
+#pragma unroll
+            for (int bb = 0; bb < 16; bb++) {
+                tv[bb] = __uint_as_float(__float_as_uint(yv[bb]) ^ (((cw >> bb) & 1u) << 31));
+                ay += fabsf(yv[bb]);
+            }
+#pragma unroll
+            for (int k = 0; k < K - 1; k++) {
+                if (k >= ncand) break;
+                const uint32_t bk = bw[k] >> sh;
+#pragma unroll
+                for (int bb = 0; bb < 16; bb++)
+                    if ((bk >> bb) & 1u) s32[k] += tv[bb];
+            }
+        }
+        const double bnd = (double)ay * (64.0 * 5.9604645e-8 * 1.001) * 1.0001;   // >= gamma_63 * sum|y| (+ rounding of ay)
+        // argmin (ties -> lowest pattern index) and the runner-up, in fp32
+        // (indices and approximations tracked in registers: no runtime indexing
+        // of the top-K arrays, which would move them to local memory)
+        int kb = 0, bi = ci[0];
+        float ba = t.b[0];
+        float eb32 = s32[0], es32 = CUDART_INF_F;
+        bool clear = true;
+#pragma unroll
+        for (int k = 1; k < K - 1; k++) {
+            if (k >= ncand) break;
+            const float e = s32[k];
+            if (e < eb32 || (e == eb32 && ci[k] < bi)) { es32 = eb32; eb32 = e; kb = k; bi = ci[k]; ba = t.b[k]; }
+            else if (e < es32) es32 = e;
+        }
+        // every other candidate must be separated from the best by > 2 bnd
+#pragma unroll
+        for (int k = 0; k < K - 1; k++) {
+            if (k >= ncand) break;
+            if (k != kb && !((double)s32[k] - (double)eb32 > 2.0 * bnd)) clear = false;
+        }
+        const double ebd = (double)eb32;
+        if (!(fabs(ebd) > bnd)) clear = false;                                  // sign of the best
+        if (fabs(fabs(ebd) - (double)thr) <= bnd) clear = false;               // TIE_ACCEPT side
+        if (ncand > 1 && fabs(((double)es32 - ebd) - (double)thr) <= 2.0 * bnd) clear = false;   // TIE_ARGMIN side
+        if (clear) {
+            best = bi;
+            best_approx = ba;
+            if ((t.b[K - 1] - t.b[0]) < win) flags |= MPW_F_UNRESOLVED;
+            if (ncand > 1 && ((double)es32 - ebd) < (double)thr) flags |= MPW_F_TIE_ARGMIN;
+            improve = ebd < 0.0;
+            if (fabs(ebd) < (double)thr) flags |= MPW_F_TIE_ACCEPT;
+            return;
+        }
+    }
+    // pass 2 (rare): float64 sums over the support in ascending position
     double sc[K - 1];
 #pragma unroll
     for (int k = 0; k < K - 1; k++) sc[k] = 0.0;
-    // y in 16-value half words: the next half's loads are in flight while the
-    // current half is converted to float64 once (sign of x folded in) and
-    // added into every window candidate whose support holds the position
-    const float4* y4 = reinterpret_cast<const float4*>(yrow);
-    float4 yb[2][4];
-#pragma unroll
-    for (int q = 0; q < 4; q++) yb[0][q] = __ldg(y4 + q);
-    uint32_t bits[K - 1];
-#pragma unroll
+    // y in 16-value half words, converted to float64 once (sign of x folded in)
+    // and added into every window candidate whose support holds the position
+#pragma unroll 1
     for (int hw = 0; hw < 2 * NW; hw++) {
         const int w = hw >> 1, sh = (hw & 1) * 16;
-        if (hw + 1 < 2 * NW) {
+        float4 yq[4];
 #pragma unroll
-            for (int q = 0; q < 4; q++) yb[(hw + 1) & 1][q] = __ldg(y4 + (hw + 1) * 4 + q);
-        }
-        if (sh == 0) {
+        for (int q = 0; q < 4; q++) yq[q] = YSMEM ? y4[hw * 4 + q] : __ldg(y4 + hw * 4 + q);
+        const float* yv = reinterpret_cast<const float*>(yq);
+        const uint32_t cw = select_word<NW>(c, w) >> sh;
+        uint32_t bw2[K - 1];
 #pragma unroll
-            for (int k = 0; k < K - 1; k++) bits[k] = (k < ncand) ? __ldg(pbits + (size_t)t.i[k] * NW + w) : 0u;
-        }
-        const float* yv = reinterpret_cast<const float*>(yb[hw & 1]);
-        const uint32_t cw = c[w] >> sh;
+        for (int k = 0; k < K - 1; k++) bw2[k] = (k < ncand) ? __ldg(pbits + (size_t)ci[k] * NW + w) : 0u;
         double yd[16];
 #pragma unroll
         for (int bb = 0; bb < 16; bb++) {
@@ -294,7 +381,7 @@ __device__ __forceinline__ void certify_window(const TopK<K>& t, const float* __
 #pragma unroll
         for (int k = 0; k < K - 1; k++) {
             if (k >= ncand) break;
-            const uint32_t bk = bits[k] >> sh;
+            const uint32_t bk = bw2[k] >> sh;
 #pragma unroll
             for (int bb = 0; bb < 16; bb++)
                 if ((bk >> bb) & 1u) sc[k] += yd[bb];
@@ -302,15 +389,17 @@ __device__ __forceinline__ void certify_window(const TopK<K>& t, const float* __
     }
     double eb = sc[0];
     double e_second = CUDART_INF;
+    int kb = 0;
 #pragma unroll
     for (int k = 1; k < K - 1; k++) {
         if (k >= ncand) break;
         const double e = sc[k];
-        if (e < eb || (e == eb && t.i[k] < best)) {
+        if (e < eb || (e == eb && ci[k] < best)) {
             e_second = eb;
             eb = e;
-            best = t.i[k];
+            best = ci[k];
             best_approx = t.b[k];
+            kb = k;
         } else if (e < e_second) {
             e_second = e;
         }
@@ -328,6 +417,8 @@ template <int KB, int NW, int LIMBS, int MODE>
 __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
     constexpr int STAGES = stages_for(KB, LIMBS);
     constexpr bool PROF = MODE == 2;
+    // round-end staging of every row's received word in the (then idle) B ring
+    constexpr bool YSTAGE = ROWS * NW * 32 * 4 <= STAGES * B_STAGE_BYTES;
     const int xp = PROF ? prm.experiment : 0;
     long long* const trace = MODE >= 1 ? prm.trace : nullptr;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -336,14 +427,16 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
     unsigned char* a_lo = sm + KB * A_KBLK_BYTES;          // used only when LIMBS == 2
     unsigned char* b_ring = sm + LIMBS * KB * A_KBLK_BYTES;
     PoolEnt* pool = reinterpret_cast<PoolEnt*>(b_ring + STAGES * B_STAGE_BYTES);   // [POOL]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(pool + POOL);
+    float* row_wadd = reinterpret_cast<float*>(pool + POOL);                        // [ROWS]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(row_wadd + ROWS);
     // barriers: full[STAGES], empty[STAGES], tfull[2], tempty[2], go
     uint64_t* full = bars;
     uint64_t* empty = bars + STAGES;
     uint64_t* tfull = bars + 2 * STAGES;
     uint64_t* tempty = tfull + 2;
     uint64_t* go = tempty + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(go + 1);
+    uint64_t* ybar = go + 1;      // [2]: rows' y staged for certification / for refills
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ybar + 2);
     volatile int* done_flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
     int* pool_head = const_cast<int*>(done_flag) + 1;     // next pool index to consume
     volatile int* pool_tail = pool_head + 1;              // pool indices < tail hold entries
@@ -355,6 +448,8 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
         for (int s = 0; s < STAGES; s++) { mbar_init(smem_u32(&full[s]), 1); mbar_init(smem_u32(&empty[s]), 1); }
         for (int b = 0; b < 2; b++) { mbar_init(smem_u32(&tfull[b]), 1); mbar_init(smem_u32(&tempty[b]), EPI_WARPS); }
         mbar_init(smem_u32(go), 1);
+        mbar_init(smem_u32(&ybar[0]), 128);
+        mbar_init(smem_u32(&ybar[1]), 128);
         *done_flag = 0;
         *pool_head = 0;
         *pool_tail = 0;
@@ -370,40 +465,25 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
     const uint32_t tmem_base = *tmem_slot;
 
     if (warp == 0) {
-        // ===== producer: streams P tiles round after round without waiting for
-        // the round end (the ring runs ahead into the next round while the
-        // epilogue decides and refills).  While it waits for a free stage it
-        // polls done_flag; once set it stops and waits for the copies it
-        // issued that the MMA will never consume.
+        // ===== producer: one pass over the P tiles per round, started by the
+        // round's go (between rounds the ring holds the rows' received words
+        // for the round-end certification and refills)
         if (lane == 0) {
             int stage = 0;
-            uint32_t phase = 0, issued = 0;
-            bool quit = false;
-            for (uint32_t round = 0; !quit; round++) {
-                if (xp & 64) {   // profiling: no run-ahead across the round end
-                    mbar_wait(smem_u32(go), round & 1);
-                    if (*done_flag) break;
-                }
-                for (int j = 0; j < ntiles && !quit; j++) {
+            uint32_t phase = 0;
+            for (uint32_t round = 0;; round++) {
+                mbar_wait(smem_u32(go), round & 1);
+                if (*done_flag) break;
+                for (int j = 0; j < ntiles; j++) {
                     for (int kb = 0; kb < KB; kb++) {
-                        const uint32_t eb = smem_u32(&empty[stage]);
-                        while (!mbar_try_hint(eb, phase ^ 1)) {
-                            if (*done_flag) { quit = true; break; }
-                        }
-                        if (quit) break;
+                        mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
                         const uint32_t fb = smem_u32(&full[stage]);
                         mbar_expect_tx(fb, B_STAGE_BYTES);
                         bulk_g2s(smem_u32(b_ring + stage * B_STAGE_BYTES),
                                  prm.btiles + ((size_t)j * KB + kb) * B_STAGE_BYTES, B_STAGE_BYTES, fb);
-                        issued++;
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
                     }
                 }
-            }
-            const uint32_t pending = issued < (uint32_t)STAGES ? issued : (uint32_t)STAGES;
-            for (uint32_t k = 0; k < pending; k++) {
-                if (stage == 0) { stage = STAGES - 1; phase ^= 1; } else stage--;
-                mbar_wait(smem_u32(&full[stage]), phase);
             }
         }
     } else if (warp == 1) {
@@ -503,13 +583,14 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
         };
         // next prefetched trajectory from the CTA pool (entries published at
         // the previous round end; tr < 0 marks a claim that found no work)
-        auto claim_pool = [&]() -> bool {
+        auto claim_pool = [&](int& pidx) -> bool {
             const int tail = *pool_tail;
             for (;;) {
                 const int idx = atomicAdd(pool_head, 1);
                 if (idx >= tail) return false;
                 const PoolEnt& e = pool[idx % POOL];
                 if (e.tr < 0) continue;
+                pidx = idx;
                 tr = e.tr;
                 frame = e.frame;
                 err_row = e.err;
@@ -520,19 +601,22 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
         };
         // A row of the new centre: t = x ⊙ y split into fp16 limbs, canonical
         // fp32 ED; y is read one 32-value word ahead of its use
-        auto build_row = [&]() {
+        auto build_row = [&](const float* ysrc) {
             iters = 0;
             flags = 0;
-            ed = 0.f;
-            const float4* y4 = reinterpret_cast<const float4*>(prm.y + (size_t)frame * n);
+            // fp16(x*y) = x*fp16(y) (round-to-nearest is sign symmetric), so each
+            // pair is one f16x2 conversion and a sign-bit flip; the fp32 canonical
+            // ED (only used for the tie window) is |y|^2 + N - 2 sum_i x_i y_i
+            float syy = 0.f, sxy = 0.f;
+            const float4* y4 = reinterpret_cast<const float4*>(ysrc);
             float4 yb[2][8];
 #pragma unroll
-            for (int q = 0; q < 8; q++) yb[0][q] = __ldg(y4 + q);
+            for (int q = 0; q < 8; q++) yb[0][q] = y4[q];
 #pragma unroll
             for (int w = 0; w < NW; w++) {
                 if (w + 1 < NW) {
 #pragma unroll
-                    for (int q = 0; q < 8; q++) yb[(w + 1) & 1][q] = __ldg(y4 + (w + 1) * 8 + q);
+                    for (int q = 0; q < 8; q++) yb[(w + 1) & 1][q] = y4[(w + 1) * 8 + q];
                 }
                 const float* yw = reinterpret_cast<const float*>(yb[w & 1]);
                 const uint32_t cw = c[w];
@@ -542,19 +626,18 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
 #pragma unroll
                     for (int e = 0; e < 8; e += 2) {
                         const int b0 = qq * 8 + e;
-                        const float x0 = ((cw >> b0) & 1u) ? -1.f : 1.f;
-                        const float x1 = ((cw >> (b0 + 1)) & 1u) ? -1.f : 1.f;
-                        const float t0 = x0 * yw[b0], t1 = x1 * yw[b0 + 1];
-                        const __half h0 = __float2half_rn(t0), h1 = __float2half_rn(t1);
-                        hi[e / 2] = (uint32_t)__half_as_ushort(h0) | ((uint32_t)__half_as_ushort(h1) << 16);
+                        const float y0 = yw[b0], y1 = yw[b0 + 1];
+                        const uint32_t sgn = (((cw >> b0) & 1u) << 15) | (((cw >> (b0 + 1)) & 1u) << 31);
+                        const __half2 h = __floats2half2_rn(y0, y1);
+                        hi[e / 2] = *reinterpret_cast<const uint32_t*>(&h) ^ sgn;
                         if (LIMBS == 2) {
-                            const __half l0 = __float2half_rn(t0 - __half2float(h0));
-                            const __half l1 = __float2half_rn(t1 - __half2float(h1));
-                            lo[e / 2] = (uint32_t)__half_as_ushort(l0) | ((uint32_t)__half_as_ushort(l1) << 16);
+                            const __half2 l = __floats2half2_rn(y0 - __low2float(h), y1 - __high2float(h));
+                            lo[e / 2] = *reinterpret_cast<const uint32_t*>(&l) ^ sgn;
                         }
-                        const float d0 = yw[b0] - x0, d1 = yw[b0 + 1] - x1;
-                        ed = fmaf(d0, d0, ed);
-                        ed = fmaf(d1, d1, ed);
+                        syy = fmaf(y0, y0, syy);
+                        syy = fmaf(y1, y1, syy);
+                        sxy += __uint_as_float(__float_as_uint(y0) ^ (((cw >> b0) & 1u) << 31));
+                        sxy += __uint_as_float(__float_as_uint(y1) ^ (((cw >> (b0 + 1)) & 1u) << 31));
                     }
                     const int c8 = w * 4 + qq;
                     const int kb = c8 >> 3, col = (c8 & 7) * 8;
@@ -563,6 +646,7 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
                     if (LIMBS == 2) *reinterpret_cast<uint4*>(a_lo + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
                 }
             }
+            ed = syy + (float)n - 2.0f * sxy;
         };
         auto store_row = [&]() {
 #pragma unroll
@@ -604,7 +688,8 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
 
         if (primary) {
             active = claim_direct();
-            if (active) build_row();
+            if (active) build_row(prm.y + (size_t)frame * n);
+            row_wadd[row] = 2.0f * err_row + prm.tie_rel * ed * 0.25f;
         }
         fence_proxy_async();
         int any = epi_bar_or(active);
@@ -613,11 +698,17 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
             mbar_arrive(smem_u32(go));
         }
         p_fill = use_pool ? POOL : 0;
-        uint32_t gtile = 0;
+        uint32_t gtile = 0, rnd = 0;
+        constexpr uint32_t YB = NW * 32 * 4;                      // bytes of one received word
+        float* const ysm = reinterpret_cast<float*>(b_ring + (size_t)row * YB);
+        // pool entries whose y is staged beside the rows' at the round end
+        constexpr int XS_FIT = YSTAGE ? (int)((STAGES * B_STAGE_BYTES - ROWS * YB) / YB) : 0;
+        constexpr int XS = XS_FIT < POOL ? XS_FIT : POOL;
+        int xs_base = 0;
         const bool dbg_on = (xp & 8) && blockIdx.x == 0 && primary && row == 0;
         const bool dbg_seg = (xp & 8) && blockIdx.x == 0;
         long long t_scan = 0, t_round = 0, t_mark = 0, t_scan0 = 0, n_rounds = 0, t_early = 0;
-        long long seg[6] = {0, 0, 0, 0, 0, 0}, t_seg = 0;
+        long long seg[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, t_seg = 0, n_pool = 0, n_direct = 0;
 #define SEG(k) if (dbg_seg) { const long long t_ = clock64(); seg[k] += t_ - t_seg; t_seg = t_; }
         while (any) {
             if (dbg_on) t_scan0 = clock64();
@@ -626,7 +717,8 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
             // insertion threshold: the K-th best, but never above best + window --
             // candidates outside the certification window of the running best can
             // never be needed (running best >= final best)
-            const float wadd = 2.0f * err_row + prm.tie_rel * ed * 0.25f;
+            // (the secondary half of a row reads the window its primary published)
+            const float wadd = primary ? 2.0f * err_row + prm.tie_rel * ed * 0.25f : row_wadd[row];
             float lastv = CUDART_INF_F;   // min(top.last(), top.b[0] + wadd)
             for (int j = 0; j < ntiles; j++, gtile++) {
                 const uint32_t buf = gtile & 1;
@@ -635,21 +727,43 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
                 tc_fence_after();
                 const bool tr_on = trace && blockIdx.x == 0 && gtile < (uint32_t)TRACE_TILES && lane == 0;
                 if (tr_on) trace[(size_t)gtile * TRACE_W + warp] = clock64();
+                if (YSTAGE && primary && j == ntiles - 1) {
+                    // every MMA of the round is complete: the B ring is idle until
+                    // the next go.  Stage this row's y there for the certification,
+                    // and the y of the next XS pool entries for this round's refills.
+                    xs_base = *reinterpret_cast<volatile int*>(pool_head);
+                    const int ptail = *pool_tail;
+                    bool xs_on = false;
+                    int xf = 0;
+                    if (row < XS && xs_base + row < ptail) {
+                        const PoolEnt& e = pool[(xs_base + row) % POOL];
+                        xs_on = e.tr >= 0;
+                        xf = e.frame;
+                    }
+                    mbar_expect_tx(smem_u32(&ybar[0]), (active ? YB : 0u) + (xs_on ? YB : 0u));
+                    if (active) bulk_g2s(smem_u32(ysm), prm.y + (size_t)frame * n, YB, smem_u32(&ybar[0]));
+                    if (xs_on)
+                        bulk_g2s(smem_u32(b_ring + (size_t)(ROWS + row) * YB), prm.y + (size_t)xf * n, YB,
+                                 smem_u32(&ybar[0]));
+                }
                 const int pbase = j * NT_COLS;
+                const bool tail = pbase + NT_COLS > np_;
                 // slow path (rare per lane once the running best settles): values
                 // below the threshold are inserted in increasing index order (ties
                 // keep the lowest index); register values are picked by a select
-                // tree.  Columns past |P| (zero pattern columns of the last tile)
-                // are skipped here, so the min trees need no tail masking.
-                auto slow = [&](const uint32_t (&v)[32], int p0) {
+                // tree.
+                auto slow = [&](const uint32_t (&v)[32], int p0, float mn) {
+                    // after this chunk the running best is <= mn, so nothing at or
+                    // above mn + wadd can enter the final window: tighten first
+                    const float lim = fminf(lastv, mn + wadd);
                     uint32_t hits = 0;
 #pragma unroll
-                    for (int e = 0; e < 32; e++) hits |= (__uint_as_float(v[e]) < lastv ? 1u : 0u) << e;
+                    for (int e = 0; e < 32; e++) hits |= (__uint_as_float(v[e]) < lim ? 1u : 0u) << e;
                     while (hits) {
                         const int e = __ffs(hits) - 1;
                         hits &= hits - 1;
                         const float sv = select32(v, e);
-                        if (sv < lastv && p0 + e < np_) {
+                        if (sv < lastv) {
                             top.insert_inline(sv, p0 + e);
                             lastv = fminf(top.last(), top.b[0] + wadd);
                         }
@@ -671,10 +785,18 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
                         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                     }
                     if (PROF && (xp & 1)) continue;
+                    if (tail) {   // zero pattern columns past |P| in the last tile
+                        const int pa = pbase + (ch0 + k) * 32;
+#pragma unroll
+                        for (int e = 0; e < 32; e++) {
+                            if (pa + e >= np_) va[e] = __float_as_uint(CUDART_INF_F);
+                            if (pa + 32 + e >= np_) vb[e] = __float_as_uint(CUDART_INF_F);
+                        }
+                    }
                     const float ma = min32(va), mb = min32(vb);
                     if (PROF && (xp & 16)) { if (ma == -12345.f || mb == -12345.f) top.b[0] = 0.f; continue; }
-                    if (ma < lastv) slow(va, pbase + (ch0 + k) * 32);
-                    if (mb < lastv) slow(vb, pbase + (ch0 + k + 1) * 32);
+                    if (ma < lastv) slow(va, pbase + (ch0 + k) * 32, ma);
+                    if (mb < lastv) slow(vb, pbase + (ch0 + k + 1) * 32, mb);
                 }
                 tc_fence_before();
                 __syncwarp();
@@ -718,20 +840,29 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
                     }
                 }
             }
+            if (YSTAGE && primary) mbar_wait(smem_u32(&ybar[0]), rnd & 1);
+            bool refill = false;
             if (active) {
                 iters++;
                 int i1;
                 bool improve;
                 float sb;
-                certify_window<TOPK, NW>(top, prm.y + (size_t)frame * n, c, prm.pbits, ed, prm.tie_rel, err_row, i1,
-                                         improve, sb, flags);
+                uint32_t pwv[NW];
+                bool have_bits;
+                if (YSTAGE)
+                    certify_window<TOPK, NW, true>(top, ysm, c, prm.pbits, ed, prm.tie_rel, err_row, i1, improve, sb,
+                                                   flags, pwv, have_bits);
+                else
+                    certify_window<TOPK, NW, false>(top, prm.y + (size_t)frame * n, c, prm.pbits, ed, prm.tie_rel,
+                                                    err_row, i1, improve, sb, flags, pwv, have_bits);
                 SEG(2);
                 if (improve) {
                     // flip the fp16 sign bits of the moved positions 8 at a time
                     // (one 16-byte RMW per swizzle chunk, no per-bit loop)
-                    uint32_t pwv[NW];
+                    if (!have_bits) {
 #pragma unroll
-                    for (int w = 0; w < NW; w++) pwv[w] = __ldg(prm.pbits + (size_t)i1 * NW + w);
+                        for (int w = 0; w < NW; w++) pwv[w] = __ldg(prm.pbits + (size_t)i1 * NW + w);
+                    }
                     {
 #pragma unroll
                         for (int w = 0; w < NW; w++) {
@@ -769,11 +900,26 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
                     if (prm.s2.traj_hops)
                         for (int h = iters - (improve ? 0 : 1); h < T; h++) prm.s2.traj_hops[(size_t)tr * T + h] = -1;
                     store_row();
-                    active = claim_pool() || claim_direct();
-                    if (active) build_row();
+                    SEG(6);
+                    int pidx = -1;
+                    active = claim_pool(pidx);
+                    if (dbg_seg) { n_pool += active; }
+                    if (!active) { active = claim_direct(); if (dbg_seg) n_direct++; }
+                    refill = active;
+                    SEG(7);
+                    if (refill) {
+                        const int xs = pidx - xs_base;
+                        const float* ysrc = (pidx >= 0 && xs >= 0 && xs < XS)
+                                                ? reinterpret_cast<const float*>(b_ring + (size_t)(ROWS + xs) * YB)
+                                                : prm.y + (size_t)frame * n;
+                        build_row(ysrc);
+                    }
+                    SEG(9);
                 }
             }
+            rnd++;
             SEG(4);
+            if (primary) row_wadd[row] = 2.0f * err_row + prm.tie_rel * ed * 0.25f;
             fence_proxy_async();
             any = epi_bar_or(active);
             SEG(5);
@@ -795,12 +941,18 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
 #undef SEG
         if (dbg_seg) {
 #pragma unroll
-            for (int k = 0; k < 6; k++)
+            for (int k = 0; k < 10; k++)
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) seg[k] = max(seg[k], __shfl_xor_sync(MPW_FULL, seg[k], o));
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                n_pool += __shfl_xor_sync(MPW_FULL, n_pool, o);
+                n_direct += __shfl_xor_sync(MPW_FULL, n_direct, o);
+            }
             if (lane == 0)
-                printf("[hop_tc seg] warp %d: pre-merge %lld merge-wait %lld certify %lld move %lld refill %lld or-wait %lld\n",
-                       warp, seg[0], seg[1], seg[2], seg[3], seg[4], seg[5]);
+                printf("[hop_tc seg] warp %d: pre-merge %lld merge-wait %lld certify %lld move %lld refill %lld or-wait %lld"
+                       " | store %lld claim %lld ycopy %lld build %lld | pool %lld direct %lld\n",
+                       warp, seg[0], seg[1], seg[2], seg[3], seg[4], seg[5], seg[6], seg[7], seg[8], seg[9], n_pool, n_direct);
         }
     }
     tc_fence_before();

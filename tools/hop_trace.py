@@ -16,7 +16,7 @@ first_wake = wake.min(1)
 last_done = done.max(1)
 period = np.diff(first_wake)
 epi = last_done - first_wake
-print(f"tiles {n}")
+print(f"tiles {n}, CTA-0 cycles first wake -> last done: {int(last_done[-1] - first_wake[0])}")
 print("tile period (first wake to first wake): median %d  mean %.0f  p90 %d  p99 %d" % (
     np.median(period), period.mean(), np.percentile(period, 90), np.percentile(period, 99)))
 print("epilogue span per tile (first wake to last done): median %d mean %.0f p90 %d" % (

@@ -244,7 +244,8 @@ struct Params {
     long long* trace;      // experiment & 128: per-tile clock64 trace of CTA 0 (TRACE_W per tile)
     int experiment;        // profiling knob: 1 skip epilogue math, 2 skip TMEM loads, 4 force T scans,
                            // 8 cycle report from CTA 0, 16 skip top-K insertion, 32 no work pool,
-                           // 64 producer waits for the round end
+                           // 64 producer waits for the round end, 256 no P reloads after round 0, 1024 P tiles
+                           // fetched twice (power probes)
 };
 
 // Certified decision (same rule and arithmetic as certify_topk in
@@ -478,9 +479,21 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
                     for (int kb = 0; kb < KB; kb++) {
                         mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
                         const uint32_t fb = smem_u32(&full[stage]);
-                        mbar_expect_tx(fb, B_STAGE_BYTES);
-                        bulk_g2s(smem_u32(b_ring + stage * B_STAGE_BYTES),
-                                 prm.btiles + ((size_t)j * KB + kb) * B_STAGE_BYTES, B_STAGE_BYTES, fb);
+                        if (PROF && (xp & 256) && round > 0) {
+                            // profiling only (results wrong): no P traffic after the first round
+                            mbar_arrive(fb);
+                        } else if (PROF && (xp & 1024)) {
+                            // profiling only: every P tile fetched twice (doubles the L2->SM stream)
+                            mbar_expect_tx(fb, 2 * B_STAGE_BYTES);
+                            bulk_g2s(smem_u32(b_ring + stage * B_STAGE_BYTES),
+                                     prm.btiles + ((size_t)j * KB + kb) * B_STAGE_BYTES, B_STAGE_BYTES, fb);
+                            bulk_g2s(smem_u32(b_ring + stage * B_STAGE_BYTES),
+                                     prm.btiles + ((size_t)j * KB + kb) * B_STAGE_BYTES, B_STAGE_BYTES, fb);
+                        } else {
+                            mbar_expect_tx(fb, B_STAGE_BYTES);
+                            bulk_g2s(smem_u32(b_ring + stage * B_STAGE_BYTES),
+                                     prm.btiles + ((size_t)j * KB + kb) * B_STAGE_BYTES, B_STAGE_BYTES, fb);
+                        }
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
                     }
                 }

@@ -55,10 +55,17 @@ __host__ __device__ inline SclLayout scl_layout(int n, int L, int nw) {
     return o;
 }
 
+// f(a,b) = sign(a)·sign(b)·min(|a|,|b|) with sign(0) = 0 (decoders.py:173-174),
+// evaluated on the IEEE bit patterns with integer ops (exact: magnitudes of
+// non-NaN doubles order like their unsigned bit patterns; a zero operand
+// gives +0.0).  Keeps the float64 pipe free for the g additions.
 __device__ __forceinline__ double scl_f(double a, double b) {
-    if (a == 0.0 || b == 0.0) return 0.0;
-    double mn = fmin(fabs(a), fabs(b));
-    return ((a < 0.0) != (b < 0.0)) ? -mn : mn;
+    const unsigned long long ia = (unsigned long long)__double_as_longlong(a);
+    const unsigned long long ib = (unsigned long long)__double_as_longlong(b);
+    const unsigned long long ma = ia & 0x7FFFFFFFFFFFFFFFull, mb = ib & 0x7FFFFFFFFFFFFFFFull;
+    const unsigned long long mn = ma < mb ? ma : mb;
+    const unsigned long long sg = (ia ^ ib) & 0x8000000000000000ull;
+    return __longlong_as_double((long long)(mn ? (mn | sg) : 0ull));
 }
 
 template <int NW>

@@ -41,7 +41,8 @@ struct SclLane {
     static constexpr size_t SVAL = (PTR + 4 * (size_t)L * PTRW + 7) & ~(size_t)7;
     static constexpr size_t SSRC = SVAL + 8 * (size_t)L;
     static constexpr size_t SBIT = SSRC + 4 * (size_t)L;
-    static constexpr size_t TOTAL = (SBIT + 4 * (size_t)L + 15) & ~(size_t)15;
+    static constexpr size_t CAND = (SBIT + 4 * (size_t)L + 15) & ~(size_t)15;   // (pm, pm+|dm|) per path
+    static constexpr size_t TOTAL = CAND + 16 * (size_t)L;
     // offset of stored level lvl (3..M) inside an instance
     __host__ __device__ static constexpr int off(int lvl) { return N / 4 - 2 * (N >> (lvl > 0 ? lvl : 0)); }
 };
@@ -158,6 +159,7 @@ __global__ void __launch_bounds__(128) scl_lane_kernel(CodeDev code, const float
     double* sel_val = reinterpret_cast<double*>(base + Lay::SVAL);
     int32_t* sel_src = reinterpret_cast<int32_t*>(base + Lay::SSRC);
     int32_t* sel_bit = reinterpret_cast<int32_t*>(base + Lay::SBIT);
+    double2* cand = reinterpret_cast<double2*>(base + Lay::CAND);
     uint32_t* psrow = ps_all + l * NWP;
     uint32_t* urow = u_all + l * NWP;
     uint8_t* ptrrow = ptr_all + l * Lay::PTRW * 4;
@@ -214,14 +216,17 @@ __global__ void __launch_bounds__(128) scl_lane_kernel(CodeDev code, const float
             if (frozen) {
                 pm = pm + fabs(dm) * (double)(dm < 0.0);                      // :216-218
             } else {
-                // stable rank of the 2L candidates (pm_k natural, pm_k + |dm_k| flipped)
+                // stable rank of the 2L candidates (pm_k natural, pm_k + |dm_k| flipped);
+                // every path publishes its pair once, then reads all L pairs with
+                // broadcast 16-byte loads (instead of 2L 64-bit shuffles)
                 const double vn = pm, vf = pm + fabs(dm);
+                cand[l] = make_double2(vn, vf);
+                __syncwarp();
                 int rn = 0, rf = 0;
 #pragma unroll
                 for (int k = 0; k < L; k++) {
-                    const double pk = __shfl_sync(MPW_FULL, pm, g0 + k);
-                    const double dk = __shfl_sync(MPW_FULL, dm, g0 + k);
-                    const double fk = pk + fabs(dk);
+                    const double2 ck = cand[k];
+                    const double pk = ck.x, fk = ck.y;
                     rn += (pk < vn) || (pk == vn && k < l);
                     rn += (fk < vn);
                     rf += (pk <= vf);

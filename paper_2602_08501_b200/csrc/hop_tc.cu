@@ -10,6 +10,12 @@
 // ---------------------------------------------------------------------------
 // host side
 
+// CTA-pair P streaming (multicast) for the cfg4 shape; MPW_TC_CLUSTER=0 disables it
+static bool tc_cluster() {
+    const char* e = getenv("MPW_TC_CLUSTER");
+    return !(e && atoi(e) == 0);
+}
+
 static int tc_experiment() {
     const char* e = getenv("MPW_TC_EXPERIMENT");
     return e ? atoi(e) : 0;
@@ -45,7 +51,7 @@ int tc_build(TcPatterns& t, const uint32_t* bits, int np, int n, int nw) {
     return 0;
 }
 
-template <int KB, int NW, int LIMBS, int MODE>
+template <int KB, int NW, int LIMBS, int MODE, int CL = 1>
 static int tc_launch_t(const TcPatterns& t, int n, int nw, int A, int T, const float* y, S2Dev s2, PatDev P,
                        int num_sms, cudaStream_t st) {
     tc::Params prm;
@@ -62,10 +68,31 @@ static int tc_launch_t(const TcPatterns& t, int n, int nw, int A, int T, const f
         prm.trace = trace;
     }
     const size_t smem = tc::smem_bytes(KB, LIMBS);
-    cudaError_t e = cudaFuncSetAttribute(tc::hop_tc_kernel<KB, NW, LIMBS, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+    auto kern = tc::hop_tc_kernel<KB, NW, LIMBS, MODE, CL>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return -(int)e;
-    tc::hop_tc_kernel<KB, NW, LIMBS, MODE><<<num_sms, tc::THREADS, smem, st>>>(prm);
+    if (CL == 1) {
+        kern<<<num_sms, tc::THREADS, smem, st>>>(prm);
+    } else {
+        // one CTA pair per two SMs (as many pairs as can be co-resident)
+        cudaLaunchConfig_t cfg = {};
+        cfg.blockDim = dim3(tc::THREADS);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = CL;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        cfg.gridDim = dim3((unsigned)((num_sms / CL) * CL));
+        int clusters = 0;
+        if (cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg) == cudaSuccess && clusters > 0)
+            cfg.gridDim = dim3((unsigned)(clusters * CL));
+        e = cudaLaunchKernelEx(&cfg, kern, prm);
+        if (e != cudaSuccess) return -(int)e;
+    }
     e = cudaGetLastError();
     if (e == cudaSuccess && prm.trace) {
         // profiling only: dump the trace of this launch (CTA 0), overwriting the previous one
@@ -89,9 +116,12 @@ int tc_launch(const TcPatterns& t, int n, int nw, int A, int T, const float* y, 
             case 256: {
                 // profiling builds of the cfg4 shape: 128 alone = trace only, other knobs = full
                 const int x = tc_experiment();
-                if (x == 128) return tc_launch_t<4, 8, 1, 1>(t, n, nw, A, T, y, s2, P, num_sms, st);
+                const bool pair = tc_cluster();
+                if (x == 128) return pair ? tc_launch_t<4, 8, 1, 1, 2>(t, n, nw, A, T, y, s2, P, num_sms, st)
+                                          : tc_launch_t<4, 8, 1, 1>(t, n, nw, A, T, y, s2, P, num_sms, st);
                 if (x) return tc_launch_t<4, 8, 1, 2>(t, n, nw, A, T, y, s2, P, num_sms, st);
-                return tc_launch_t<4, 8, 1, 0>(t, n, nw, A, T, y, s2, P, num_sms, st);
+                return pair ? tc_launch_t<4, 8, 1, 0, 2>(t, n, nw, A, T, y, s2, P, num_sms, st)
+                            : tc_launch_t<4, 8, 1, 0>(t, n, nw, A, T, y, s2, P, num_sms, st);
             }
             default: return 1;
         }

@@ -185,7 +185,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg4")
     ap.add_argument("--frames", type=int, default=1 << 17)
-    ap.add_argument("--variant", default="auto", choices=["auto", "gather", "tensor", "tensor2"])
+    ap.add_argument("--variant", default="auto", choices=["auto", "gather", "tensor", "tensor2", "tensor_i8"])
     ap.add_argument("--seed", type=int, default=2026)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-step-seconds", type=float, default=10.0)
@@ -282,7 +282,7 @@ def main():
         stage_h = torch.empty((F,), dtype=torch.uint8).pin_memory()
         ctr_h = torch.zeros((8,), dtype=torch.int64).pin_memory()
         mode = _native.MODE_CRC_GATED if cfg.activation_mode == "crc_gated" else _native.MODE_ALWAYS_ON
-        var = {"auto": 0, "gather": 1, "tensor": 2, "tensor2": 3}[args.variant]
+        var = {"auto": 0, "gather": 1, "tensor": 2, "tensor2": 3, "tensor_i8": 4}[args.variant]
         stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
         def host_step(i):
@@ -317,7 +317,18 @@ def main():
         variant_used = args.variant
         if variant_used == "auto":
             variant_used = "tensor" if dec.tensor_path_ready else "gather"
-        if variant_used in ("tensor", "tensor2"):
+        if variant_used == "tensor_i8":
+            ops = evals / ws * 2.0 * code.n                # 2N int8 tensor ops per evaluation
+            ach = ops / (hop_ms / 1000.0) / 1e12
+            peak = 2.0 * peaks["bf16_tflops"]              # the i8 MMA rate is twice the f16 rate per SM
+            traffic, tsrc = _ncu_traffic(f"hop_tc_i8_{args.frames}")
+            roof = {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TOP/s",
+                    "frac": ach / peak, "traffic": traffic, "traffic_source": tsrc,
+                    "kernel": "hop_tc_kernel<LIMBS=0> (kind::i8)", "op_per_eval": 2 * code.n,
+                    "peak_source": f"2 x {peak_kind} bf16_tflops (no measured int8 peak; kind::i8 issues at twice "
+                                   "the kind::f16 rate)",
+                    "nominal_peak": 4500.0, "frac_of_nominal": ach / 4500.0}
+        elif variant_used in ("tensor", "tensor2"):
             limbs = 1 if variant_used == "tensor" else 2
             flop = evals / ws * 2.0 * limbs * code.n  # limbs x 2N FLOP per evaluation
             ach = flop / (hop_ms / 1000.0) / 1e12
@@ -344,7 +355,8 @@ def main():
                 "scaling": "weak", "vs_baseline": None,
                 "dtype": {"gather": "f64 (stage 1) / f32 (stage 2 hop)",
                           "tensor": "f64 (stage 1) / f16 1-limb f32-accum screen + f64 certify (stage 2 hop)",
-                          "tensor2": "f64 (stage 1) / f16 2-limb f32-accum + f64 certify (stage 2 hop)"}[variant_used],
+                          "tensor2": "f64 (stage 1) / f16 2-limb f32-accum + f64 certify (stage 2 hop)",
+                          "tensor_i8": "f64 (stage 1) / int8 s32-accum screen + f32/f64 certify (stage 2 hop)"}[variant_used],
                 "data": "synthetic (seeded block-keyed Philox AWGN, host-generated)",
                 "config": _config(args, cfg, code, sph),
                 "evals_per_s": evals / (ms_max / 1000.0),

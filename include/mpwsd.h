@@ -56,6 +56,7 @@ extern "C" {
 #define MPW_HOP_GATHER 1  /* shared-memory gather-sum on CUDA cores */
 #define MPW_HOP_TENSOR 2  /* tcgen05, one fp16 limb of t, float64-certified top-4 (default) */
 #define MPW_HOP_TENSOR_2LIMB 3 /* tcgen05, fp16 hi+lo limbs of t, float64-certified top-4 */
+#define MPW_HOP_TENSOR_I8 4 /* tcgen05 kind::i8, per-frame int8 quantisation of t, certified top-16 (N = 128, 256) */
 
 /* counters (int64, accumulated by mpw_two_stage_batch; caller zeroes) */
 #define MPW_CTR_FRAMES 0

@@ -43,6 +43,7 @@ struct S2Dev {
     uint8_t* traj_flags;   // [cap x A] bit0 near-tie argmin, bit1 near-tie accept
     int32_t* work_next;    // [1] persistent-kernel work counter
     float4* ebound;        // [cap] per-frame score error bounds (warp_error_bounds)
+    float4* qscale;        // [cap] int8 quantisation of the frame (warp_i8_scale): inv_s, s, error bound
     int wmax;              // max pattern weight of P
 };
 
@@ -189,6 +190,41 @@ __device__ __forceinline__ float4 warp_error_bounds(const float* __restrict__ yr
     const float u = 1.1920929e-7f;   // 2^-23
     return make_float4(T1 + (float)wmax * u * A, T2 + 2.0f * (float)wmax * u * A,
                        (float)wmax * u * A, A);
+}
+
+// Per-frame int8 quantisation for the int8 tensor screen: t_i = ±y_i is
+// represented as s·q_i with q_i = ±rint(|y_i|·inv_s) in [-127, 127],
+// inv_s = 127 / max|y|, s = rcp_rn(inv_s) (the kernels repeat exactly these
+// fp32 operations).  The MMA sums the q_i exactly (s32 accumulators), so the
+// score error of every pattern is at most the sum of the wmax largest
+// |(|y_i| - s·q_i)| plus the fp32 rounding of s·acc and of the window
+// arithmetic (|acc| <= 127·wmax).  Returns {inv_s, s, bound, 0}.
+__device__ __forceinline__ float i8_inv_scale(float ymax) {
+    return ymax > 1e-30f ? __fdiv_rn(127.0f, ymax) : 1.0f;
+}
+__device__ __forceinline__ int i8_quant(float ay, float inv_s) { return __float2int_rn(__fmul_rn(ay, inv_s)); }
+
+__device__ __forceinline__ float4 warp_i8_scale(const float* __restrict__ yrow, int n, int wmax) {
+    const int lane = threadIdx.x & 31;
+    float ay[32], e8[32];
+    int cnt = 0;
+    float mx = 0.0f;
+    for (int i = lane; i < n; i += 32, cnt++) {
+        ay[cnt] = fabsf(yrow[i]);
+        mx = fmaxf(mx, ay[cnt]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(MPW_FULL, mx, o));
+    const float inv_s = i8_inv_scale(mx);
+    const float s = __frcp_rn(inv_s);
+    for (int j = 0; j < cnt; j++) {
+        const int q = i8_quant(ay[j], inv_s);
+        const double e = fabs((double)ay[j] - (double)s * (double)q);
+        e8[j] = __double2float_ru(e);
+    }
+    const float T8 = warp_topw_bound(e8, cnt, wmax);
+    const float u = 1.1920929e-7f;   // 2^-23
+    return make_float4(inv_s, s, T8 + 4.0f * u * s * 127.0f * (float)wmax, 0.0f);
 }
 
 // Running top-K (K small) of a scan; ascending values, index order breaks ties.

@@ -23,11 +23,44 @@ static int tc_experiment() {
 
 
 bool tc_supported(int n, int np) { return (n == 64 || n == 128 || n == 256) && np >= 1; }
+bool tc_i8_supported(int n, int np) { return (n == 128 || n == 256) && np >= 1; }
 
 void tc_release(TcPatterns& t) {
     if (t.tiles) cudaFree(t.tiles);
+    if (t.tiles8) cudaFree(t.tiles8);
     t.tiles = nullptr;
+    t.tiles8 = nullptr;
     t.ready = false;
+    t.ready8 = false;
+}
+
+// u8 0/1 images for the int8 screen: one 32 KB stage = 256 patterns x 128 positions
+static int tc_build8(TcPatterns& t, const uint32_t* bits, int np, int n, int nw) {
+    // packed (score, index) keys need |P| <= 2^17 and 127 * wmax < 8192
+    int wmax = 0;
+    for (int p = 0; p < np; p++) {
+        int w = 0;
+        for (int k = 0; k < nw; k++) w += __builtin_popcount(bits[(size_t)p * nw + k]);
+        wmax = w > wmax ? w : wmax;
+    }
+    if (np > (1 << tc::KEY_IBITS) || 127 * wmax >= tc::KEY_BIAS) return 0;   // int8 screen unavailable
+    const int kb = n / 128;
+    const int ntiles = (np + tc::NT_COLS - 1) / tc::NT_COLS;
+    const size_t bytes = (size_t)ntiles * kb * tc::B_STAGE_BYTES;
+    std::vector<uint8_t> img(bytes, 0);
+    for (int p = 0; p < np; p++) {
+        const int j = p / tc::NT_COLS, r = p % tc::NT_COLS;
+        for (int i = 0; i < n; i++) {
+            if (!((bits[(size_t)p * nw + (i >> 5)] >> (i & 31)) & 1u)) continue;
+            const int k = i / 128, col = i % 128;
+            img[((size_t)j * kb + k) * tc::B_STAGE_BYTES + tc::sw128_chunk(r, col >> 4) + (col & 15)] = 1;
+        }
+    }
+    if (cudaMalloc(&t.tiles8, bytes) != cudaSuccess) return -1;
+    if (cudaMemcpy(t.tiles8, img.data(), bytes, cudaMemcpyHostToDevice) != cudaSuccess) return -1;
+    t.kb8 = kb;
+    t.ready8 = true;
+    return 0;
 }
 
 int tc_build(TcPatterns& t, const uint32_t* bits, int np, int n, int nw) {
@@ -48,6 +81,7 @@ int tc_build(TcPatterns& t, const uint32_t* bits, int np, int n, int nw) {
     if (cudaMalloc(&t.tiles, bytes) != cudaSuccess) return -1;
     if (cudaMemcpy(t.tiles, img.data(), bytes, cudaMemcpyHostToDevice) != cudaSuccess) return -1;
     t.np = np; t.ntiles = ntiles; t.kb = kb; t.ready = true;
+    if (tc_i8_supported(n, np) && tc_build8(t, bits, np, n, nw)) return -1;
     return 0;
 }
 
@@ -56,7 +90,7 @@ static int tc_launch_t(const TcPatterns& t, int n, int nw, int A, int T, const f
                        int num_sms, cudaStream_t st) {
     tc::Params prm;
     prm.n = n; prm.nw = nw; prm.A = A; prm.T = T; prm.np = t.np; prm.ntiles = t.ntiles;
-    prm.y = y; prm.s2 = s2; prm.pbits = P.bits; prm.btiles = t.tiles; prm.tie_rel = 1e-5f;
+    prm.y = y; prm.s2 = s2; prm.pbits = P.bits; prm.btiles = LIMBS == 0 ? t.tiles8 : t.tiles; prm.tie_rel = 1e-5f;
     prm.err = 2e-3f;
     prm.experiment = tc_experiment();
     static long long* trace = nullptr;
@@ -72,11 +106,11 @@ static int tc_launch_t(const TcPatterns& t, int n, int nw, int A, int T, const f
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return -(int)e;
     if (CL == 1) {
-        kern<<<num_sms, tc::THREADS, smem, st>>>(prm);
+        kern<<<num_sms, tc::threads_for(LIMBS), smem, st>>>(prm);
     } else {
         // one CTA pair per two SMs (as many pairs as can be co-resident)
         cudaLaunchConfig_t cfg = {};
-        cfg.blockDim = dim3(tc::THREADS);
+        cfg.blockDim = dim3(tc::threads_for(LIMBS));
         cfg.dynamicSmemBytes = smem;
         cfg.stream = st;
         cudaLaunchAttribute attr[1];
@@ -109,6 +143,21 @@ static int tc_launch_t(const TcPatterns& t, int n, int nw, int A, int T, const f
 int tc_launch(const TcPatterns& t, int n, int nw, int A, int T, const float* y, S2Dev s2, PatDev P,
                      int num_sms, int limbs, cudaStream_t st) {
     if (!t.ready) return 1;
+    if (limbs == 0) {
+        if (!t.ready8) return 1;
+        switch (n) {
+            case 128: return tc_experiment() ? tc_launch_t<1, 4, 0, 2>(t, n, nw, A, T, y, s2, P, num_sms, st)
+                                             : tc_launch_t<1, 4, 0, 0>(t, n, nw, A, T, y, s2, P, num_sms, st);
+            case 256: {
+                const int x = tc_experiment();
+                if (x == 128) return tc_launch_t<2, 8, 0, 1, 2>(t, n, nw, A, T, y, s2, P, num_sms, st);
+                if (x) return tc_launch_t<2, 8, 0, 2>(t, n, nw, A, T, y, s2, P, num_sms, st);
+                return tc_cluster() ? tc_launch_t<2, 8, 0, 0, 2>(t, n, nw, A, T, y, s2, P, num_sms, st)
+                                    : tc_launch_t<2, 8, 0, 0>(t, n, nw, A, T, y, s2, P, num_sms, st);
+            }
+            default: return 1;
+        }
+    }
     if (limbs == 1) {
         switch (n) {
             case 64: return tc_launch_t<1, 2, 1, 0>(t, n, nw, A, T, y, s2, P, num_sms, st);

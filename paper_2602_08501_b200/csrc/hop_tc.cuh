@@ -17,6 +17,15 @@
 //   warps 2..5  epilogue: tcgen05.ld of the fp32 tile, argmin, moves, refills
 // TMEM: 2 accumulators x 256 fp32 columns (double buffer, 512 columns).
 // Shared memory: A_hi/A_lo [KB][128 rows x 64 fp16] SWIZZLE_128B, B ring.
+//
+// LIMBS = 0 selects the int8 screen: t is quantised per frame to
+// s·q_i, q_i ∈ [-127, 127] (warp_i8_scale in common.cuh), P is u8 0/1, and
+// tcgen05.mma.kind::i8 (K = 32 per instruction, twice the f16 rate) sums the
+// q_i exactly into s32 TMEM accumulators.  The epilogue works in q units
+// (integer min trees); the frame's bound on |S - s·acc| sets the wider
+// certification window, so the row keeps a top-16 instead of a top-6.
+// The smem geometry is unchanged: a 128-byte swizzle row holds 128 int8
+// instead of 64 fp16 elements, so a K-block covers twice the positions.
 #pragma once
 #include <cuda_fp16.h>
 
@@ -33,9 +42,10 @@ constexpr int NT_COLS = 256;     // UMMA N (patterns per tile)
 constexpr int KBLK = 64;         // fp16 elements per 128-byte swizzle row
 constexpr int B_STAGE_BYTES = NT_COLS * KBLK * 2;    // 32 KB
 constexpr int A_KBLK_BYTES = ROWS * KBLK * 2;        // 16 KB
-constexpr int EPI_WARPS = 8;     // two per TMEM lane quarter, each scans half of a tile
-constexpr int EPI_THREADS = 32 * EPI_WARPS;
-constexpr int THREADS = 64 + EPI_THREADS;
+// epilogue warps: two per TMEM lane quarter, each scans half of a tile (four
+// per quarter for the int8 screen measured slower: 96-register cap, spills)
+__host__ __device__ constexpr int epi_warps(int limbs) { return 8; }
+__host__ __device__ constexpr int threads_for(int limbs) { return 64 + 32 * epi_warps(limbs); }
 
 constexpr int SMEM_LIMIT = 232448;   // 227 KB opt-in maximum per CTA
 #ifndef MPW_TC_TOPK
@@ -43,6 +53,7 @@ constexpr int SMEM_LIMIT = 232448;   // 227 KB opt-in maximum per CTA
 #endif
 constexpr int TOPK = MPW_TC_TOPK;    // candidates tracked per row for certification
 static_assert(TOPK <= 8, "top-K hand-over uses 16 TMEM columns");
+constexpr int TOPK_I8 = 16;          // int8 screen: wider window (hand-over uses 32 columns)
 constexpr int TRACE_W = 18, TRACE_TILES = 1 << 16;
 constexpr int POOL = 64;                     // prefetched stage-2 work items per CTA
 
@@ -52,12 +63,14 @@ struct PoolEnt {
     int tr;            // trajectory id (queue slot * A + anchor), -1 = none
     int frame;
     float err;         // per-frame score error bound for this limb count
-    int pad;
+    int pad;           // int8 screen: the frame's inv_s (float bits)
 };
 constexpr int POOL_BYTES = POOL * (int)sizeof(PoolEnt);
 
+__host__ __device__ constexpr int a_buffers(int limbs) { return limbs == 2 ? 2 : 1; }
 __host__ __device__ constexpr int fixed_bytes(int kb, int limbs) {
-    return 1024 /*align slack*/ + limbs * kb * A_KBLK_BYTES + POOL_BYTES + ROWS * 4 /*row windows*/ + 256;
+    return 1024 /*align slack*/ + a_buffers(limbs) * kb * A_KBLK_BYTES + POOL_BYTES + ROWS * 4 /*row windows*/ +
+           (limbs == 0 ? ROWS * 8 : 0) /*int8 continuation state*/ + 256;
 }
 
 __host__ __device__ constexpr int stages_for(int kb, int limbs) {
@@ -185,18 +198,27 @@ __device__ __forceinline__ void tc_mma_f16(uint32_t d_tmem, uint64_t adesc, uint
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
+__device__ __forceinline__ void tc_mma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ void epi_bar_sync() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
-__device__ __forceinline__ void sec_bar_sync() { asm volatile("bar.sync 3, 128;" ::: "memory"); }
+template <int NT>
+__device__ __forceinline__ void epi_bar_sync() { asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory"); }
+template <int NT>
 __device__ __forceinline__ int epi_bar_or(int pred) {
     int r;
     asm volatile(
         "{\n\t.reg .pred p, q;\n\t"
         "setp.ne.s32 p, %1, 0;\n\t"
-        "bar.red.or.pred q, 2, 256, p;\n\t"
+        "bar.red.or.pred q, 2, %2, p;\n\t"
         "selp.s32 %0, 1, 0, q;\n\t}"
         : "=r"(r)
-        : "r"(pred)
+        : "r"(pred), "n"(NT)
         : "memory");
     return r;
 }
@@ -204,6 +226,19 @@ __device__ __forceinline__ int epi_bar_or(int pred) {
 #define TC_LD32(taddr, v)                                                                                   \
     asm volatile(                                                                                           \
         "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"     \
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                           \
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),   \
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),          \
+          "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),        \
+          "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),        \
+          "=r"(v[29]), "=r"(v[30]), "=r"(v[31])                                                             \
+        : "r"(taddr))
+
+// 64 s32 columns -> 32 registers of s16x2 (low half = even column); the int8
+// screen's scores fit 16 bits (|acc| <= 127 * wmax < 8192)
+#define TC_LD32P(taddr, v)                                                                                  \
+    asm volatile(                                                                                           \
+        "tcgen05.ld.sync.aligned.32x32b.x32.pack::16b.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15," \
         "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                           \
         : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),   \
           "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),          \
@@ -244,6 +279,54 @@ __device__ __forceinline__ float min32(const uint32_t (&v)[32]) {
     return fminf(fmin3(q0, q1, q2), q3);
 }
 
+__device__ __forceinline__ uint32_t min3_s16x2(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t r;
+    asm("min.s16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    asm("min.s16x2 %0, %1, %2;" : "=r"(r) : "r"(r), "r"(c));   // fused into VIMNMX3.S16x2
+    return r;
+}
+// minimum of 64 packed s16 values (32 registers): 16 three-input instructions, depth 4
+__device__ __forceinline__ int min64_s16(const uint32_t (&v)[32]) {
+    uint32_t m[11];
+#pragma unroll
+    for (int e = 0; e < 10; e++) m[e] = min3_s16x2(v[3 * e], v[3 * e + 1], v[3 * e + 2]);
+    uint32_t r;
+    asm("min.s16x2 %0, %1, %2;" : "=r"(r) : "r"(v[30]), "r"(v[31]));
+    m[10] = r;
+    const uint32_t q0 = min3_s16x2(m[0], m[1], m[2]), q1 = min3_s16x2(m[3], m[4], m[5]);
+    const uint32_t q2 = min3_s16x2(m[6], m[7], m[8]), q3 = min3_s16x2(m[9], m[10], q0);
+    const uint32_t f = min3_s16x2(q1, q2, q3);
+    return min((int)(short)(f & 0xFFFFu), (int)(short)(f >> 16));
+}
+
+// int8 screen: a candidate is one 32-bit key (acc + KEY_BIAS) << KEY_IBITS | p,
+// so key order = (score, pattern index) order (ties -> lowest index, as in
+// decoders.py:391) and a top-16 costs 16 registers.  Needs |acc| < KEY_BIAS
+// (127·wmax < 8192: wmax <= 64) and |P| <= 2^17 (checked on the host).
+constexpr int KEY_IBITS = 17;
+constexpr int KEY_BIAS = 8192;
+__device__ __forceinline__ uint32_t make_key(int acc, int p) {
+    return ((uint32_t)(acc + KEY_BIAS) << KEY_IBITS) | (uint32_t)p;
+}
+__device__ __forceinline__ int key_val(uint32_t key) { return (int)(key >> KEY_IBITS) - KEY_BIAS; }
+template <int K>
+struct TopKey {
+    uint32_t k[K];
+    __device__ __forceinline__ void reset() {
+#pragma unroll
+        for (int j = 0; j < K; j++) k[j] = 0xFFFFFFFFu;
+    }
+    // precondition: key < k[K-1]; branch-free sorted insertion
+    __device__ __forceinline__ void insert_inline(uint32_t key) {
+#pragma unroll
+        for (int j = K - 1; j > 0; j--) {
+            const bool up = key < k[j - 1];
+            k[j] = up ? k[j - 1] : (key < k[j] ? key : k[j]);
+        }
+        if (key < k[0]) k[0] = key;
+    }
+};
+
 // c[w] for a runtime w without local memory
 template <int NW>
 __device__ __forceinline__ uint32_t select_word(const uint32_t (&c)[NW], int w) {
@@ -254,7 +337,7 @@ __device__ __forceinline__ uint32_t select_word(const uint32_t (&c)[NW], int w) 
 }
 
 // v[e] for a runtime e without local memory: 5-level select tree (31 SEL)
-__device__ __forceinline__ float select32(const uint32_t (&v)[32], int e) {
+__device__ __forceinline__ uint32_t select32(const uint32_t (&v)[32], int e) {
     uint32_t a[16];
 #pragma unroll
     for (int k = 0; k < 16; k++) a[k] = (e & 16) ? v[k + 16] : v[k];
@@ -264,7 +347,7 @@ __device__ __forceinline__ float select32(const uint32_t (&v)[32], int e) {
     for (int k = 0; k < 4; k++) a[k] = (e & 4) ? a[k + 4] : a[k];
 #pragma unroll
     for (int k = 0; k < 2; k++) a[k] = (e & 2) ? a[k + 2] : a[k];
-    return __uint_as_float((e & 1) ? a[1] : a[0]);
+    return (e & 1) ? a[1] : a[0];
 }
 
 // K-major SWIZZLE_128B smem descriptor (sm100 format: version 1 at bit 46,
@@ -278,6 +361,12 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t addr) {
 __host__ __device__ __forceinline__ uint32_t sw128_off(int row, int col) {
     return (uint32_t)(row * 128 + ((((col >> 3) ^ (row & 7)) & 7) << 4) + ((col & 7) << 1));
 }
+// byte offset of 16-byte chunk ch (0..7) of row `row` inside one SW128 K-block
+__host__ __device__ __forceinline__ uint32_t sw128_chunk(int row, int ch) {
+    return (uint32_t)(row * 128 + (((ch ^ (row & 7)) & 7) << 4));
+}
+// 4-bit mask -> byte mask (bit k -> 0xFF in byte k)
+__device__ __forceinline__ uint32_t byte_mask4(uint32_t m4) { return ((m4 * 0x00204081u) & 0x01010101u) * 0xFFu; }
 
 struct Params {
     int n, nw, A, T, np, ntiles;
@@ -289,6 +378,7 @@ struct Params {
     float err;             // bound on |S_fp32 - S_exact| (S units)
     long long* trace;      // experiment & 128: per-tile clock64 trace of CTA 0 (TRACE_W per tile)
     int experiment;        // profiling knob: 1 skip epilogue math, 2 skip TMEM loads, 4 force T scans,
+                           // 2048 int8 window overflow at 4 keys (exercises the continuation passes),
                            // 8 cycle report from CTA 0, 16 skip top-K insertion, 32 no work pool,
                            // 64 producer waits for the round end, 256 no P reloads after round 0, 1024 P tiles
                            // fetched twice (power probes)
@@ -300,21 +390,25 @@ struct Params {
 // i.  Here all window candidates are scored in one pass over y, one 32-value
 // word at a time with the next word's loads in flight, so a row pays about
 // one L2 round trip instead of one per (candidate, word).
-template <int K, int NW, bool YSMEM>
+// FORCE: an improving best is always re-scored (the int8 screen's scores are
+// too coarse for the running ED); best_score returns the re-scored value when
+// there is one, else the approximation.
+template <int K, int NW, bool YSMEM, bool FORCE = false>
 __device__ __forceinline__ void certify_window(const TopK<K>& t, const float* __restrict__ yrow,
                                                const uint32_t (&c)[NW], const uint32_t* __restrict__ pbits,
                                                float ed, float tie_rel, float err_row, int& best, bool& improve,
                                                float& best_approx, uint8_t& flags, uint32_t (&best_bits)[NW],
-                                               bool& have_bits) {
+                                               bool& have_bits, float& best_score) {
     const float thr = tie_rel * ed * 0.25f;
     const float win = thr + 2.0f * err_row;
     best = t.i[0];
     best_approx = t.b[0];
     improve = t.b[0] < 0.0f;
     have_bits = false;
+    best_score = t.b[0];
     const bool pair = (t.b[1] - t.b[0]) < win;
     const bool zero = fabsf(t.b[0]) < err_row + thr;
-    if (!pair && !zero) return;
+    if (!pair && !zero && !(FORCE && improve)) return;
     // candidate indices copied out of the top-K (the loops below must not
     // address the top-K arrays, or they would be demoted to local memory)
     int ci[K - 1];
@@ -395,6 +489,7 @@ __device__ __forceinline__ void certify_window(const TopK<K>& t, const float* __
         if (clear) {
             best = bi;
             best_approx = ba;
+            best_score = eb32;
             if ((t.b[K - 1] - t.b[0]) < win) flags |= MPW_F_UNRESOLVED;
             if (ncand > 1 && ((double)es32 - ebd) < (double)thr) flags |= MPW_F_TIE_ARGMIN;
             improve = ebd < 0.0;
@@ -455,6 +550,7 @@ __device__ __forceinline__ void certify_window(const TopK<K>& t, const float* __
     if (e_second - eb < (double)thr) flags |= MPW_F_TIE_ARGMIN;
     improve = eb < 0.0;
     if (fabs(eb) < (double)thr) flags |= MPW_F_TIE_ACCEPT;
+    best_score = (float)eb;
 }
 
 // ---------------------------------------------------------------------------
@@ -464,9 +560,21 @@ __device__ __forceinline__ void certify_window(const TopK<K>& t, const float* __
 // fetches half of every stage and multicasts it to both), halving the L2->SM
 // traffic; the pair runs its rounds in step.
 template <int KB, int NW, int LIMBS, int MODE, int CL>
-__global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
+__global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params prm) {
     constexpr int STAGES = stages_for(KB, LIMBS);
     constexpr bool PROF = MODE == 2;
+    constexpr bool I8 = LIMBS == 0;                  // int8 screen (see the header comment)
+    constexpr int KT = I8 ? TOPK_I8 : TOPK;          // candidates tracked per row
+    // SUBS = 2 would issue every 256-pattern tile as two N = 128 sub-tiles into
+    // four 128-column accumulators (MMAs up to two tiles ahead of the
+    // epilogue); measured slower for int8 (N = 128 instructions run at ~64 % of
+    // the N = 256 rate), so every variant uses one N = 256 tile, two accumulators
+    constexpr int SUBS = 1;
+    constexpr int TW = NT_COLS / SUBS;               // accumulator columns per sub-tile
+    constexpr int NBUF = 2 * SUBS;                   // accumulators (NBUF x TW = 512 columns)
+    constexpr int EW = epi_warps(LIMBS);             // epilogue warps
+    constexpr int EPI_T = 32 * EW;
+    constexpr int WC = TW * 4 / EW;                  // accumulator columns per epilogue warp
     // round-end staging of every row's received word in the (then idle) B ring
     constexpr bool YSTAGE = ROWS * NW * 32 * 4 <= STAGES * B_STAGE_BYTES;
     const int xp = PROF ? prm.experiment : 0;
@@ -475,16 +583,19 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
     unsigned char* sm = reinterpret_cast<unsigned char*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     unsigned char* a_hi = sm;
     unsigned char* a_lo = sm + KB * A_KBLK_BYTES;          // used only when LIMBS == 2
-    unsigned char* b_ring = sm + LIMBS * KB * A_KBLK_BYTES;
+    unsigned char* b_ring = sm + a_buffers(LIMBS) * KB * A_KBLK_BYTES;
     PoolEnt* pool = reinterpret_cast<PoolEnt*>(b_ring + STAGES * B_STAGE_BYTES);   // [POOL]
     float* row_wadd = reinterpret_cast<float*>(pool + POOL);                        // [ROWS]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(row_wadd + ROWS);
+    // int8: per-row continuation state {key floor, window base} for the secondary half
+    uint2* row_cont = reinterpret_cast<uint2*>(row_wadd + ROWS);                    // [ROWS] (I8 only)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(row_wadd + ROWS) +
+                                                 (I8 ? ROWS * sizeof(uint2) : 0));
     // barriers: full[STAGES], empty[STAGES], tfull[2], tempty[2], go
     uint64_t* full = bars;
     uint64_t* empty = bars + STAGES;
     uint64_t* tfull = bars + 2 * STAGES;
-    uint64_t* tempty = tfull + 2;
-    uint64_t* go = tempty + 2;
+    uint64_t* tempty = tfull + NBUF;
+    uint64_t* go = tempty + NBUF;
     uint64_t* ybar = go + 1;      // [2]: rows' y staged for certification / for refills
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ybar + 2);
     volatile int* done_flag = reinterpret_cast<volatile int*>(tmem_slot + 1);
@@ -499,7 +610,7 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; s++) { mbar_init(smem_u32(&full[s]), 1); mbar_init(smem_u32(&empty[s]), CL); }
-        for (int b = 0; b < 2; b++) { mbar_init(smem_u32(&tfull[b]), 1); mbar_init(smem_u32(&tempty[b]), EPI_WARPS); }
+        for (int b = 0; b < NBUF; b++) { mbar_init(smem_u32(&tfull[b]), 1); mbar_init(smem_u32(&tempty[b]), EW); }
         mbar_init(smem_u32(go), CL);
         mbar_init(smem_u32(&ybar[0]), 128);
         mbar_init(smem_u32(&ybar[1]), 128);
@@ -573,7 +684,9 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
     } else if (warp == 1) {
         // ===== MMA issuer =====
         if (lane == 0) {
-            const uint32_t idesc = (1u << 4) | ((uint32_t)(NT_COLS >> 3) << 17) | ((uint32_t)(ROWS >> 4) << 24);
+            // f16: D f32 (1 << 4), A/B f16.  i8: D s32 (2 << 4), A s8 (1 << 7), B u8.
+            const uint32_t idesc = (I8 ? (2u << 4) | (1u << 7) : (1u << 4)) | ((uint32_t)(TW >> 3) << 17) |
+                                   ((uint32_t)(ROWS >> 4) << 24);
             int stage = 0;
             uint32_t phase = 0;
             uint32_t gtile = 0;
@@ -587,34 +700,50 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
                 if (!more) break;
                 tc_fence_after();
                 for (int j = 0; j < ntiles; j++, gtile++) {
-                    const uint32_t buf = gtile & 1;
+                  for (int h = 0; h < SUBS; h++) {
+                    // sub-tile h = patterns [h TW, (h+1) TW) of the tile: rows h TW.. of
+                    // every B stage (128 bytes per row), its own accumulator
+                    const uint32_t gs = gtile * SUBS + h;
+                    const uint32_t buf = gs % NBUF;
                     if (dbg) t0 = clock64();
-                    mbar_wait(smem_u32(&tempty[buf]), ((gtile >> 1) & 1) ^ 1);
+                    mbar_wait(smem_u32(&tempty[buf]), ((gs / NBUF) & 1) ^ 1);
                     if (dbg) w_tempty += clock64() - t0;
-                    const bool tr_on = trace && blockIdx.x == 0 && gtile < (uint32_t)TRACE_TILES;
-                    if (tr_on) trace[(size_t)gtile * TRACE_W] = clock64();
+                    const bool tr_on = trace && blockIdx.x == 0 && gs < (uint32_t)TRACE_TILES;
+                    if (tr_on) trace[(size_t)gs * TRACE_W] = clock64();
                     tc_fence_after();
-                    const uint32_t d = tmem_base + buf * NT_COLS;
+                    const uint32_t d = tmem_base + buf * TW;
+                    int st = stage;
+                    uint32_t ph = phase;
                     for (int kb = 0; kb < KB; kb++) {
-                        if (dbg) t0 = clock64();
-                        mbar_wait(smem_u32(&full[stage]), phase);
-                        if (dbg) w_full += clock64() - t0;
-                        tc_fence_after();
-                        const uint64_t bd = sw128_desc(bring + stage * B_STAGE_BYTES);
+                        if (h == 0) {
+                            if (dbg) t0 = clock64();
+                            mbar_wait(smem_u32(&full[st]), ph);
+                            if (dbg) w_full += clock64() - t0;
+                            tc_fence_after();
+                        }
+                        const uint64_t bd = sw128_desc(bring + st * B_STAGE_BYTES + h * TW * 128);
                         const uint64_t ah = sw128_desc(ahi + kb * A_KBLK_BYTES);
                         const uint64_t al = sw128_desc(alo + kb * A_KBLK_BYTES);
 #pragma unroll
-                        for (int ks = 0; ks < KBLK / 16; ks++) {
-                            // +32 bytes per 16-element K step inside the 128-byte swizzle row
-                            tc_mma_f16(d, ah + 2 * ks, bd + 2 * ks, idesc, (kb | ks) != 0);
-                            if (LIMBS == 2) tc_mma_f16(d, al + 2 * ks, bd + 2 * ks, idesc, 1u);
+                        for (int ks = 0; ks < 4; ks++) {
+                            // +32 bytes per K step (16 fp16 / 32 int8 elements) inside the 128-byte swizzle row
+                            if (I8) {
+                                tc_mma_i8(d, ah + 2 * ks, bd + 2 * ks, idesc, (kb | ks) != 0);
+                            } else {
+                                tc_mma_f16(d, ah + 2 * ks, bd + 2 * ks, idesc, (kb | ks) != 0);
+                                if (LIMBS == 2) tc_mma_f16(d, al + 2 * ks, bd + 2 * ks, idesc, 1u);
+                            }
                         }
-                        if (CL > 1) tc_commit_mc(smem_u32(&empty[stage]), CMASK);   // frees the stage in both CTAs
-                        else tc_commit(smem_u32(&empty[stage]));
-                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                        if (h == SUBS - 1) {   // the stage's last reader: free it
+                            if (CL > 1) tc_commit_mc(smem_u32(&empty[st]), CMASK);   // in both CTAs of the pair
+                            else tc_commit(smem_u32(&empty[st]));
+                        }
+                        if (++st == STAGES) { st = 0; ph ^= 1; }
                     }
                     tc_commit(smem_u32(&tfull[buf]));
-                    if (tr_on) trace[(size_t)gtile * TRACE_W + 1] = clock64();
+                    if (tr_on) trace[(size_t)gs * TRACE_W + 1] = clock64();
+                    if (h == SUBS - 1) { stage = st; phase = ph; }
+                  }
                 }
             }
             if (dbg) printf("[hop_tc mma] wait go %lld tempty %lld full %lld\n", w_go, w_tempty, w_full);
@@ -628,8 +757,9 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
         const int g = warp & 3;                  // TMEM lane quarter accessible to this warp
         const int row = g * 32 + lane;
         const bool primary = warp < 6;
-        const int sec = threadIdx.x - 64 - 128;  // secondary thread index 0..127
-        const int ch0 = primary ? 0 : (NT_COLS / 32) / 2;
+        const int grp = (warp - 2) >> 2;         // column group: 0 = primary, 1.. = secondary
+        const int sec = threadIdx.x - 64 - 128;  // secondary thread index (the pool uses 0..POOL-1)
+        const int ch0 = grp * (WC / 32);         // first 32-column chunk of this warp's columns
         const uint32_t t_lane = tmem_base + ((uint32_t)(g * 32) << 16);
         const int count = *prm.s2.count;
         const int ntraj = count * A;
@@ -637,6 +767,15 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
         int tr = -1;
         int iters = 0, frame = 0;
         float ed = 0.f, err_row = 0.f;
+        float inv_s = 1.f, sc = 1.f;             // int8 screen: quantisation of this row's frame
+        // int8 window overflow: when more than KT-1 candidates fall inside the
+        // certification window, the row re-scans P in the next round collecting
+        // the keys above kfloor (same window base cbase), and the exact scores
+        // of every pass are merged into (xb_s, xb_i, xs2) before deciding
+        uint32_t kfloor = 0u;
+        int cbase = 0;
+        double xb_s = CUDART_INF, xs2 = CUDART_INF;
+        int xb_i = 0;
         uint8_t flags = 0;
         bool active = false;
         // pool bookkeeping (identical in every secondary thread)
@@ -644,7 +783,7 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
         // this secondary thread's in-flight pool claim
         int cl_tr = -1, cl_q = 0;
         int cl_frame = 0, cl_nanc = 0;
-        float cl_err = 0.f;
+        float cl_err = 0.f, cl_inv = 1.f;
         // the pool needs three tile boundaries per round; with fewer tiles rows
         // refill straight from the global queue
         const int j_claim = ntiles >= 3 ? (ntiles / 2 < ntiles - 3 ? ntiles / 2 : ntiles - 3) : -1;
@@ -659,8 +798,15 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
                 if (a >= prm.s2.nanchor[q]) continue;
                 tr = cand;
                 frame = prm.s2.frame[q];
-                const float4 eb = prm.s2.ebound[q];
-                err_row = (LIMBS == 1) ? eb.x : eb.y;
+                if (I8) {
+                    const float4 qs = prm.s2.qscale[q];
+                    inv_s = qs.x;
+                    sc = qs.y;
+                    err_row = qs.z;
+                } else {
+                    const float4 eb = prm.s2.ebound[q];
+                    err_row = (LIMBS == 1) ? eb.x : eb.y;
+                }
 #pragma unroll
                 for (int w = 0; w < NW; w++) c[w] = prm.s2.anchors[(size_t)tr * NW + w];
                 return true;
@@ -679,6 +825,10 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
                 tr = e.tr;
                 frame = e.frame;
                 err_row = e.err;
+                if (I8) {
+                    inv_s = __int_as_float(e.pad);
+                    sc = __frcp_rn(inv_s);
+                }
 #pragma unroll
                 for (int w = 0; w < NW; w++) c[w] = __ldg(prm.s2.anchors + (size_t)tr * NW + w);
                 return true;
@@ -705,6 +855,33 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
                 }
                 const float* yw = reinterpret_cast<const float*>(yb[w & 1]);
                 const uint32_t cw = c[w];
+                if (I8) {
+                    // q_i = ±rint(|y_i| inv_s), negative iff sign(y_i) xor c_i; two
+                    // 16-byte chunks (16 positions each) per 32-position word
+#pragma unroll
+                    for (int h = 0; h < 2; h++) {
+                        uint32_t qw[4];
+#pragma unroll
+                        for (int e4 = 0; e4 < 4; e4++) {
+                            uint32_t acc = 0;
+#pragma unroll
+                            for (int b = 0; b < 4; b++) {
+                                const int bi = h * 16 + e4 * 4 + b;
+                                const float yv = yw[bi];
+                                const int q = i8_quant(fabsf(yv), inv_s);
+                                const bool neg = (((cw >> bi) & 1u) != 0u) != (yv < 0.0f);
+                                acc |= ((uint32_t)(neg ? -q : q) & 0xFFu) << (8 * b);
+                                syy = fmaf(yv, yv, syy);
+                                sxy += __uint_as_float(__float_as_uint(yv) ^ (((cw >> bi) & 1u) << 31));
+                            }
+                            qw[e4] = acc;
+                        }
+                        const int ch = w * 2 + h;
+                        *reinterpret_cast<uint4*>(a_hi + (ch >> 3) * A_KBLK_BYTES + sw128_chunk(row, ch & 7)) =
+                            make_uint4(qw[0], qw[1], qw[2], qw[3]);
+                    }
+                    continue;
+                }
 #pragma unroll
                 for (int qq = 0; qq < 4; qq++) {
                     uint32_t hi[4], lo[4];
@@ -754,8 +931,14 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
                     cl_q = cl_tr / A;
                     cl_nanc = prm.s2.nanchor[cl_q];
                     cl_frame = prm.s2.frame[cl_q];
-                    const float4 eb = prm.s2.ebound[cl_q];
-                    cl_err = (LIMBS == 1) ? eb.x : eb.y;
+                    if (I8) {
+                        const float4 qs = prm.s2.qscale[cl_q];
+                        cl_err = qs.z;
+                        cl_inv = qs.x;
+                    } else {
+                        const float4 eb = prm.s2.ebound[cl_q];
+                        cl_err = (LIMBS == 1) ? eb.x : eb.y;
+                    }
                 }
             } else {
                 PoolEnt& e = pool[(p_tail + sec) % POOL];
@@ -764,6 +947,7 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
                 if (ok) {
                     e.frame = cl_frame;
                     e.err = cl_err;
+                    e.pad = __float_as_int(cl_inv);
                     prefetch_l2(prm.s2.anchors + (size_t)cl_tr * NW);
                     const char* yl = reinterpret_cast<const char*>(prm.y + (size_t)cl_frame * n);
                     for (int o = 0; o < n * 4; o += 128) prefetch_l2(yl + o);
@@ -771,10 +955,18 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
             }
         };
 
+        // insertion window of the row in the epilogue's units (S units, or q
+        // units for the int8 screen: widened by the rounding of the conversion
+        // and one count, so it never excludes a candidate the S window keeps)
+        auto row_window = [&]() -> float {
+            const float w = 2.0f * err_row + prm.tie_rel * ed * 0.25f;
+            return I8 ? w * inv_s * 1.00001f + 1.0f : w;
+        };
         if (primary) {
             active = claim_direct();
             if (active) build_row(prm.y + (size_t)frame * n);
-            row_wadd[row] = 2.0f * err_row + prm.tie_rel * ed * 0.25f;
+            row_wadd[row] = row_window();
+            if (I8) row_cont[row] = make_uint2(0u, 0u);
         }
         // round-end signal: this CTA's rows-left flag to every CTA of the cluster,
         // then one arrive on every CTA's go barrier; the epilogue continues while
@@ -800,7 +992,7 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
             return more ? 1 : 0;
         };
         fence_proxy_async();
-        int any = signal_round(epi_bar_or(active));
+        int any = signal_round(epi_bar_or<EPI_T>(active));
         p_fill = use_pool ? POOL : 0;
         uint32_t gtile = 0, rnd = 0;
         constexpr uint32_t YB = NW * 32 * 4;                      // bytes of one received word
@@ -816,22 +1008,36 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
 #define SEG(k) if (dbg_seg) { const long long t_ = clock64(); seg[k] += t_ - t_seg; t_seg = t_; }
         while (any) {
             if (dbg_on) t_scan0 = clock64();
-            TopK<TOPK> top;
+            TopK<I8 ? 1 : KT> top;      // f16 screens: (score, index) pairs
             top.reset();
+            TopKey<I8 ? KT : 1> tk;     // int8 screen: packed keys
+            tk.reset();
             // insertion threshold: the K-th best, but never above best + window --
             // candidates outside the certification window of the running best can
             // never be needed (running best >= final best)
             // (the secondary half of a row reads the window its primary published)
-            const float wadd = primary ? 2.0f * err_row + prm.tie_rel * ed * 0.25f : row_wadd[row];
+            const float wadd = primary ? row_window() : row_wadd[row];
             float lastv = CUDART_INF_F;   // min(top.last(), top.b[0] + wadd)
+            const int wq = I8 ? __float2int_ru(wadd) : 0;          // int8: window in q units
+            // int8: scores below lastq go to the slow path (the K-th score
+            // itself included: a lower index with an equal score still enters)
+            uint2 cst = make_uint2(0u, 0u);
+            if (I8) cst = primary ? make_uint2(kfloor, (uint32_t)cbase) : row_cont[row];
+            const uint32_t kfl = cst.x;                 // keys <= kfl were examined by earlier passes
+            const int cb = (int)cst.y;
+            auto wbase = [&]() -> int { return kfl ? cb : key_val(tk.k[0]); };
+            int lastq = kfl ? cb + wq : 0x7FFFFFFF;
+            auto upd_lastq = [&]() { lastq = min(key_val(tk.k[KT - 1]) + 1, wbase() + wq); };
             for (int j = 0; j < ntiles; j++, gtile++) {
-                const uint32_t buf = gtile & 1;
-                if (dbg_on && j == 16) t_early += clock64() - t_scan0;
-                mbar_wait(smem_u32(&tfull[buf]), (gtile >> 1) & 1);
+              for (int h = 0; h < SUBS; h++) {
+                const uint32_t gs = gtile * SUBS + h;
+                const uint32_t buf = gs % NBUF;
+                if (dbg_on && j == 16 && h == 0) t_early += clock64() - t_scan0;
+                mbar_wait(smem_u32(&tfull[buf]), (gs / NBUF) & 1);
                 tc_fence_after();
-                const bool tr_on = trace && blockIdx.x == 0 && gtile < (uint32_t)TRACE_TILES && lane == 0;
-                if (tr_on) trace[(size_t)gtile * TRACE_W + warp] = clock64();
-                if (YSTAGE && primary && j == ntiles - 1) {
+                const bool tr_on = trace && blockIdx.x == 0 && gs < (uint32_t)TRACE_TILES && lane == 0;
+                if (tr_on) trace[(size_t)gs * TRACE_W + warp] = clock64();
+                if (YSTAGE && primary && j == ntiles - 1 && h == SUBS - 1) {
                     // every MMA of the round is complete: the B ring is idle until
                     // the next go.  Stage this row's y there for the certification,
                     // and the y of the next XS pool entries for this round's refills.
@@ -850,8 +1056,8 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
                         bulk_g2s(smem_u32(b_ring + (size_t)(ROWS + row) * YB), prm.y + (size_t)xf * n, YB,
                                  smem_u32(&ybar[0]));
                 }
-                const int pbase = j * NT_COLS;
-                const bool tail = pbase + NT_COLS > np_;
+                const int pbase = j * NT_COLS + h * TW;
+                const bool tail = pbase + TW > np_;
                 // slow path (rare per lane once the running best settles): values
                 // below the threshold are inserted in increasing index order (ties
                 // keep the lowest index); register values are picked by a select
@@ -866,20 +1072,80 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
                     while (hits) {
                         const int e = __ffs(hits) - 1;
                         hits &= hits - 1;
-                        const float sv = select32(v, e);
+                        const float sv = __uint_as_float(select32(v, e));
                         if (sv < lastv) {
                             top.insert_inline(sv, p0 + e);
                             lastv = fminf(top.last(), top.b[0] + wadd);
                         }
                     }
                 };
+                // int8 slow path over 64 packed scores (column p0 + 2e + half):
+                // keys carry the index, so the insertion order does not matter
+                auto slow8 = [&](const uint32_t (&v)[32], int p0, int mn) {
+                    const int lim = min(lastq, mn + wq);
+                    uint32_t hlo = 0, hhi = 0;
+#pragma unroll
+                    for (int e = 0; e < 32; e++) {
+                        hlo |= ((int)(short)(v[e] & 0xFFFFu) < lim ? 1u : 0u) << e;
+                        hhi |= ((int)(short)(v[e] >> 16) < lim ? 1u : 0u) << e;
+                    }
+                    auto take = [&](int sv, int p) {
+                        const uint32_t key = make_key(sv, p);
+                        if (key < tk.k[KT - 1] && key > kfl && sv < wbase() + wq) {
+                            tk.insert_inline(key);
+                            upd_lastq();
+                        }
+                    };
+                    while (hlo) {
+                        const int e = __ffs(hlo) - 1;
+                        hlo &= hlo - 1;
+                        take((int)(short)(select32(v, e) & 0xFFFFu), p0 + 2 * e);
+                    }
+                    while (hhi) {
+                        const int e = __ffs(hhi) - 1;
+                        hhi &= hhi - 1;
+                        take((int)(short)(select32(v, e) >> 16), p0 + 2 * e + 1);
+                    }
+                };
                 // two 32-column chunks per step: both TMEM loads in flight together,
                 // then two interleaved min trees
-                constexpr int NCH = (NT_COLS / 32) / 2;
-                const uint32_t tbase = t_lane + buf * NT_COLS + ch0 * 32;
+                constexpr int NCH = WC / 32;
+                const uint32_t tbase = t_lane + buf * TW + ch0 * 32;
                 uint32_t va[32], vb[32];
+                if constexpr (I8) {
+                    // the warp's TW/2 columns as packed s16 scores (64 per load), one wait
+                    constexpr int NLD = WC / 64;
+                    if (PROF && (xp & 2)) {
+#pragma unroll
+                        for (int e = 0; e < 32; e++) { va[e] = 0x7FFF7FFFu; vb[e] = va[e]; }
+                    } else {
+                        TC_LD32P(tbase, va);
+                        if constexpr (NLD == 2) TC_LD32P(tbase + 64, vb);
+                        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    }
+                    const int pa = pbase + ch0 * 32;
+                    if (tail) {
+#pragma unroll
+                        for (int e = 0; e < 32; e++) {
+                            if (pa + 2 * e >= np_) va[e] = (va[e] & 0xFFFF0000u) | 0x7FFFu;   // s16 max
+                            if (pa + 2 * e + 1 >= np_) va[e] = (va[e] & 0xFFFFu) | 0x7FFF0000u;
+                            if (pa + 64 + 2 * e >= np_) vb[e] = (vb[e] & 0xFFFF0000u) | 0x7FFFu;
+                            if (pa + 64 + 2 * e + 1 >= np_) vb[e] = (vb[e] & 0xFFFFu) | 0x7FFF0000u;
+                        }
+                    }
+                    if (!(PROF && (xp & 1))) {
+                        const int ma = min64_s16(va);
+                        const int mb = NLD == 2 ? min64_s16(vb) : 0x7FFF;
+                        if (PROF && (xp & 16)) {
+                            if (ma == -12345 || mb == -12345) tk.k[0] = 0u;
+                        } else {
+                            if (ma < lastq) slow8(va, pa, ma);
+                            if (NLD == 2 && mb < lastq) slow8(vb, pa + 64, mb);
+                        }
+                    }
+                }
 #pragma unroll 1
-                for (int k = 0; k < NCH; k += 2) {
+                for (int k = 0; k < (I8 ? 0 : NCH); k += 2) {
                     if (PROF && (xp & 2)) {
 #pragma unroll
                         for (int e = 0; e < 32; e++) { va[e] = __float_as_uint(1.0f); vb[e] = va[e]; }
@@ -891,10 +1157,11 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
                     if (PROF && (xp & 1)) continue;
                     if (tail) {   // zero pattern columns past |P| in the last tile
                         const int pa = pbase + (ch0 + k) * 32;
+                        const uint32_t big = __float_as_uint(CUDART_INF_F);
 #pragma unroll
                         for (int e = 0; e < 32; e++) {
-                            if (pa + e >= np_) va[e] = __float_as_uint(CUDART_INF_F);
-                            if (pa + 32 + e >= np_) vb[e] = __float_as_uint(CUDART_INF_F);
+                            if (pa + e >= np_) va[e] = big;
+                            if (pa + 32 + e >= np_) vb[e] = big;
                         }
                     }
                     const float ma = min32(va), mb = min32(vb);
@@ -904,70 +1171,166 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
                 }
                 tc_fence_before();
                 __syncwarp();
-                if (tr_on) trace[(size_t)gtile * TRACE_W + 8 + warp] = clock64();
+                if (tr_on) trace[(size_t)gs * TRACE_W + 8 + warp] = clock64();
                 if (lane == 0) mbar_arrive(smem_u32(&tempty[buf]));
+              }
                 if (!primary && use_pool && j >= j_claim && j < j_claim + 3) pool_step(j - j_claim);
             }
             if (dbg_on) { t_mark = clock64(); t_scan += t_mark - t_scan0; }
             if (dbg_seg) t_seg = clock64();
-            // ---- end of a full scan of P: merge the two column halves, then
-            // decide, move, refill.  The secondary half hands its top-K over
-            // through TMEM: columns [128, 144) of the last tile's accumulator,
-            // which only this secondary warp reads (the next round's MMAs
-            // start after the round end).
-            const uint32_t xaddr = t_lane + ((gtile - 1) & 1) * NT_COLS + NT_COLS / 2;
+            // ---- end of a full scan of P: merge the column groups, then
+            // decide, move, refill.  Each secondary warp hands its top-K over
+            // through TMEM: the first 16 of its own columns of the last tile's
+            // accumulator, which only it reads (the next round's MMAs start
+            // after the round end).
+            const uint32_t lastacc = t_lane + ((gtile * SUBS - 1) % NBUF) * TW;
+            const uint32_t xaddr = lastacc + grp * WC;
             if (!primary) {
+                // f16: 8 values then 8 indices; int8: 16 keys
                 uint32_t xs[16];
 #pragma unroll
                 for (int k = 0; k < 8; k++) {
-                    xs[k] = k < TOPK ? __float_as_uint(top.b[k]) : 0u;
-                    xs[8 + k] = k < TOPK ? (uint32_t)top.i[k] : 0u;
+                    if constexpr (I8) {
+                        xs[k] = tk.k[k];
+                        xs[8 + k] = tk.k[8 + k];
+                    } else {
+                        xs[k] = k < KT ? __float_as_uint(top.b[k]) : 0u;
+                        xs[8 + k] = k < KT ? (uint32_t)top.i[k] : 0u;
+                    }
                 }
                 TC_ST16(xaddr, xs);
                 asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
                 tc_fence_before();
             }
             SEG(0);
-            epi_bar_sync();
+            epi_bar_sync<EPI_T>();
             SEG(1);
             if (primary) {
-                tc_fence_after();
+              tc_fence_after();
+#pragma unroll 1
+              for (int gs2 = 1; gs2 < EW / 4; gs2++) {
                 uint32_t xs[16];
-                TC_LD16(xaddr, xs);
+                TC_LD16(lastacc + gs2 * WC, xs);
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if constexpr (I8) {
 #pragma unroll
-                for (int k = 0; k < TOPK; k++) {
+                    for (int k = 0; k < KT; k++) {
+                        const uint32_t key = xs[k];
+                        if (key < tk.k[KT - 1] && key_val(key) < wbase() + wq) {
+                            tk.insert_inline(key);
+                            upd_lastq();
+                        }
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < (I8 ? 0 : KT); k++) {
                     const float s = __uint_as_float(xs[k]);
                     if (s < lastv) {
                         top.insert_inline(s, (int)xs[8 + k]);
                         lastv = fminf(top.last(), top.b[0] + wadd);
                     }
                 }
+              }
             }
             if (YSTAGE && primary) mbar_wait(smem_u32(&ybar[0]), rnd & 1);
             bool refill = false;
+            bool cont_more = false;          // int8: window overflow, the row re-scans P
             if (active) {
-                iters++;
                 int i1;
                 bool improve;
                 float sb;
                 uint32_t pwv[NW];
-                bool have_bits;
-                if (YSTAGE)
-                    certify_window<TOPK, NW, true>(top, ysm, c, prm.pbits, ed, prm.tie_rel, err_row, i1, improve, sb,
-                                                   flags, pwv, have_bits);
-                else
-                    certify_window<TOPK, NW, false>(top, prm.y + (size_t)frame * n, c, prm.pbits, ed, prm.tie_rel,
-                                                    err_row, i1, improve, sb, flags, pwv, have_bits);
+                bool have_bits = false;
+                float sx;
+                const float* yrow = YSTAGE ? ysm : prm.y + (size_t)frame * n;
+                bool done_cont = false;
+                if constexpr (I8) {
+                    const float thr = prm.tie_rel * ed * 0.25f;
+                    const float win = thr + 2.0f * err_row;
+                    const int base = kfloor ? cbase : key_val(tk.k[0]);
+                    // (profiling knob 2048, for tests: overflow at 4 keys, forcing continuation passes)
+                    const int kov = (PROF && (xp & 2048)) ? 4 : KT;
+                    const uint32_t klast = (PROF && (xp & 2048)) ? tk.k[3] : tk.k[KT - 1];
+                    const bool overflow = klast != 0xFFFFFFFFu && (float)(key_val(klast) - base) * sc < win;
+                    if (kfloor || overflow) {
+                        // exact float64 scores of this pass's window candidates, merged
+                        // with the earlier passes' (ties -> lowest pattern index)
+#pragma unroll 1
+                        for (int k = 0; k < kov; k++) {
+                            const uint32_t key = tk.k[k];
+                            if (key == 0xFFFFFFFFu || !((float)(key_val(key) - base) * sc < win)) break;
+                            const int pi = (int)(key & ((1u << KEY_IBITS) - 1u));
+                            const double e = exact_score<NW>(yrow, c, prm.pbits + (size_t)pi * NW, NW, n);
+                            if (e < xb_s || (e == xb_s && pi < xb_i)) { xs2 = xb_s; xb_s = e; xb_i = pi; }
+                            else if (e < xs2) xs2 = e;
+                        }
+                        if (overflow) {
+                            kfloor = klast;
+                            cbase = base;
+                            cont_more = true;
+                        } else {
+                            i1 = xb_i;
+                            improve = xb_s < 0.0;
+                            sb = (float)xb_s;
+                            if (xs2 - xb_s < (double)thr) flags |= MPW_F_TIE_ARGMIN;
+                            if (fabs(xb_s) < (double)thr) flags |= MPW_F_TIE_ACCEPT;
+                            kfloor = 0u;
+                            xb_s = xs2 = CUDART_INF;
+                        }
+                        done_cont = true;
+                    }
+                }
+                if (!done_cont) {
+                    TopK<KT> cand;
+                    if constexpr (I8) {   // keys -> (S-unit score, index)
+#pragma unroll
+                        for (int k = 0; k < KT; k++) {
+                            cand.b[k] = tk.k[k] == 0xFFFFFFFFu ? CUDART_INF_F : (float)key_val(tk.k[k]) * sc;
+                            cand.i[k] = (int)(tk.k[k] & ((1u << KEY_IBITS) - 1u));
+                        }
+                    } else {
+                        cand = top;
+                    }
+                    if (YSTAGE)
+                        certify_window<KT, NW, true, I8>(cand, ysm, c, prm.pbits, ed, prm.tie_rel, err_row, i1,
+                                                         improve, sb, flags, pwv, have_bits, sx);
+                    else
+                        certify_window<KT, NW, false, I8>(cand, yrow, c, prm.pbits, ed, prm.tie_rel, err_row, i1,
+                                                          improve, sb, flags, pwv, have_bits, sx);
+                    if (I8) sb = sx;
+                }
+                if (!cont_more) iters++;
                 SEG(2);
-                if (improve) {
+                if (!cont_more && improve) {
                     // flip the fp16 sign bits of the moved positions 8 at a time
                     // (one 16-byte RMW per swizzle chunk, no per-bit loop)
                     if (!have_bits) {
 #pragma unroll
                         for (int w = 0; w < NW; w++) pwv[w] = __ldg(prm.pbits + (size_t)i1 * NW + w);
                     }
-                    {
+                    if (I8) {
+                        // negate the int8 values of the moved positions (16 per chunk)
+#pragma unroll
+                        for (int w = 0; w < NW; w++) {
+                            const uint32_t bits = pwv[w];
+                            c[w] ^= bits;
+#pragma unroll
+                            for (int h = 0; h < 2; h++) {
+                                const uint32_t b16 = (bits >> (16 * h)) & 0xFFFFu;
+                                if (!b16) continue;
+                                const int ch = w * 2 + h;
+                                uint4* pq = reinterpret_cast<uint4*>(a_hi + (ch >> 3) * A_KBLK_BYTES +
+                                                                     sw128_chunk(row, ch & 7));
+                                uint4 v = *pq;
+                                uint32_t m;
+                                m = byte_mask4(b16 & 0xFu);         v.x = (v.x & ~m) | (__vsub4(0u, v.x) & m);
+                                m = byte_mask4((b16 >> 4) & 0xFu);  v.y = (v.y & ~m) | (__vsub4(0u, v.y) & m);
+                                m = byte_mask4((b16 >> 8) & 0xFu);  v.z = (v.z & ~m) | (__vsub4(0u, v.z) & m);
+                                m = byte_mask4((b16 >> 12) & 0xFu); v.w = (v.w & ~m) | (__vsub4(0u, v.w) & m);
+                                *pq = v;
+                            }
+                        }
+                    } else {
 #pragma unroll
                         for (int w = 0; w < NW; w++) {
                             const uint32_t bits = pwv[w];
@@ -1000,7 +1363,7 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
                     if (prm.s2.traj_hops) prm.s2.traj_hops[(size_t)tr * T + iters - 1] = i1 + 1;
                 }
                 SEG(3);
-                if ((!improve && !(xp & 4)) || iters == T) {
+                if (!cont_more && ((!improve && !(xp & 4)) || iters == T)) {
                     if (prm.s2.traj_hops)
                         for (int h = iters - (improve ? 0 : 1); h < T; h++) prm.s2.traj_hops[(size_t)tr * T + h] = -1;
                     store_row();
@@ -1023,9 +1386,12 @@ __global__ void __launch_bounds__(THREADS, 1) hop_tc_kernel(Params prm) {
             }
             rnd++;
             SEG(4);
-            if (primary) row_wadd[row] = 2.0f * err_row + prm.tie_rel * ed * 0.25f;
+            if (primary) {
+                row_wadd[row] = row_window();
+                if (I8) row_cont[row] = make_uint2(kfloor, (uint32_t)cbase);
+            }
             fence_proxy_async();
-            any = epi_bar_or(active);
+            any = epi_bar_or<EPI_T>(active);
             SEG(5);
             if (!primary && use_pool) {
                 // publish this round's pool fill; consumed indices never exceed the old tail

@@ -94,6 +94,7 @@ struct mpw_handle {
     DevBuf<uint32_t> s2_anchors, traj_cw;
     DevBuf<uint8_t> traj_flags;
     DevBuf<float4> ebound;
+    DevBuf<float4> qscale;
     DevBuf<uint8_t> s1_flags;       // OSD stage-1 near-tie flags
     int wmax = 0;
     int scl_generic = 0;            // force the warp-per-frame SCL kernel
@@ -267,10 +268,12 @@ __global__ void queue_identity_kernel(int F, int A, int n, const float* __restri
     if (q == 0 && lane == 0) *s2.count = F;
     if (q < F) {
         const float4 eb = warp_error_bounds(y + (size_t)q * n, n, s2.wmax);
+        const float4 qs = warp_i8_scale(y + (size_t)q * n, n, s2.wmax);
         if (lane == 0) {
             s2.frame[q] = q;
             s2.nanchor[q] = nanchor ? min(nanchor[q], A) : A;
             s2.ebound[q] = eb;
+            s2.qscale[q] = qs;
         }
     }
 }
@@ -281,8 +284,10 @@ __global__ void ebound_kernel(int n, const float* __restrict__ y, S2Dev s2) {
     const int warps = gridDim.x * (blockDim.x >> 5);
     const int count = *s2.count;
     for (int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); q < count; q += warps) {
-        const float4 eb = warp_error_bounds(y + (size_t)s2.frame[q] * n, n, s2.wmax);
-        if (lane == 0) s2.ebound[q] = eb;
+        const float* yr = y + (size_t)s2.frame[q] * n;
+        const float4 eb = warp_error_bounds(yr, n, s2.wmax);
+        const float4 qs = warp_i8_scale(yr, n, s2.wmax);
+        if (lane == 0) { s2.ebound[q] = eb; s2.qscale[q] = qs; }
     }
 }
 
@@ -298,6 +303,7 @@ int ensure_s2(mpw_handle* h, int F, int A, int T) {
     CK(h->traj_hops.ensure(traj * T));
     CK(h->traj_flags.ensure(traj));
     CK(h->ebound.ensure(F));
+    CK(h->qscale.ensure(F));
     return 0;
 }
 
@@ -307,7 +313,7 @@ S2Dev s2_dev(mpw_handle* h, const uint32_t* anchors_override) {
     s.anchors = anchors_override ? const_cast<uint32_t*>(anchors_override) : h->s2_anchors.p;
     s.traj_cw = h->traj_cw.p; s.traj_iters = h->traj_iters.p; s.traj_hops = h->traj_hops.p;
     s.traj_flags = h->traj_flags.p; s.work_next = h->work_next.p;
-    s.ebound = h->ebound.p; s.wmax = h->wmax;
+    s.ebound = h->ebound.p; s.qscale = h->qscale.p; s.wmax = h->wmax;
     return s;
 }
 
@@ -389,9 +395,11 @@ int launch_gather(mpw_handle* h, HopParams hp, int max_traj, cudaStream_t st) {
 
 int run_hops(mpw_handle* h, const float* y, int Fmax, int A, int T, int variant, S2Dev s2, cudaStream_t st) {
     if (variant == MPW_HOP_AUTO) variant = tc_supported(h->n, h->np) && h->tcp.ready ? MPW_HOP_TENSOR : MPW_HOP_GATHER;
-    if (variant == MPW_HOP_TENSOR || variant == MPW_HOP_TENSOR_2LIMB) {
+    if (variant == MPW_HOP_TENSOR || variant == MPW_HOP_TENSOR_2LIMB || variant == MPW_HOP_TENSOR_I8) {
         if (!h->tcp.ready) return fail(MPW_ERR_UNSUPPORTED, "tensor-core hop operand not built for this pattern set");
-        const int limbs = variant == MPW_HOP_TENSOR ? 1 : 2;
+        if (variant == MPW_HOP_TENSOR_I8 && !h->tcp.ready8)
+            return fail(MPW_ERR_UNSUPPORTED, "int8 tensor-core hop needs N = 128 or 256");
+        const int limbs = variant == MPW_HOP_TENSOR ? 1 : variant == MPW_HOP_TENSOR_2LIMB ? 2 : 0;
         int rc = tc_launch(h->tcp, h->n, h->nw, A, T, y, s2, pat_dev(h), h->num_sms, limbs, st);
         if (rc) return fail(MPW_ERR_CUDA, "tensor-core hop launch failed: %s",
                             rc < 0 ? cudaGetErrorString((cudaError_t)-rc) : "unsupported shape");
@@ -459,7 +467,7 @@ void mpw_destroy(mpw_handle* h) {
     h->crc_h.release(); h->mix.release(); h->pbits.release(); h->poff.release(); h->soff.release();
     h->pidx.release(); h->sup.release(); h->s2_count.release(); h->s2_frame.release();
     h->s2_nanchor.release(); h->traj_iters.release(); h->traj_hops.release(); h->work_next.release();
-    h->s2_anchors.release(); h->traj_cw.release(); h->traj_flags.release(); h->ebound.release(); h->s1_flags.release();
+    h->s2_anchors.release(); h->traj_cw.release(); h->traj_flags.release(); h->ebound.release(); h->qscale.release(); h->s1_flags.release();
     tc_release(h->tcp);
     if (h->ev_init) for (int i = 0; i < 8; i++) cudaEventDestroy(h->ev[i]);
     delete h;

@@ -46,11 +46,20 @@ def test_scl_lists_bit_exact_vs_reference(fx):
         np.testing.assert_array_equal(pm[f, :c], g["list_pm"][f, :c])
 
 
-@pytest.mark.parametrize("variant", ["gather", "tensor", "tensor2"])
+VARIANTS = ["gather", "tensor", "tensor2", "tensor_i8"]
+
+
+def _skip_i8(variant, n):
+    if variant == "tensor_i8" and n not in (128, 256):
+        pytest.skip("int8 screen: N = 128, 256")
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
 @pytest.mark.parametrize("fx", two_stage_fixtures())
 def test_two_stage_vs_reference_golden(fx, variant):
     g = load(fx)
     cfg = cfg_of(fx)
+    _skip_i8(variant, g["y32"].shape[1])
     dec = decoder(cfg)
     mode = "crc_gated" if int(g["gated"]) else "always_on"
     o = dec.two_stage_batch(g["y32"], float(g["sigma"]), int(g["list_size"]), int(g["num_paths"]),
@@ -76,14 +85,17 @@ def test_two_stage_vs_reference_golden(fx, variant):
     np.testing.assert_array_equal(msg[ok], ref_msg[ok])
 
 
-@pytest.mark.parametrize("variant", ["gather", "tensor", "tensor2"])
+@pytest.mark.parametrize("variant", VARIANTS)
 @pytest.mark.parametrize("name", ["cfg1", "cfg3", "cfg2", "cfg4"])
 def test_two_stage_vs_oracle_random_frames(name, variant):
     cfg = configs.CONFIGS[name]
     code, sph = code_and_sphere(cfg)
+    _skip_i8(variant, code.n)
     from paper_2602_08501_b200 import channel
     sigma = cfg.sigma(code=code)
     F = {"cfg1": 4096, "cfg3": 2048, "cfg2": 256, "cfg4": 96}[name]
+    if variant == "tensor_i8" and name in ("cfg2", "cfg4"):
+        F *= 4      # the int8 screen's wider window: more frames
     if name == "cfg4" and variant == "gather":
         F = 32
     _, cw, y = channel.bulk_inputs(code, 11, 0, 0, F, sigma)
@@ -102,12 +114,13 @@ def test_two_stage_vs_oracle_random_frames(name, variant):
     np.testing.assert_array_equal(_np(o["iters"])[ok], r["iters"][ok])
 
 
-@pytest.mark.parametrize("variant", ["gather", "tensor", "tensor2"])
-def test_mp_wsd_random_anchors_vs_oracle(variant):
-    cfg = configs.CONFIGS["cfg1"]
+@pytest.mark.parametrize("variant,name", [(v, "cfg1") for v in VARIANTS[:3]] +
+                         [("tensor_i8", "cfg3"), ("tensor_i8", "cfg2"), ("tensor", "cfg2")])
+def test_mp_wsd_random_anchors_vs_oracle(variant, name):
+    cfg = configs.CONFIGS[name]
     code, sph = code_and_sphere(cfg)
     rng = np.random.default_rng(5)
-    F, A, T = 1000, 4, 4
+    F, A, T = (1000, 4, 4) if name != "cfg2" else (200, 8, 6)
     from paper_2602_08501_b200.codes import encode_batch
     msgs = rng.integers(0, 2, (F * A, code.k), dtype=np.uint8)
     anc64 = encode_batch(code, msgs).reshape(F, A, -1)
@@ -146,3 +159,29 @@ def test_scl_kernels_agree_bit_exact(name, generic):
         got = words32_to_64(o["list_cw"][f, :c].cpu().numpy().view(np.uint32), code.n)
         np.testing.assert_array_equal(got, cw)
         np.testing.assert_array_equal(o["list_pm"][f, :c].cpu().numpy(), pm)
+
+
+@pytest.mark.parametrize("name", ["cfg4", "cfg2"])
+def test_int8_window_overflow_continuation(name, monkeypatch):
+    """int8 screen: with the overflow threshold forced down to 4 keys (profiling
+    knob 2048), most scans take continuation passes; decisions must still equal
+    the oracle's, with no frame left unresolved."""
+    cfg = configs.CONFIGS[name]
+    code, sph = code_and_sphere(cfg)
+    from paper_2602_08501_b200 import channel
+    sigma = cfg.sigma(code=code)
+    F = 128 if name == "cfg4" else 256
+    _, cw, y = channel.bulk_inputs(code, 12, 0, 0, F, sigma)
+    monkeypatch.setenv("MPW_TC_EXPERIMENT", "2048")
+    o = decoder(cfg).two_stage_batch(y, sigma, cfg.list_size, cfg.num_paths, cfg.max_iterations,
+                                     cfg.activation_mode, variant="tensor_i8")
+    r = orc.two_stage_batch(y, code, sph, cfg.list_size, cfg.num_paths, cfg.max_iterations,
+                            cfg.activation_mode == "crc_gated", sigma, nthreads=8)
+    best = words32_to_64(_np(o["best"]).view(np.uint32), code.n)
+    flags = _np(o["flags"])
+    assert not (flags & UNRESOLVED).any()
+    mism = np.flatnonzero((best != r["best"]).any(axis=1))
+    risky = np.flatnonzero(flags & TIE_FINAL)
+    assert set(mism.tolist()) <= set(risky.tolist()), f"mismatches {mism}"
+    ok = np.setdiff1d(np.arange(F), risky)
+    np.testing.assert_array_equal(_np(o["iters"])[ok], r["iters"][ok])

@@ -69,7 +69,9 @@ constexpr int POOL_BYTES = POOL * (int)sizeof(PoolEnt);
 
 __host__ __device__ constexpr int a_buffers(int limbs) { return limbs == 2 ? 2 : 1; }
 __host__ __device__ constexpr int fixed_bytes(int kb, int limbs) {
-    return 1024 /*align slack*/ + a_buffers(limbs) * kb * A_KBLK_BYTES + POOL_BYTES + ROWS * 4 /*row windows*/ +
+    // align slack: the int8 layout relies on the __align__(1024) of the dynamic
+    // shared memory (checked in the kernel) to fit six 32 KB stages
+    return (limbs == 0 ? 0 : 1024) + a_buffers(limbs) * kb * A_KBLK_BYTES + POOL_BYTES + ROWS * 4 /*row windows*/ +
            (limbs == 0 ? ROWS * 8 : 0) /*int8 continuation state*/ + 256;
 }
 
@@ -285,9 +287,10 @@ __device__ __forceinline__ uint32_t min3_s16x2(uint32_t a, uint32_t b, uint32_t 
     asm("min.s16x2 %0, %1, %2;" : "=r"(r) : "r"(r), "r"(c));   // fused into VIMNMX3.S16x2
     return r;
 }
-// minimum of 64 packed s16 values (32 registers): 16 three-input instructions, depth 4
-__device__ __forceinline__ int min64_s16(const uint32_t (&v)[32]) {
-    uint32_t m[11];
+// minimum of 64 packed s16 values (32 registers): 16 three-input instructions,
+// depth 4; m[g] keeps the packed minimum of register group g (registers
+// 3g..3g+2, group 10 = registers 30, 31) for the insertion path's group test
+__device__ __forceinline__ int min64_s16(const uint32_t (&v)[32], uint32_t (&m)[11]) {
 #pragma unroll
     for (int e = 0; e < 10; e++) m[e] = min3_s16x2(v[3 * e], v[3 * e + 1], v[3 * e + 2]);
     uint32_t r;
@@ -581,6 +584,7 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
     long long* const trace = MODE >= 1 ? prm.trace : nullptr;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* sm = reinterpret_cast<unsigned char*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    if (I8 && sm != smem_raw) __trap();   // no slack in the int8 layout
     unsigned char* a_hi = sm;
     unsigned char* a_lo = sm + KB * A_KBLK_BYTES;          // used only when LIMBS == 2
     unsigned char* b_ring = sm + a_buffers(LIMBS) * KB * A_KBLK_BYTES;
@@ -1081,30 +1085,46 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
                 };
                 // int8 slow path over 64 packed scores (column p0 + 2e + half):
                 // keys carry the index, so the insertion order does not matter
-                auto slow8 = [&](const uint32_t (&v)[32], int p0, int mn) {
+                // register groups whose packed minimum is below the limit are
+                // searched value by value: group test, switch to the group's three
+                // registers, one insertion site (no runtime register indexing)
+                auto slow8 = [&](const uint32_t (&v)[32], const uint32_t (&gm)[11], int p0, int mn) {
                     const int lim = min(lastq, mn + wq);
-                    uint32_t hlo = 0, hhi = 0;
+                    const uint32_t l16 = (uint32_t)min(lim, 32767) & 0xFFFFu;
+                    const uint32_t lim2 = l16 | (l16 << 16);
+                    uint32_t gmask = 0;
 #pragma unroll
-                    for (int e = 0; e < 32; e++) {
-                        hlo |= ((int)(short)(v[e] & 0xFFFFu) < lim ? 1u : 0u) << e;
-                        hhi |= ((int)(short)(v[e] >> 16) < lim ? 1u : 0u) << e;
-                    }
-                    auto take = [&](int sv, int p) {
-                        const uint32_t key = make_key(sv, p);
-                        if (key < tk.k[KT - 1] && key > kfl && sv < wbase() + wq) {
-                            tk.insert_inline(key);
-                            upd_lastq();
+                    for (int g = 0; g < 11; g++) gmask |= (__vcmplts2(gm[g], lim2) != 0u ? 1u : 0u) << g;
+                    while (gmask) {
+                        const int g = __ffs(gmask) - 1;
+                        gmask &= gmask - 1;
+                        uint32_t r0, r1, r2;
+                        switch (g) {
+#define MPW_GRP(G) case G: r0 = v[3 * G]; r1 = v[3 * G + 1]; r2 = v[3 * G + 2]; break;
+                            MPW_GRP(0) MPW_GRP(1) MPW_GRP(2) MPW_GRP(3) MPW_GRP(4)
+                            MPW_GRP(5) MPW_GRP(6) MPW_GRP(7) MPW_GRP(8) MPW_GRP(9)
+#undef MPW_GRP
+                            default: r0 = v[30]; r1 = v[31]; r2 = 0x7FFF7FFFu; break;
                         }
-                    };
-                    while (hlo) {
-                        const int e = __ffs(hlo) - 1;
-                        hlo &= hlo - 1;
-                        take((int)(short)(select32(v, e) & 0xFFFFu), p0 + 2 * e);
-                    }
-                    while (hhi) {
-                        const int e = __ffs(hhi) - 1;
-                        hhi &= hhi - 1;
-                        take((int)(short)(select32(v, e) >> 16), p0 + 2 * e + 1);
+                        uint32_t hm = 0;
+                        hm |= ((int)(short)(r0 & 0xFFFFu) < lim ? 1u : 0u);
+                        hm |= ((int)(short)(r0 >> 16) < lim ? 2u : 0u);
+                        hm |= ((int)(short)(r1 & 0xFFFFu) < lim ? 4u : 0u);
+                        hm |= ((int)(short)(r1 >> 16) < lim ? 8u : 0u);
+                        hm |= ((int)(short)(r2 & 0xFFFFu) < lim ? 16u : 0u);
+                        hm |= ((int)(short)(r2 >> 16) < lim ? 32u : 0u);
+                        while (hm) {
+                            const int h = __ffs(hm) - 1;
+                            hm &= hm - 1;
+                            const uint32_t r = (h >> 1) == 0 ? r0 : ((h >> 1) == 1 ? r1 : r2);
+                            const int sv = (h & 1) ? (int)(short)(r >> 16) : (int)(short)(r & 0xFFFFu);
+                            const int p = p0 + 2 * (3 * g + (h >> 1)) + (h & 1);
+                            const uint32_t key = make_key(sv, p);
+                            if (key < tk.k[KT - 1] && key > kfl && sv < wbase() + wq) {
+                                tk.insert_inline(key);
+                                upd_lastq();
+                            }
+                        }
                     }
                 };
                 // two 32-column chunks per step: both TMEM loads in flight together,
@@ -1134,13 +1154,14 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
                         }
                     }
                     if (!(PROF && (xp & 1))) {
-                        const int ma = min64_s16(va);
-                        const int mb = NLD == 2 ? min64_s16(vb) : 0x7FFF;
+                        uint32_t ga[11], gb[11];
+                        const int ma = min64_s16(va, ga);
+                        const int mb = NLD == 2 ? min64_s16(vb, gb) : 0x7FFF;
                         if (PROF && (xp & 16)) {
                             if (ma == -12345 || mb == -12345) tk.k[0] = 0u;
                         } else {
-                            if (ma < lastq) slow8(va, pa, ma);
-                            if (NLD == 2 && mb < lastq) slow8(vb, pa + 64, mb);
+                            if (ma < lastq) slow8(va, ga, pa, ma);
+                            if (NLD == 2 && mb < lastq) slow8(vb, gb, pa + 64, mb);
                         }
                     }
                 }

@@ -579,7 +579,7 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
     constexpr int EPI_T = 32 * EW;
     constexpr int WC = TW * 4 / EW;                  // accumulator columns per epilogue warp
     // round-end staging of every row's received word in the (then idle) B ring
-    constexpr bool YSTAGE = ROWS * NW * 32 * 4 <= STAGES * B_STAGE_BYTES;
+    constexpr bool YSTAGE = ROWS * (NW * 32 * 4 + 16) <= STAGES * B_STAGE_BYTES;
     const int xp = PROF ? prm.experiment : 0;
     long long* const trace = MODE >= 1 ? prm.trace : nullptr;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -1000,9 +1000,12 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
         p_fill = use_pool ? POOL : 0;
         uint32_t gtile = 0, rnd = 0;
         constexpr uint32_t YB = NW * 32 * 4;                      // bytes of one received word
-        float* const ysm = reinterpret_cast<float*>(b_ring + (size_t)row * YB);
+        // staging pitch: +16 bytes per word, so the 32 rows of a warp reading the
+        // same position hit 8 different 16-byte bank groups (no 8-way conflicts)
+        constexpr uint32_t YP = YB + 16;
+        float* const ysm = reinterpret_cast<float*>(b_ring + (size_t)row * YP);
         // pool entries whose y is staged beside the rows' at the round end
-        constexpr int XS_FIT = YSTAGE ? (int)((STAGES * B_STAGE_BYTES - ROWS * YB) / YB) : 0;
+        constexpr int XS_FIT = YSTAGE ? (int)((STAGES * B_STAGE_BYTES - ROWS * YP) / YP) : 0;
         constexpr int XS = XS_FIT < POOL ? XS_FIT : POOL;
         int xs_base = 0;
         const bool dbg_on = (xp & 8) && blockIdx.x == 0 && primary && row == 0;
@@ -1057,7 +1060,7 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
                     mbar_expect_tx(smem_u32(&ybar[0]), (active ? YB : 0u) + (xs_on ? YB : 0u));
                     if (active) bulk_g2s(smem_u32(ysm), prm.y + (size_t)frame * n, YB, smem_u32(&ybar[0]));
                     if (xs_on)
-                        bulk_g2s(smem_u32(b_ring + (size_t)(ROWS + row) * YB), prm.y + (size_t)xf * n, YB,
+                        bulk_g2s(smem_u32(b_ring + (size_t)(ROWS + row) * YP), prm.y + (size_t)xf * n, YB,
                                  smem_u32(&ybar[0]));
                 }
                 const int pbase = j * NT_COLS + h * TW;
@@ -1398,7 +1401,7 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
                     if (refill) {
                         const int xs = pidx - xs_base;
                         const float* ysrc = (pidx >= 0 && xs >= 0 && xs < XS)
-                                                ? reinterpret_cast<const float*>(b_ring + (size_t)(ROWS + xs) * YB)
+                                                ? reinterpret_cast<const float*>(b_ring + (size_t)(ROWS + xs) * YP)
                                                 : prm.y + (size_t)frame * n;
                         build_row(ysrc);
                     }

@@ -1135,6 +1135,14 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
                 constexpr int NCH = WC / 32;
                 const uint32_t tbase = t_lane + buf * TW + ch0 * 32;
                 uint32_t va[32], vb[32];
+                // the accumulator is handed back to the MMA issuer as soon as the
+                // warp's last TMEM loads complete; the scan of the registers then
+                // overlaps the next MMAs
+                auto release = [&]() {
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(smem_u32(&tempty[buf]));
+                };
                 if constexpr (I8) {
                     // the warp's TW/2 columns as packed s16 scores (64 per load), one wait
                     constexpr int NLD = WC / 64;
@@ -1146,6 +1154,7 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
                         if constexpr (NLD == 2) TC_LD32P(tbase + 64, vb);
                         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                     }
+                    release();   // every column of this warp is in registers
                     const int pa = pbase + ch0 * 32;
                     if (tail) {
 #pragma unroll
@@ -1178,6 +1187,7 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
                         TC_LD32(tbase + (k + 1) * 32, vb);
                         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                     }
+                    if (k + 2 >= NCH) release();   // the tile's last loads are done
                     if (PROF && (xp & 1)) continue;
                     if (tail) {   // zero pattern columns past |P| in the last tile
                         const int pa = pbase + (ch0 + k) * 32;
@@ -1193,10 +1203,7 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
                     if (ma < lastv) slow(va, pbase + (ch0 + k) * 32, ma);
                     if (mb < lastv) slow(vb, pbase + (ch0 + k + 1) * 32, mb);
                 }
-                tc_fence_before();
-                __syncwarp();
                 if (tr_on) trace[(size_t)gs * TRACE_W + 8 + warp] = clock64();
-                if (lane == 0) mbar_arrive(smem_u32(&tempty[buf]));
               }
                 if (!primary && use_pool && j >= j_claim && j < j_claim + 3) pool_step(j - j_claim);
             }

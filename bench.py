@@ -169,11 +169,17 @@ def run_reference(args, cfg, code, sph, sigma):
 
 
 def _config(args, cfg, code, sph):
-    return {"workload": f"{cfg.name}: CA-polar({code.n},{code.inner.k}) K={code.k}+CRC11, SCL L={cfg.list_size}, "
+    if getattr(code, "inner", None) is not None:
+        cname = f"CA-polar({code.n},{code.inner.k}) K={code.k}+CRC{code.inner.k - code.k}"
+    else:
+        cname = f"polar({code.n},{code.k}) (no CRC)"
+    mode = "stage 2 forced" if cfg.activation_mode == "always_on" else "CRC-gated stage 2"
+    return {"workload": f"{cfg.name}: {cname}, SCL L={cfg.list_size}, "
                         f"A={cfg.num_paths}, T={cfg.max_iterations}, |P|={sph.nonzero_size} "
-                        f"(w<=56, wbar={sph.mean_nonzero_weight:.2f}), Eb/N0={cfg.ebno_db[0]} dB, stage 2 forced",
+                        f"(w<={int(sph.member_weights.max())}, wbar={sph.mean_nonzero_weight:.2f}), "
+                        f"Eb/N0={cfg.ebno_db[0]} dB, {mode}",
             "frames_per_step_per_gpu": args.frames, "hop_variant": args.variant,
-            "l2": "inputs larger than L2 (frames x 256 x 4 B per step, two alternating batches)",
+            "l2": f"inputs larger than L2 (frames x {code.n} x 4 B per step, two alternating batches)",
             "parallelism": f"frame-range shards x{_dist_env()[0]}"}
 
 
@@ -316,7 +322,7 @@ def main():
         hop_ms = float(kms[1])
         variant_used = args.variant
         if variant_used == "auto":
-            variant_used = "tensor" if dec.tensor_path_ready else "gather"
+            variant_used = dec.auto_variant
         if variant_used == "tensor_i8":
             ops = evals / ws * 2.0 * code.n                # 2N int8 tensor ops per evaluation
             ach = ops / (hop_ms / 1000.0) / 1e12

@@ -174,6 +174,8 @@ int mpw_channel_batch(mpw_handle* h, uint64_t seed, int snr_idx, long long first
 
 int mpw_num_patterns(mpw_handle* h);
 int mpw_tensor_path_ready(mpw_handle* h);
+/* The hop variant MPW_HOP_AUTO resolves to for the current code and pattern set. */
+int mpw_hop_auto_variant(mpw_handle* h);
 
 /* Host-side pattern-set generation (off the timed path). */
 int64_t mpw_enumerate_lowweight(const uint64_t* gen, int k, int n, int cap, int64_t* spectrum,

@@ -45,6 +45,7 @@ _SIGS = {
     "mpw_channel_batch": (c_int, [c_void_p, c_uint64, c_int, ctypes.c_longlong, c_int, c_double,
                                   c_void_p, c_void_p, c_void_p, c_void_p]),
     "mpw_tensor_path_ready": (c_int, [c_void_p]),
+    "mpw_hop_auto_variant": (c_int, [c_void_p]),
     "mpw_enumerate_lowweight": (c_int64, [c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_int64, c_int]),
     "mpw_two_stage_osd_batch": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int, c_int, c_int,
                                         c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,

@@ -393,8 +393,19 @@ int launch_gather(mpw_handle* h, HopParams hp, int max_traj, cudaStream_t st) {
     return 0;
 }
 
+// MPW_HOP_AUTO: the int8 screen where a round streams enough of P to amortise
+// its wider certification window (N = 256 and >= 32 tiles of 256 patterns:
+// cfg4 0.71x the f16 hop time; slower on cfg2/cfg3), else one fp16 limb, else
+// the gather kernel
+int resolve_variant(mpw_handle* h, int variant) {
+    if (variant != MPW_HOP_AUTO) return variant;
+    if (!(tc_supported(h->n, h->np) && h->tcp.ready)) return MPW_HOP_GATHER;
+    if (h->tcp.ready8 && h->n >= 256 && h->tcp.ntiles >= 32) return MPW_HOP_TENSOR_I8;
+    return MPW_HOP_TENSOR;
+}
+
 int run_hops(mpw_handle* h, const float* y, int Fmax, int A, int T, int variant, S2Dev s2, cudaStream_t st) {
-    if (variant == MPW_HOP_AUTO) variant = tc_supported(h->n, h->np) && h->tcp.ready ? MPW_HOP_TENSOR : MPW_HOP_GATHER;
+    variant = resolve_variant(h, variant);
     if (variant == MPW_HOP_TENSOR || variant == MPW_HOP_TENSOR_2LIMB || variant == MPW_HOP_TENSOR_I8) {
         if (!h->tcp.ready) return fail(MPW_ERR_UNSUPPORTED, "tensor-core hop operand not built for this pattern set");
         if (variant == MPW_HOP_TENSOR_I8 && !h->tcp.ready8)
@@ -998,5 +1009,7 @@ int mpw_read_timing(mpw_handle* h, double* ms_out /*4*/, long long* launches_out
 int mpw_num_patterns(mpw_handle* h) { return h ? h->np : -1; }
 
 int mpw_tensor_path_ready(mpw_handle* h) { return (h && h->tcp.ready) ? 1 : 0; }
+
+int mpw_hop_auto_variant(mpw_handle* h) { return h ? resolve_variant(h, MPW_HOP_AUTO) : MPW_ERR_ARG; }
 
 }  // extern "C"

@@ -259,6 +259,12 @@ class DeviceDecoder:
     def tensor_path_ready(self) -> bool:
         return bool(_native.lib().mpw_tensor_path_ready(self._h))
 
+    @property
+    def auto_variant(self) -> str:
+        """The hop variant 'auto' resolves to for this code and pattern set."""
+        v = _native.lib().mpw_hop_auto_variant(self._h)
+        return {code: name for name, code in _HOP.items()}[v]
+
     def close(self):
         if getattr(self, "_h", None):
             _native.lib().mpw_destroy(self._h)

@@ -93,11 +93,6 @@ static int tc_launch_t(const TcPatterns& t, int n, int nw, int A, int T, const f
     prm.y = y; prm.s2 = s2; prm.pbits = P.bits; prm.btiles = LIMBS == 0 ? t.tiles8 : t.tiles; prm.tie_rel = 1e-5f;
     prm.err = 2e-3f;
     prm.experiment = tc_experiment();
-    {
-        const char* e = getenv("MPW_TC_PRESCAN");
-        const int want = e ? atoi(e) : 4;
-        prm.prescan = (LIMBS == 0 && t.ntiles >= 4 * want && want > 0) ? want : 0;
-    }
     static long long* trace = nullptr;
     prm.trace = nullptr;
     if (prm.experiment & 128) {

@@ -380,7 +380,6 @@ struct Params {
     float tie_rel;
     float err;             // bound on |S_fp32 - S_exact| (S units)
     long long* trace;      // experiment & 128: per-tile clock64 trace of CTA 0 (TRACE_W per tile)
-    int prescan;           // int8: tiles scanned for the running minimum only, then again at the end
     int experiment;        // profiling knob: 1 skip epilogue math, 2 skip TMEM loads, 4 force T scans,
                            // 2048 int8 window overflow at 4 keys (exercises the continuation passes),
                            // 8 cycle report from CTA 0, 16 skip top-K insertion, 32 no work pool,
@@ -655,8 +654,7 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
             uint32_t phase = 0;
             for (uint32_t round = 0;; round++) {
                 if (!wait_go(round & 1)) break;
-                for (int jj = 0; jj < ntiles + prm.prescan; jj++) {
-                    const int j = jj < ntiles ? jj : jj - ntiles;   // the pre-scanned tiles come again last
+                for (int j = 0; j < ntiles; j++) {
                     for (int kb = 0; kb < KB; kb++) {
                         mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
                         const uint32_t fb = smem_u32(&full[stage]);
@@ -705,7 +703,7 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
                 if (dbg) w_go += clock64() - t0;
                 if (!more) break;
                 tc_fence_after();
-                for (int jj = 0; jj < ntiles + prm.prescan; jj++, gtile++) {
+                for (int j = 0; j < ntiles; j++, gtile++) {
                   for (int h = 0; h < SUBS; h++) {
                     // sub-tile h = patterns [h TW, (h+1) TW) of the tile: rows h TW.. of
                     // every B stage (128 bytes per row), its own accumulator
@@ -1034,19 +1032,10 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
             if (I8) cst = primary ? make_uint2(kfloor, (uint32_t)cbase) : row_cont[row];
             const uint32_t kfl = cst.x;                 // keys <= kfl were examined by earlier passes
             const int cb = (int)cst.y;
-            int bmin = 0x7FFFFFFF;                      // int8 pre-scan minimum (q units)
-            auto wbase = [&]() -> int { return kfl ? cb : min(key_val(tk.k[0]), bmin); };
+            auto wbase = [&]() -> int { return kfl ? cb : key_val(tk.k[0]); };
             int lastq = kfl ? cb + wq : 0x7FFFFFFF;
             auto upd_lastq = [&]() { lastq = min(key_val(tk.k[KT - 1]) + 1, wbase() + wq); };
-            // int8 pre-scan: the first prm.prescan tiles only lower the running
-            // minimum (no insertions); they are scanned again, with insertions,
-            // after the last tile.  The running-minimum records of a fresh scan
-            // (the insertion path's main load at a round start) then start from
-            // the minimum over the pre-scanned tiles.
-            for (int jj = 0; jj < ntiles + prm.prescan; jj++, gtile++) {
-              const int j = jj < ntiles ? jj : jj - ntiles;
-              const bool minonly = I8 && jj < prm.prescan;
-              if (I8 && jj == prm.prescan && jj > 0) upd_lastq();
+            for (int j = 0; j < ntiles; j++, gtile++) {
               for (int h = 0; h < SUBS; h++) {
                 const uint32_t gs = gtile * SUBS + h;
                 const uint32_t buf = gs % NBUF;
@@ -1055,7 +1044,7 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
                 tc_fence_after();
                 const bool tr_on = trace && blockIdx.x == 0 && gs < (uint32_t)TRACE_TILES && lane == 0;
                 if (tr_on) trace[(size_t)gs * TRACE_W + warp] = clock64();
-                if (YSTAGE && primary && jj == ntiles + prm.prescan - 1 && h == SUBS - 1) {
+                if (YSTAGE && primary && j == ntiles - 1 && h == SUBS - 1) {
                     // every MMA of the round is complete: the B ring is idle until
                     // the next go.  Stage this row's y there for the certification,
                     // and the y of the next XS pool entries for this round's refills.
@@ -1182,8 +1171,6 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
                         const int mb = NLD == 2 ? min64_s16(vb, gb) : 0x7FFF;
                         if (PROF && (xp & 16)) {
                             if (ma == -12345 || mb == -12345) tk.k[0] = 0u;
-                        } else if (minonly) {
-                            bmin = min(bmin, min(ma, mb));
                         } else {
                             if (ma < lastq) slow8(va, ga, pa, ma);
                             if (NLD == 2 && mb < lastq) slow8(vb, gb, pa + 64, mb);
@@ -1218,7 +1205,7 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
                 }
                 if (tr_on) trace[(size_t)gs * TRACE_W + 8 + warp] = clock64();
               }
-                if (!primary && use_pool && jj >= j_claim && jj < j_claim + 3) pool_step(jj - j_claim);
+                if (!primary && use_pool && j >= j_claim && j < j_claim + 3) pool_step(j - j_claim);
             }
             if (dbg_on) { t_mark = clock64(); t_scan += t_mark - t_scan0; }
             if (dbg_seg) t_seg = clock64();

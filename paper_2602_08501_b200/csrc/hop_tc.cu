@@ -16,6 +16,12 @@ static bool tc_cluster() {
     return !(e && atoi(e) == 0);
 }
 
+// int8 screen: cta_group::2 pair kernel (MPW_TC_PAIR=1)
+static bool tc_pair() {
+    const char* e = getenv("MPW_TC_PAIR");
+    return e && atoi(e) == 1;
+}
+
 static int tc_experiment() {
     const char* e = getenv("MPW_TC_EXPERIMENT");
     return e ? atoi(e) : 0;
@@ -101,7 +107,7 @@ static int tc_launch_t(const TcPatterns& t, int n, int nw, int A, int T, const f
         if (trace) memset(trace, 0, tb);
         prm.trace = trace;
     }
-    const size_t smem = tc::smem_bytes(KB, LIMBS);
+    const size_t smem = tc::smem_bytes(KB, LIMBS, CL);
     auto kern = tc::hop_tc_kernel<KB, NW, LIMBS, MODE, CL>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return -(int)e;
@@ -149,11 +155,16 @@ int tc_launch(const TcPatterns& t, int n, int nw, int A, int T, const float* y, 
             case 128: return tc_experiment() ? tc_launch_t<1, 4, 0, 2>(t, n, nw, A, T, y, s2, P, num_sms, st)
                                              : tc_launch_t<1, 4, 0, 0>(t, n, nw, A, T, y, s2, P, num_sms, st);
             case 256: {
+                // single CTAs by default; MPW_TC_PAIR=1 selects the cta_group::2 pair
+                // kernel (correct, but slower: the pair's MMAs wait for the slower of
+                // two epilogues every tile -- 164 vs 115 ms at cfg4)
                 const int x = tc_experiment();
-                if (x == 128) return tc_launch_t<2, 8, 0, 1, 2>(t, n, nw, A, T, y, s2, P, num_sms, st);
+                const bool pair = tc_pair();
+                if (x == 128) return pair ? tc_launch_t<2, 8, 0, 1, 2>(t, n, nw, A, T, y, s2, P, num_sms, st)
+                                          : tc_launch_t<2, 8, 0, 1>(t, n, nw, A, T, y, s2, P, num_sms, st);
                 if (x) return tc_launch_t<2, 8, 0, 2>(t, n, nw, A, T, y, s2, P, num_sms, st);
-                return tc_cluster() ? tc_launch_t<2, 8, 0, 0, 2>(t, n, nw, A, T, y, s2, P, num_sms, st)
-                                    : tc_launch_t<2, 8, 0, 0>(t, n, nw, A, T, y, s2, P, num_sms, st);
+                return pair ? tc_launch_t<2, 8, 0, 0, 2>(t, n, nw, A, T, y, s2, P, num_sms, st)
+                            : tc_launch_t<2, 8, 0, 0>(t, n, nw, A, T, y, s2, P, num_sms, st);
             }
             default: return 1;
         }

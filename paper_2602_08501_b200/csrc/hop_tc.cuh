@@ -72,16 +72,25 @@ __host__ __device__ constexpr int fixed_bytes(int kb, int limbs) {
     // align slack: the int8 layout relies on the __align__(1024) of the dynamic
     // shared memory (checked in the kernel) to fit six 32 KB stages
     return (limbs == 0 ? 0 : 1024) + a_buffers(limbs) * kb * A_KBLK_BYTES + POOL_BYTES + ROWS * 4 /*row windows*/ +
-           (limbs == 0 ? ROWS * 8 : 0) /*int8 continuation state*/ + 256;
+           (limbs == 0 ? ROWS * 8 : 0) /*int8 continuation state*/ +
+           (limbs == 0 ? 384 : 256) /*barriers + flags: 8 B per barrier, up to 12 ring stages*/;
 }
 
-__host__ __device__ constexpr int stages_for(int kb, int limbs) {
-    return (SMEM_LIMIT - fixed_bytes(kb, limbs)) / B_STAGE_BYTES > 6 ? 6
-                                                                       : (SMEM_LIMIT - fixed_bytes(kb, limbs)) / B_STAGE_BYTES;
+// int8 screen with clusters of two: one tcgen05.mma.cta_group::2 (M = 256) per
+// K step for the CTA pair, each CTA holding its 128 rows of A and its half of
+// every P stage (128 patterns, 16 KB), so a ring stage is half as large
+__host__ __device__ constexpr bool pair_mma(int limbs, int cl) { return limbs == 0 && cl == 2; }
+__host__ __device__ constexpr int ring_stage_bytes(int limbs, int cl) {
+    return pair_mma(limbs, cl) ? B_STAGE_BYTES / 2 : B_STAGE_BYTES;
+}
+__host__ __device__ constexpr int stages_for(int kb, int limbs, int cl = 1) {
+    return (SMEM_LIMIT - fixed_bytes(kb, limbs)) / ring_stage_bytes(limbs, cl) > (pair_mma(limbs, cl) ? 12 : 6)
+               ? (pair_mma(limbs, cl) ? 12 : 6)
+               : (SMEM_LIMIT - fixed_bytes(kb, limbs)) / ring_stage_bytes(limbs, cl);
 }
 
-__host__ __device__ constexpr size_t smem_bytes(int kb, int limbs) {
-    return (size_t)fixed_bytes(kb, limbs) + (size_t)stages_for(kb, limbs) * B_STAGE_BYTES;
+__host__ __device__ constexpr size_t smem_bytes(int kb, int limbs, int cl = 1) {
+    return (size_t)fixed_bytes(kb, limbs) + (size_t)stages_for(kb, limbs, cl) * ring_stage_bytes(limbs, cl);
 }
 
 // ---------------------------------------------------------------------------
@@ -207,6 +216,19 @@ __device__ __forceinline__ void tc_mma_i8(uint32_t d_tmem, uint64_t adesc, uint6
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void tc_mma_i8_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                               uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void tc_commit_pair(uint32_t bar, uint16_t ctamask) {
+    asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                 ::"r"(bar), "h"(ctamask)
+                 : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 template <int NT>
@@ -564,9 +586,11 @@ __device__ __forceinline__ void certify_window(const TopK<K>& t, const float* __
 // traffic; the pair runs its rounds in step.
 template <int KB, int NW, int LIMBS, int MODE, int CL>
 __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params prm) {
-    constexpr int STAGES = stages_for(KB, LIMBS);
+    constexpr int STAGES = stages_for(KB, LIMBS, CL);
     constexpr bool PROF = MODE == 2;
     constexpr bool I8 = LIMBS == 0;                  // int8 screen (see the header comment)
+    constexpr bool PAIR = pair_mma(LIMBS, CL);       // cta_group::2 MMAs issued by the pair's rank 0
+    constexpr int RSB = ring_stage_bytes(LIMBS, CL); // bytes of one ring stage in this CTA
     constexpr int KT = I8 ? TOPK_I8 : TOPK;          // candidates tracked per row
     // SUBS = 2 would issue every 256-pattern tile as two N = 128 sub-tiles into
     // four 128-column accumulators (MMAs up to two tiles ahead of the
@@ -579,7 +603,7 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
     constexpr int EPI_T = 32 * EW;
     constexpr int WC = TW * 4 / EW;                  // accumulator columns per epilogue warp
     // round-end staging of every row's received word in the (then idle) B ring
-    constexpr bool YSTAGE = ROWS * (NW * 32 * 4 + 16) <= STAGES * B_STAGE_BYTES;
+    constexpr bool YSTAGE = ROWS * (NW * 32 * 4 + 16) <= STAGES * RSB;
     const int xp = PROF ? prm.experiment : 0;
     long long* const trace = MODE >= 1 ? prm.trace : nullptr;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -588,7 +612,7 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
     unsigned char* a_hi = sm;
     unsigned char* a_lo = sm + KB * A_KBLK_BYTES;          // used only when LIMBS == 2
     unsigned char* b_ring = sm + a_buffers(LIMBS) * KB * A_KBLK_BYTES;
-    PoolEnt* pool = reinterpret_cast<PoolEnt*>(b_ring + STAGES * B_STAGE_BYTES);   // [POOL]
+    PoolEnt* pool = reinterpret_cast<PoolEnt*>(b_ring + STAGES * RSB);             // [POOL]
     float* row_wadd = reinterpret_cast<float*>(pool + POOL);                        // [ROWS]
     // int8: per-row continuation state {key floor, window base} for the secondary half
     uint2* row_cont = reinterpret_cast<uint2*>(row_wadd + ROWS);                    // [ROWS] (I8 only)
@@ -613,8 +637,14 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
     const int n = prm.n, nw = prm.nw, A = prm.A, T = prm.T, np_ = prm.np, ntiles = prm.ntiles;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < STAGES; s++) { mbar_init(smem_u32(&full[s]), 1); mbar_init(smem_u32(&empty[s]), CL); }
-        for (int b = 0; b < NBUF; b++) { mbar_init(smem_u32(&tfull[b]), 1); mbar_init(smem_u32(&tempty[b]), EW); }
+        // PAIR: rank 0's full[] also waits for the peer's half of the stage (one
+        // forwarded arrival) and its tempty[] for the peer's epilogue warps
+        const uint32_t lead = (PAIR && crank == 0) ? 2u : 1u;
+        for (int s = 0; s < STAGES; s++) {
+            mbar_init(smem_u32(&full[s]), lead);
+            mbar_init(smem_u32(&empty[s]), PAIR ? 1 : CL);
+        }
+        for (int b = 0; b < NBUF; b++) { mbar_init(smem_u32(&tfull[b]), 1); mbar_init(smem_u32(&tempty[b]), EW * lead); }
         mbar_init(smem_u32(go), CL);
         mbar_init(smem_u32(&ybar[0]), 128);
         mbar_init(smem_u32(&ybar[1]), 128);
@@ -624,8 +654,13 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        if constexpr (PAIR) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        }
     }
     tc_fence_before();
     __syncthreads();
@@ -658,7 +693,12 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
                     for (int kb = 0; kb < KB; kb++) {
                         mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
                         const uint32_t fb = smem_u32(&full[stage]);
-                        if (PROF && (xp & 256) && round > 0) {
+                        if constexpr (PAIR) {
+                            // this CTA's half of the stage (patterns 128 crank .. +127) into its own ring
+                            mbar_expect_tx(fb, RSB);
+                            bulk_g2s(smem_u32(b_ring + stage * RSB),
+                                     prm.btiles + ((size_t)j * KB + kb) * B_STAGE_BYTES + crank * RSB, RSB, fb);
+                        } else if (PROF && (xp & 256) && round > 0) {
                             // profiling only (results wrong): no P traffic after the first round
                             mbar_arrive(fb);
                         } else if (PROF && (xp & 1024)) {
@@ -686,11 +726,26 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
             }
         }
     } else if (warp == 1) {
-        // ===== MMA issuer =====
-        if (lane == 0) {
-            // f16: D f32 (1 << 4), A/B f16.  i8: D s32 (2 << 4), A s8 (1 << 7), B u8.
+        // ===== MMA issuer (PAIR: rank 0 only, for both CTAs) =====
+        if (PAIR && lane == 0 && crank == 1) {
+            // rank 1's MMA warp is the forwarder: once this CTA's half of a stage has
+            // landed, one arrival on the same stage's full barrier of rank 0
+            int stage = 0;
+            uint32_t phase = 0;
+            const uint32_t full0 = mapa_peer(smem_u32(full), 0);
+            for (uint32_t round = 0;; round++) {
+                if (!wait_go(round & 1)) break;
+                for (int u = 0; u < ntiles * KB; u++) {
+                    mbar_wait(smem_u32(&full[stage]), phase);
+                    mbar_arrive_cluster(full0 + stage * 8);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+        if (lane == 0 && (!PAIR || crank == 0)) {
+            // f16: D f32 (1 << 4), A/B f16.  i8: D s32 (2 << 4), A s8 (1 << 7), B u8.  M = 256 for the pair
             const uint32_t idesc = (I8 ? (2u << 4) | (1u << 7) : (1u << 4)) | ((uint32_t)(TW >> 3) << 17) |
-                                   ((uint32_t)(ROWS >> 4) << 24);
+                                   ((uint32_t)((PAIR ? 2 : 1) * ROWS >> 4) << 24);
             int stage = 0;
             uint32_t phase = 0;
             uint32_t gtile = 0;
@@ -725,13 +780,15 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
                             if (dbg) w_full += clock64() - t0;
                             tc_fence_after();
                         }
-                        const uint64_t bd = sw128_desc(bring + st * B_STAGE_BYTES + h * TW * 128);
+                        const uint64_t bd = sw128_desc(bring + st * RSB + h * TW * 128);
                         const uint64_t ah = sw128_desc(ahi + kb * A_KBLK_BYTES);
                         const uint64_t al = sw128_desc(alo + kb * A_KBLK_BYTES);
 #pragma unroll
                         for (int ks = 0; ks < 4; ks++) {
                             // +32 bytes per K step (16 fp16 / 32 int8 elements) inside the 128-byte swizzle row
-                            if (I8) {
+                            if (PAIR) {
+                                tc_mma_i8_pair(d, ah + 2 * ks, bd + 2 * ks, idesc, (kb | ks) != 0);
+                            } else if (I8) {
                                 tc_mma_i8(d, ah + 2 * ks, bd + 2 * ks, idesc, (kb | ks) != 0);
                             } else {
                                 tc_mma_f16(d, ah + 2 * ks, bd + 2 * ks, idesc, (kb | ks) != 0);
@@ -739,12 +796,14 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
                             }
                         }
                         if (h == SUBS - 1) {   // the stage's last reader: free it
-                            if (CL > 1) tc_commit_mc(smem_u32(&empty[st]), CMASK);   // in both CTAs of the pair
+                            if (PAIR) tc_commit_pair(smem_u32(&empty[st]), CMASK);
+                            else if (CL > 1) tc_commit_mc(smem_u32(&empty[st]), CMASK);   // in both CTAs of the pair
                             else tc_commit(smem_u32(&empty[st]));
                         }
                         if (++st == STAGES) { st = 0; ph ^= 1; }
                     }
-                    tc_commit(smem_u32(&tfull[buf]));
+                    if (PAIR) tc_commit_pair(smem_u32(&tfull[buf]), CMASK);   // both CTAs' accumulators
+                    else tc_commit(smem_u32(&tfull[buf]));
                     if (tr_on) trace[(size_t)gs * TRACE_W + 1] = clock64();
                     if (h == SUBS - 1) { stage = st; phase = ph; }
                   }
@@ -1005,7 +1064,7 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
         constexpr uint32_t YP = YB + 16;
         float* const ysm = reinterpret_cast<float*>(b_ring + (size_t)row * YP);
         // pool entries whose y is staged beside the rows' at the round end
-        constexpr int XS_FIT = YSTAGE ? (int)((STAGES * B_STAGE_BYTES - ROWS * YP) / YP) : 0;
+        constexpr int XS_FIT = YSTAGE ? (int)((STAGES * RSB - ROWS * YP) / YP) : 0;
         constexpr int XS = XS_FIT < POOL ? XS_FIT : POOL;
         int xs_base = 0;
         const bool dbg_on = (xp & 8) && blockIdx.x == 0 && primary && row == 0;
@@ -1141,7 +1200,10 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
                 auto release = [&]() {
                     tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(smem_u32(&tempty[buf]));
+                    if (lane == 0) {
+                        if (PAIR && crank == 1) mbar_arrive_cluster(mapa_peer(smem_u32(&tempty[buf]), 0));
+                        else mbar_arrive(smem_u32(&tempty[buf]));
+                    }
                 };
                 if constexpr (I8) {
                     // the warp's TW/2 columns as packed s16 scores (64 per load), one wait
@@ -1458,7 +1520,8 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
     if (CL > 1) cluster_sync_all();      // no CTA leaves while its peer may still signal it
     if (warp == 1) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+        if constexpr (PAIR) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+        else asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
     }
 }
 

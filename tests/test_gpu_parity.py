@@ -185,3 +185,27 @@ def test_int8_window_overflow_continuation(name, monkeypatch):
     assert set(mism.tolist()) <= set(risky.tolist()), f"mismatches {mism}"
     ok = np.setdiff1d(np.arange(F), risky)
     np.testing.assert_array_equal(_np(o["iters"])[ok], r["iters"][ok])
+
+
+def test_int8_pair_kernel_vs_oracle(monkeypatch):
+    """The cta_group::2 variant of the int8 screen (MPW_TC_PAIR=1: one M = 256 MMA
+    per K step for a CTA pair, each CTA holding half of every P stage) decodes
+    like the oracle."""
+    cfg = configs.CONFIGS["cfg4"]
+    code, sph = code_and_sphere(cfg)
+    from paper_2602_08501_b200 import channel
+    sigma = cfg.sigma(code=code)
+    F = 192
+    _, cw, y = channel.bulk_inputs(code, 13, 0, 0, F, sigma)
+    monkeypatch.setenv("MPW_TC_PAIR", "1")
+    o = decoder(cfg).two_stage_batch(y, sigma, cfg.list_size, cfg.num_paths, cfg.max_iterations,
+                                     cfg.activation_mode, variant="tensor_i8")
+    r = orc.two_stage_batch(y, code, sph, cfg.list_size, cfg.num_paths, cfg.max_iterations,
+                            cfg.activation_mode == "crc_gated", sigma, nthreads=8)
+    best = words32_to_64(_np(o["best"]).view(np.uint32), code.n)
+    flags = _np(o["flags"])
+    assert not (flags & UNRESOLVED).any()
+    mism = np.flatnonzero((best != r["best"]).any(axis=1))
+    assert set(mism.tolist()) <= set(np.flatnonzero(flags & TIE_FINAL).tolist())
+    ok = np.flatnonzero(~(flags & TIE_FINAL).astype(bool))
+    np.testing.assert_array_equal(_np(o["iters"])[ok], r["iters"][ok])

@@ -55,7 +55,8 @@ constexpr int TOPK = MPW_TC_TOPK;    // candidates tracked per row for certifica
 static_assert(TOPK <= 8, "top-K hand-over uses 16 TMEM columns");
 constexpr int TOPK_I8 = 16;          // int8 screen: wider window (hand-over uses 32 columns)
 constexpr int TRACE_W = 18, TRACE_TILES = 1 << 16;
-constexpr int POOL = 64;                     // prefetched stage-2 work items per CTA
+// prefetched stage-2 work items per CTA (int8: 32, its smem holds the rows' shared minima)
+__host__ __device__ constexpr int pool_size(int limbs) { return limbs == 0 ? 32 : 64; }
 
 // One prefetched trajectory of the stage-2 queue (claimed mid-round by the
 // secondary epilogue warps, consumed by row refills at the round end).
@@ -65,13 +66,14 @@ struct PoolEnt {
     float err;         // per-frame score error bound for this limb count
     int pad;           // int8 screen: the frame's inv_s (float bits)
 };
-constexpr int POOL_BYTES = POOL * (int)sizeof(PoolEnt);
+__host__ __device__ constexpr int pool_bytes(int limbs) { return pool_size(limbs) * (int)sizeof(PoolEnt); }
 
 __host__ __device__ constexpr int a_buffers(int limbs) { return limbs == 2 ? 2 : 1; }
 __host__ __device__ constexpr int fixed_bytes(int kb, int limbs) {
     // align slack: the int8 layout relies on the __align__(1024) of the dynamic
     // shared memory (checked in the kernel) to fit six 32 KB stages
-    return (limbs == 0 ? 0 : 1024) + a_buffers(limbs) * kb * A_KBLK_BYTES + POOL_BYTES + ROWS * 4 /*row windows*/ +
+    return (limbs == 0 ? 0 : 1024) + a_buffers(limbs) * kb * A_KBLK_BYTES + pool_bytes(limbs) + ROWS * 4 /*row windows*/ +
+           (limbs == 0 ? ROWS * 4 : 0) /*int8 shared running minima*/ +
            (limbs == 0 ? ROWS * 8 : 0) /*int8 continuation state*/ +
            (limbs == 0 ? 384 : 256) /*barriers + flags: 8 B per barrier, up to 12 ring stages*/;
 }
@@ -612,8 +614,11 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
     unsigned char* a_hi = sm;
     unsigned char* a_lo = sm + KB * A_KBLK_BYTES;          // used only when LIMBS == 2
     unsigned char* b_ring = sm + a_buffers(LIMBS) * KB * A_KBLK_BYTES;
+    constexpr int POOL = pool_size(LIMBS);
     PoolEnt* pool = reinterpret_cast<PoolEnt*>(b_ring + STAGES * RSB);             // [POOL]
-    float* row_wadd = reinterpret_cast<float*>(pool + POOL);                        // [ROWS]
+    // int8: running minimum of each row over both column halves (q units), reset at every round end
+    int* row_best = reinterpret_cast<int*>(pool + POOL);                            // [ROWS] (I8 only)
+    float* row_wadd = reinterpret_cast<float*>(row_best + (I8 ? ROWS : 0));         // [ROWS]
     // int8: per-row continuation state {key floor, window base} for the secondary half
     uint2* row_cont = reinterpret_cast<uint2*>(row_wadd + ROWS);                    // [ROWS] (I8 only)
     uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<unsigned char*>(row_wadd + ROWS) +
@@ -1029,7 +1034,7 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
             active = claim_direct();
             if (active) build_row(prm.y + (size_t)frame * n);
             row_wadd[row] = row_window();
-            if (I8) row_cont[row] = make_uint2(0u, 0u);
+            if (I8) { row_cont[row] = make_uint2(0u, 0u); row_best[row] = 0x7FFFFFFF; }
         }
         // round-end signal: this CTA's rows-left flag to every CTA of the cluster,
         // then one arrive on every CTA's go barrier; the epilogue continues while
@@ -1091,7 +1096,10 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
             if (I8) cst = primary ? make_uint2(kfloor, (uint32_t)cbase) : row_cont[row];
             const uint32_t kfl = cst.x;                 // keys <= kfl were examined by earlier passes
             const int cb = (int)cst.y;
-            auto wbase = [&]() -> int { return kfl ? cb : key_val(tk.k[0]); };
+            // window base: this half's best or the row's best over both halves
+            // (published in smem every tile), whichever is lower
+            int shb = 0x7FFFFFFF, pub = 0x7FFFFFFF;
+            auto wbase = [&]() -> int { return kfl ? cb : min(key_val(tk.k[0]), shb); };
             int lastq = kfl ? cb + wq : 0x7FFFFFFF;
             auto upd_lastq = [&]() { lastq = min(key_val(tk.k[KT - 1]) + 1, wbase() + wq); };
             for (int j = 0; j < ntiles; j++, gtile++) {
@@ -1266,6 +1274,13 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
                     if (mb < lastv) slow(vb, pbase + (ch0 + k + 1) * 32, mb);
                 }
                 if (tr_on) trace[(size_t)gs * TRACE_W + 8 + warp] = clock64();
+                if (I8 && !kfl) {
+                    // publish this half's best, take the row's best over both halves
+                    const int mine = key_val(tk.k[0]);
+                    if (mine < pub) { atomicMin(&row_best[row], mine); pub = mine; }
+                    const int sh = *reinterpret_cast<volatile int*>(&row_best[row]);
+                    if (sh < shb) { shb = sh; upd_lastq(); }
+                }
               }
                 if (!primary && use_pool && j >= j_claim && j < j_claim + 3) pool_step(j - j_claim);
             }
@@ -1481,7 +1496,7 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
             SEG(4);
             if (primary) {
                 row_wadd[row] = row_window();
-                if (I8) row_cont[row] = make_uint2(kfloor, (uint32_t)cbase);
+                if (I8) { row_cont[row] = make_uint2(kfloor, (uint32_t)cbase); row_best[row] = 0x7FFFFFFF; }
             }
             fence_proxy_async();
             any = epi_bar_or<EPI_T>(active);

@@ -198,7 +198,7 @@ __device__ __forceinline__ float4 warp_error_bounds(const float* __restrict__ yr
 // fp32 operations).  The MMA sums the q_i exactly (s32 accumulators), so the
 // score error of every pattern is at most the sum of the wmax largest
 // |(|y_i| - s·q_i)| plus the fp32 rounding of s·acc and of the window
-// arithmetic (|acc| <= 127·wmax).  Returns {inv_s, s, bound, 0}.
+// arithmetic (|acc| <= 127·wmax).  Returns {inv_s, s, bound, sum|y| (rounded up)}.
 __device__ __forceinline__ float i8_inv_scale(float ymax) {
     return ymax > 1e-30f ? __fdiv_rn(127.0f, ymax) : 1.0f;
 }
@@ -224,7 +224,11 @@ __device__ __forceinline__ float4 warp_i8_scale(const float* __restrict__ yrow, 
     }
     const float T8 = warp_topw_bound(e8, cnt, wmax);
     const float u = 1.1920929e-7f;   // 2^-23
-    return make_float4(inv_s, s, T8 + 4.0f * u * s * 127.0f * (float)wmax, 0.0f);
+    float sa = 0.0f;                 // sum |y_i|, rounded up below (certification bound)
+    for (int j = 0; j < cnt; j++) sa += ay[j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sa += __shfl_xor_sync(MPW_FULL, sa, o);
+    return make_float4(inv_s, s, T8 + 4.0f * u * s * 127.0f * (float)wmax, sa * 1.0001f);
 }
 
 // Running top-K (K small) of a scan; ascending values, index order breaks ties.

@@ -65,6 +65,8 @@ struct PoolEnt {
     int frame;
     float err;         // per-frame score error bound for this limb count
     int pad;           // int8 screen: the frame's inv_s (float bits)
+    float ay;          // sum |y_i| of the frame (certification bound)
+    int pad2[3];
 };
 __host__ __device__ constexpr int pool_bytes(int limbs) { return pool_size(limbs) * (int)sizeof(PoolEnt); }
 
@@ -425,7 +427,7 @@ __device__ __forceinline__ void certify_window(const TopK<K>& t, const float* __
                                                const uint32_t (&c)[NW], const uint32_t* __restrict__ pbits,
                                                float ed, float tie_rel, float err_row, int& best, bool& improve,
                                                float& best_approx, uint8_t& flags, uint32_t (&best_bits)[NW],
-                                               bool& have_bits, float& best_score) {
+                                               bool& have_bits, float& best_score, float ay_pre) {
     const float thr = tie_rel * ed * 0.25f;
     const float win = thr + 2.0f * err_row;
     best = t.i[0];
@@ -459,7 +461,10 @@ __device__ __forceinline__ void certify_window(const TopK<K>& t, const float* __
         float s32[K - 1];
 #pragma unroll
         for (int k = 0; k < K - 1; k++) s32[k] = 0.f;
-        float ay = 0.f;
+        // two partial sums per candidate (even / odd positions): half the dependent chain
+        float s32b[K - 1];
+#pragma unroll
+        for (int k = 0; k < K - 1; k++) s32b[k] = 0.f;
         uint32_t bw[K - 1];
 #pragma unroll 1
         for (int hw = 0; hw < 2 * NW; hw++) {
@@ -475,20 +480,23 @@ __device__ __forceinline__ void certify_window(const TopK<K>& t, const float* __
             const uint32_t cw = select_word<NW>(c, w) >> sh;
             float tv[16];
 #pragma unroll
-            for (int bb = 0; bb < 16; bb++) {
-                tv[bb] = __uint_as_float(__float_as_uint(yv[bb]) ^ (((cw >> bb) & 1u) << 31));
-                ay += fabsf(yv[bb]);
-            }
+            for (int bb = 0; bb < 16; bb++) tv[bb] = __uint_as_float(__float_as_uint(yv[bb]) ^ (((cw >> bb) & 1u) << 31));
 #pragma unroll
             for (int k = 0; k < K - 1; k++) {
                 if (k >= ncand) break;
                 const uint32_t bk = bw[k] >> sh;
 #pragma unroll
-                for (int bb = 0; bb < 16; bb++)
+                for (int bb = 0; bb < 16; bb += 2) {
                     if ((bk >> bb) & 1u) s32[k] += tv[bb];
+                    if ((bk >> (bb + 1)) & 1u) s32b[k] += tv[bb + 1];
+                }
             }
         }
-        const double bnd = (double)ay * (64.0 * 5.9604645e-8 * 1.001) * 1.0001;   // >= gamma_63 * sum|y| (+ rounding of ay)
+#pragma unroll
+        for (int k = 0; k < K - 1; k++) s32[k] += s32b[k];
+        // any summation order of <= 64 terms: |fl(S) - S| <= gamma_63 * sum|y|; sum|y| of
+        // the frame precomputed (warp_i8_scale, rounded up)
+        const double bnd = (double)ay_pre * (64.0 * 5.9604645e-8 * 1.001) * 1.0001;
         // argmin (ties -> lowest pattern index) and the runner-up, in fp32
         // (indices and approximations tracked in registers: no runtime indexing
         // of the top-K arrays, which would move them to local memory)
@@ -836,6 +844,7 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
         int iters = 0, frame = 0;
         float ed = 0.f, err_row = 0.f;
         float inv_s = 1.f, sc = 1.f;             // int8 screen: quantisation of this row's frame
+        float ay_row = 0.f;                      // sum |y_i| of this row's frame
         // int8 window overflow: when more than KT-1 candidates fall inside the
         // certification window, the row re-scans P in the next round collecting
         // the keys above kfloor (same window base cbase), and the exact scores
@@ -851,7 +860,7 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
         // this secondary thread's in-flight pool claim
         int cl_tr = -1, cl_q = 0;
         int cl_frame = 0, cl_nanc = 0;
-        float cl_err = 0.f, cl_inv = 1.f;
+        float cl_err = 0.f, cl_inv = 1.f, cl_ay = 0.f;
         // the pool needs three tile boundaries per round; with fewer tiles rows
         // refill straight from the global queue
         const int j_claim = ntiles >= 3 ? (ntiles / 2 < ntiles - 3 ? ntiles / 2 : ntiles - 3) : -1;
@@ -866,8 +875,9 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
                 if (a >= prm.s2.nanchor[q]) continue;
                 tr = cand;
                 frame = prm.s2.frame[q];
+                const float4 qs = prm.s2.qscale[q];
+                ay_row = qs.w;
                 if (I8) {
-                    const float4 qs = prm.s2.qscale[q];
                     inv_s = qs.x;
                     sc = qs.y;
                     err_row = qs.z;
@@ -893,6 +903,7 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
                 tr = e.tr;
                 frame = e.frame;
                 err_row = e.err;
+                ay_row = e.ay;
                 if (I8) {
                     inv_s = __int_as_float(e.pad);
                     sc = __frcp_rn(inv_s);
@@ -911,6 +922,7 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
             // pair is one f16x2 conversion and a sign-bit flip; the fp32 canonical
             // ED (only used for the tie window) is |y|^2 + N - 2 sum_i x_i y_i
             float syy = 0.f, sxy = 0.f;
+            float syy4[4] = {0.f, 0.f, 0.f, 0.f}, sxy4[4] = {0.f, 0.f, 0.f, 0.f};   // int8 rows: 4 chains
             const float4* y4 = reinterpret_cast<const float4*>(ysrc);
             float4 yb[2][8];
 #pragma unroll
@@ -939,8 +951,8 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
                                 const int q = i8_quant(fabsf(yv), inv_s);
                                 const bool neg = (((cw >> bi) & 1u) != 0u) != (yv < 0.0f);
                                 acc |= ((uint32_t)(neg ? -q : q) & 0xFFu) << (8 * b);
-                                syy = fmaf(yv, yv, syy);
-                                sxy += __uint_as_float(__float_as_uint(yv) ^ (((cw >> bi) & 1u) << 31));
+                                syy4[b] = fmaf(yv, yv, syy4[b]);
+                                sxy4[b] += __uint_as_float(__float_as_uint(yv) ^ (((cw >> bi) & 1u) << 31));
                             }
                             qw[e4] = acc;
                         }
@@ -976,6 +988,10 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
                     if (LIMBS == 2) *reinterpret_cast<uint4*>(a_lo + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
                 }
             }
+            if (I8) {
+                syy = (syy4[0] + syy4[1]) + (syy4[2] + syy4[3]);
+                sxy = (sxy4[0] + sxy4[1]) + (sxy4[2] + sxy4[3]);
+            }
             ed = syy + (float)n - 2.0f * sxy;
         };
         auto store_row = [&]() {
@@ -999,8 +1015,9 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
                     cl_q = cl_tr / A;
                     cl_nanc = prm.s2.nanchor[cl_q];
                     cl_frame = prm.s2.frame[cl_q];
+                    const float4 qs = prm.s2.qscale[cl_q];
+                    cl_ay = qs.w;
                     if (I8) {
-                        const float4 qs = prm.s2.qscale[cl_q];
                         cl_err = qs.z;
                         cl_inv = qs.x;
                     } else {
@@ -1016,6 +1033,7 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
                     e.frame = cl_frame;
                     e.err = cl_err;
                     e.pad = __float_as_int(cl_inv);
+                    e.ay = cl_ay;
                     prefetch_l2(prm.s2.anchors + (size_t)cl_tr * NW);
                     const char* yl = reinterpret_cast<const char*>(prm.y + (size_t)cl_frame * n);
                     for (int o = 0; o < n * 4; o += 128) prefetch_l2(yl + o);
@@ -1401,10 +1419,10 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
                     }
                     if (YSTAGE)
                         certify_window<KT, NW, true, I8>(cand, ysm, c, prm.pbits, ed, prm.tie_rel, err_row, i1,
-                                                         improve, sb, flags, pwv, have_bits, sx);
+                                                         improve, sb, flags, pwv, have_bits, sx, ay_row);
                     else
                         certify_window<KT, NW, false, I8>(cand, yrow, c, prm.pbits, ed, prm.tie_rel, err_row, i1,
-                                                          improve, sb, flags, pwv, have_bits, sx);
+                                                          improve, sb, flags, pwv, have_bits, sx, ay_row);
                     if (I8) sb = sx;
                 }
                 if (!cont_more) iters++;

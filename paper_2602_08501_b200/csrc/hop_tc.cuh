@@ -66,7 +66,6 @@ struct PoolEnt {
     float err;         // per-frame score error bound for this limb count
     int pad;           // int8 screen: the frame's inv_s (float bits)
     float ay;          // sum |y_i| of the frame (certification bound)
-    int pad2[3];
 };
 __host__ __device__ constexpr int pool_bytes(int limbs) { return pool_size(limbs) * (int)sizeof(PoolEnt); }
 

@@ -1,5 +1,5 @@
 # Round measurement: bench line (ours + reference arm), ncu launch list, ncu full captures of the hop and SCL kernels.
-P=${PFX:-r01f}
+P=${PFX:-r01g}
 timeout 900 python bench.py > gpurun_out/${P}_bench.jsonl 2> gpurun_out/${P}_bench.err; echo bench rc=$?
 timeout 600 python bench.py --impl reference --steps 2 --warmup 3 >> gpurun_out/${P}_bench.jsonl 2>> gpurun_out/${P}_bench.err; echo ref rc=$?
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/${P}_launches.csv \

@@ -53,7 +53,11 @@ constexpr int SMEM_LIMIT = 232448;   // 227 KB opt-in maximum per CTA
 #endif
 constexpr int TOPK = MPW_TC_TOPK;    // candidates tracked per row for certification
 static_assert(TOPK <= 8, "top-K hand-over uses 16 TMEM columns");
-constexpr int TOPK_I8 = 16;          // int8 screen: wider window (hand-over uses 32 columns)
+#ifndef MPW_TC_TOPK_I8
+#define MPW_TC_TOPK_I8 16
+#endif
+constexpr int TOPK_I8 = MPW_TC_TOPK_I8;   // int8 screen: keys per row (window overflow -> continuation pass)
+static_assert(TOPK_I8 <= 16, "int8 top-K hand-over uses 16 TMEM columns");
 constexpr int TRACE_W = 18, TRACE_TILES = 1 << 16;
 // prefetched stage-2 work items per CTA (int8: 32, its smem holds the rows' shared minima)
 __host__ __device__ constexpr int pool_size(int limbs) { return limbs == 0 ? 32 : 64; }
@@ -1316,8 +1320,8 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
 #pragma unroll
                 for (int k = 0; k < 8; k++) {
                     if constexpr (I8) {
-                        xs[k] = tk.k[k];
-                        xs[8 + k] = tk.k[8 + k];
+                        xs[k] = k < KT ? tk.k[k] : 0xFFFFFFFFu;
+                        xs[8 + k] = 8 + k < KT ? tk.k[(8 + k) % KT] : 0xFFFFFFFFu;
                     } else {
                         xs[k] = k < KT ? __float_as_uint(top.b[k]) : 0u;
                         xs[8 + k] = k < KT ? (uint32_t)top.i[k] : 0u;

@@ -22,6 +22,12 @@ static bool tc_pair() {
     return e && atoi(e) == 1;
 }
 
+// int8 screen cluster size (default 1: single CTAs)
+static int tc_i8_cluster() {
+    const char* e = getenv("MPW_TC_I8_CL");
+    return e ? atoi(e) : 1;
+}
+
 static int tc_experiment() {
     const char* e = getenv("MPW_TC_EXPERIMENT");
     return e ? atoi(e) : 0;
@@ -91,7 +97,7 @@ int tc_build(TcPatterns& t, const uint32_t* bits, int np, int n, int nw) {
     return 0;
 }
 
-template <int KB, int NW, int LIMBS, int MODE, int CL = 1>
+template <int KB, int NW, int LIMBS, int MODE, int CL = 1, int PM = 0>
 static int tc_launch_t(const TcPatterns& t, int n, int nw, int A, int T, const float* y, S2Dev s2, PatDev P,
                        int num_sms, cudaStream_t st) {
     tc::Params prm;
@@ -107,8 +113,8 @@ static int tc_launch_t(const TcPatterns& t, int n, int nw, int A, int T, const f
         if (trace) memset(trace, 0, tb);
         prm.trace = trace;
     }
-    const size_t smem = tc::smem_bytes(KB, LIMBS, CL);
-    auto kern = tc::hop_tc_kernel<KB, NW, LIMBS, MODE, CL>;
+    const size_t smem = tc::smem_bytes(KB, LIMBS, CL, PM);
+    auto kern = tc::hop_tc_kernel<KB, NW, LIMBS, MODE, CL, PM>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return -(int)e;
     if (CL == 1) {
@@ -155,16 +161,19 @@ int tc_launch(const TcPatterns& t, int n, int nw, int A, int T, const float* y, 
             case 128: return tc_experiment() ? tc_launch_t<1, 4, 0, 2>(t, n, nw, A, T, y, s2, P, num_sms, st)
                                              : tc_launch_t<1, 4, 0, 0>(t, n, nw, A, T, y, s2, P, num_sms, st);
             case 256: {
-                // single CTAs by default; MPW_TC_PAIR=1 selects the cta_group::2 pair
-                // kernel (correct, but slower: the pair's MMAs wait for the slower of
-                // two epilogues every tile -- 164 vs 115 ms at cfg4)
+                // MPW_TC_I8_CL: 1 single CTAs, 2 CTA pairs sharing the P stream by
+                // multicast; MPW_TC_PAIR=1 selects the cta_group::2 pair kernel (correct,
+                // but slower: the pair's MMAs wait for the slower of two epilogues)
                 const int x = tc_experiment();
                 const bool pair = tc_pair();
-                if (x == 128) return pair ? tc_launch_t<2, 8, 0, 1, 2>(t, n, nw, A, T, y, s2, P, num_sms, st)
-                                          : tc_launch_t<2, 8, 0, 1>(t, n, nw, A, T, y, s2, P, num_sms, st);
+                const int cl = tc_i8_cluster();
+                if (x == 128) return pair ? tc_launch_t<2, 8, 0, 1, 2, 1>(t, n, nw, A, T, y, s2, P, num_sms, st)
+                                          : cl == 2 ? tc_launch_t<2, 8, 0, 1, 2>(t, n, nw, A, T, y, s2, P, num_sms, st)
+                                                    : tc_launch_t<2, 8, 0, 1>(t, n, nw, A, T, y, s2, P, num_sms, st);
                 if (x) return tc_launch_t<2, 8, 0, 2>(t, n, nw, A, T, y, s2, P, num_sms, st);
-                return pair ? tc_launch_t<2, 8, 0, 0, 2>(t, n, nw, A, T, y, s2, P, num_sms, st)
-                            : tc_launch_t<2, 8, 0, 0>(t, n, nw, A, T, y, s2, P, num_sms, st);
+                if (pair) return tc_launch_t<2, 8, 0, 0, 2, 1>(t, n, nw, A, T, y, s2, P, num_sms, st);
+                return cl == 2 ? tc_launch_t<2, 8, 0, 0, 2>(t, n, nw, A, T, y, s2, P, num_sms, st)
+                               : tc_launch_t<2, 8, 0, 0>(t, n, nw, A, T, y, s2, P, num_sms, st);
             }
             default: return 1;
         }

@@ -86,18 +86,20 @@ __host__ __device__ constexpr int fixed_bytes(int kb, int limbs) {
 // int8 screen with clusters of two: one tcgen05.mma.cta_group::2 (M = 256) per
 // K step for the CTA pair, each CTA holding its 128 rows of A and its half of
 // every P stage (128 patterns, 16 KB), so a ring stage is half as large
-__host__ __device__ constexpr bool pair_mma(int limbs, int cl) { return limbs == 0 && cl == 2; }
-__host__ __device__ constexpr int ring_stage_bytes(int limbs, int cl) {
-    return pair_mma(limbs, cl) ? B_STAGE_BYTES / 2 : B_STAGE_BYTES;
+// (pm: the pair-MMA variant, int8 with CL = 2 only; CL = 2 without it shares
+// the P stream of the pair by multicast copies, each CTA issuing its own MMAs)
+__host__ __device__ constexpr bool pair_mma(int limbs, int cl, int pm) { return pm && limbs == 0 && cl == 2; }
+__host__ __device__ constexpr int ring_stage_bytes(int limbs, int cl, int pm) {
+    return pair_mma(limbs, cl, pm) ? B_STAGE_BYTES / 2 : B_STAGE_BYTES;
 }
-__host__ __device__ constexpr int stages_for(int kb, int limbs, int cl = 1) {
-    return (SMEM_LIMIT - fixed_bytes(kb, limbs)) / ring_stage_bytes(limbs, cl) > (pair_mma(limbs, cl) ? 12 : 6)
-               ? (pair_mma(limbs, cl) ? 12 : 6)
-               : (SMEM_LIMIT - fixed_bytes(kb, limbs)) / ring_stage_bytes(limbs, cl);
+__host__ __device__ constexpr int stages_for(int kb, int limbs, int cl = 1, int pm = 0) {
+    return (SMEM_LIMIT - fixed_bytes(kb, limbs)) / ring_stage_bytes(limbs, cl, pm) > (pair_mma(limbs, cl, pm) ? 12 : 6)
+               ? (pair_mma(limbs, cl, pm) ? 12 : 6)
+               : (SMEM_LIMIT - fixed_bytes(kb, limbs)) / ring_stage_bytes(limbs, cl, pm);
 }
 
-__host__ __device__ constexpr size_t smem_bytes(int kb, int limbs, int cl = 1) {
-    return (size_t)fixed_bytes(kb, limbs) + (size_t)stages_for(kb, limbs, cl) * ring_stage_bytes(limbs, cl);
+__host__ __device__ constexpr size_t smem_bytes(int kb, int limbs, int cl = 1, int pm = 0) {
+    return (size_t)fixed_bytes(kb, limbs) + (size_t)stages_for(kb, limbs, cl, pm) * ring_stage_bytes(limbs, cl, pm);
 }
 
 // ---------------------------------------------------------------------------
@@ -597,13 +599,13 @@ __device__ __forceinline__ void certify_window(const TopK<K>& t, const float* __
 // CL = 2: the CTA pair of a cluster shares one P stream (each CTA's producer
 // fetches half of every stage and multicasts it to both), halving the L2->SM
 // traffic; the pair runs its rounds in step.
-template <int KB, int NW, int LIMBS, int MODE, int CL>
+template <int KB, int NW, int LIMBS, int MODE, int CL, int PM = 0>
 __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params prm) {
-    constexpr int STAGES = stages_for(KB, LIMBS, CL);
+    constexpr int STAGES = stages_for(KB, LIMBS, CL, PM);
     constexpr bool PROF = MODE == 2;
     constexpr bool I8 = LIMBS == 0;                  // int8 screen (see the header comment)
-    constexpr bool PAIR = pair_mma(LIMBS, CL);       // cta_group::2 MMAs issued by the pair's rank 0
-    constexpr int RSB = ring_stage_bytes(LIMBS, CL); // bytes of one ring stage in this CTA
+    constexpr bool PAIR = pair_mma(LIMBS, CL, PM);   // cta_group::2 MMAs issued by the pair's rank 0
+    constexpr int RSB = ring_stage_bytes(LIMBS, CL, PM);   // bytes of one ring stage in this CTA
     constexpr int KT = I8 ? TOPK_I8 : TOPK;          // candidates tracked per row
     // SUBS = 2 would issue every 256-pattern tile as two N = 128 sub-tiles into
     // four 128-column accumulators (MMAs up to two tiles ahead of the

@@ -57,20 +57,21 @@ static int tc_build8(TcPatterns& t, const uint32_t* bits, int np, int n, int nw)
     }
     if (np > (1 << tc::KEY_IBITS) || 127 * wmax >= tc::KEY_BIAS) return 0;   // int8 screen unavailable
     const int kb = n / 128;
-    const int ntiles = (np + tc::NT_COLS - 1) / tc::NT_COLS;
-    const size_t bytes = (size_t)ntiles * kb * tc::B_STAGE_BYTES;
+    const int ntiles = (np + tc::I8_TILE - 1) / tc::I8_TILE;
+    const size_t bytes = (size_t)ntiles * kb * tc::I8_STAGE_BYTES;
     std::vector<uint8_t> img(bytes, 0);
     for (int p = 0; p < np; p++) {
-        const int j = p / tc::NT_COLS, r = p % tc::NT_COLS;
+        const int j = p / tc::I8_TILE, r = p % tc::I8_TILE;
         for (int i = 0; i < n; i++) {
             if (!((bits[(size_t)p * nw + (i >> 5)] >> (i & 31)) & 1u)) continue;
             const int k = i / 128, col = i % 128;
-            img[((size_t)j * kb + k) * tc::B_STAGE_BYTES + tc::sw128_chunk(r, col >> 4) + (col & 15)] = 1;
+            img[((size_t)j * kb + k) * tc::I8_STAGE_BYTES + tc::sw128_chunk(r, col >> 4) + (col & 15)] = 1;
         }
     }
     if (cudaMalloc(&t.tiles8, bytes) != cudaSuccess) return -1;
     if (cudaMemcpy(t.tiles8, img.data(), bytes, cudaMemcpyHostToDevice) != cudaSuccess) return -1;
     t.kb8 = kb;
+    t.ntiles8 = ntiles;
     t.ready8 = true;
     return 0;
 }
@@ -101,7 +102,7 @@ template <int KB, int NW, int LIMBS, int MODE, int CL = 1, int PM = 0>
 static int tc_launch_t(const TcPatterns& t, int n, int nw, int A, int T, const float* y, S2Dev s2, PatDev P,
                        int num_sms, cudaStream_t st) {
     tc::Params prm;
-    prm.n = n; prm.nw = nw; prm.A = A; prm.T = T; prm.np = t.np; prm.ntiles = t.ntiles;
+    prm.n = n; prm.nw = nw; prm.A = A; prm.T = T; prm.np = t.np; prm.ntiles = LIMBS == 0 ? t.ntiles8 : t.ntiles;
     prm.y = y; prm.s2 = s2; prm.pbits = P.bits; prm.btiles = LIMBS == 0 ? t.tiles8 : t.tiles; prm.tie_rel = 1e-5f;
     prm.err = 2e-3f;
     prm.experiment = tc_experiment();

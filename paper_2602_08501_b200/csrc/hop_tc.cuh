@@ -57,6 +57,16 @@ static_assert(TOPK <= 8, "top-K hand-over uses 16 TMEM columns");
 #define MPW_TC_TOPK_I8 16
 #endif
 constexpr int TOPK_I8 = MPW_TC_TOPK_I8;   // int8 screen: keys per row (window overflow -> continuation pass)
+// int8 screen tile width: 256 patterns, two s32 accumulators.  160 (three
+// accumulators, MMAs up to two tiles ahead of the slowest epilogue warp) is
+// supported and correct but measured slower (144.5 vs 112.5 ms at cfg4: the
+// MMA issue loop's per-tile barrier waits, not the MMA rate, set the tile time)
+#ifndef MPW_TC_I8_TILE
+#define MPW_TC_I8_TILE 256
+#endif
+constexpr int I8_TILE = MPW_TC_I8_TILE;
+static_assert(I8_TILE % 32 == 0 && I8_TILE <= 256 && 2 * I8_TILE <= 512, "int8 tile width");
+constexpr int I8_STAGE_BYTES = I8_TILE * 128;   // one K-block (128 int8 positions) of a tile
 static_assert(TOPK_I8 <= 16, "int8 top-K hand-over uses 16 TMEM columns");
 constexpr int TRACE_W = 18, TRACE_TILES = 1 << 16;
 // prefetched stage-2 work items per CTA (int8: 32, its smem holds the rows' shared minima)
@@ -89,12 +99,16 @@ __host__ __device__ constexpr int fixed_bytes(int kb, int limbs) {
 // (pm: the pair-MMA variant, int8 with CL = 2 only; CL = 2 without it shares
 // the P stream of the pair by multicast copies, each CTA issuing its own MMAs)
 __host__ __device__ constexpr bool pair_mma(int limbs, int cl, int pm) { return pm && limbs == 0 && cl == 2; }
+__host__ __device__ constexpr int tile_stage_bytes(int limbs) { return limbs == 0 ? I8_STAGE_BYTES : B_STAGE_BYTES; }
 __host__ __device__ constexpr int ring_stage_bytes(int limbs, int cl, int pm) {
-    return pair_mma(limbs, cl, pm) ? B_STAGE_BYTES / 2 : B_STAGE_BYTES;
+    return pair_mma(limbs, cl, pm) ? tile_stage_bytes(limbs) / 2 : tile_stage_bytes(limbs);
+}
+__host__ __device__ constexpr int stage_cap(int limbs, int cl, int pm) {
+    return pair_mma(limbs, cl, pm) ? 12 : limbs == 0 ? 10 : 6;
 }
 __host__ __device__ constexpr int stages_for(int kb, int limbs, int cl = 1, int pm = 0) {
-    return (SMEM_LIMIT - fixed_bytes(kb, limbs)) / ring_stage_bytes(limbs, cl, pm) > (pair_mma(limbs, cl, pm) ? 12 : 6)
-               ? (pair_mma(limbs, cl, pm) ? 12 : 6)
+    return (SMEM_LIMIT - fixed_bytes(kb, limbs)) / ring_stage_bytes(limbs, cl, pm) > stage_cap(limbs, cl, pm)
+               ? stage_cap(limbs, cl, pm)
                : (SMEM_LIMIT - fixed_bytes(kb, limbs)) / ring_stage_bytes(limbs, cl, pm);
 }
 
@@ -279,6 +293,13 @@ __device__ __forceinline__ int epi_bar_or(int pred) {
           "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),        \
           "=r"(v[29]), "=r"(v[30]), "=r"(v[31])                                                             \
         : "r"(taddr))
+
+// 16 s32 columns -> 8 registers of s16x2
+#define TC_LD8P(taddr, v)                                                                                   \
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.pack::16b.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"         \
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),      \
+                   "=r"(v[7])                                                                               \
+                 : "r"(taddr))
 
 #define TC_LD16(taddr, v)                                                                                   \
     asm volatile(                                                                                           \
@@ -612,8 +633,9 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
     // epilogue); measured slower for int8 (N = 128 instructions run at ~64 % of
     // the N = 256 rate), so every variant uses one N = 256 tile, two accumulators
     constexpr int SUBS = 1;
-    constexpr int TW = NT_COLS / SUBS;               // accumulator columns per sub-tile
-    constexpr int NBUF = 2 * SUBS;                   // accumulators (NBUF x TW = 512 columns)
+    constexpr int TW = I8 ? I8_TILE : NT_COLS / SUBS;   // accumulator columns per (sub-)tile
+    constexpr int NBUF = I8 ? 512 / I8_TILE : 2 * SUBS; // accumulators (NBUF x TW <= 512 columns)
+    constexpr int STB = tile_stage_bytes(LIMBS);     // bytes of one K-block of a tile
     constexpr int EW = epi_warps(LIMBS);             // epilogue warps
     constexpr int EPI_T = 32 * EW;
     constexpr int WC = TW * 4 / EW;                  // accumulator columns per epilogue warp
@@ -715,11 +737,11 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
                             // this CTA's half of the stage (patterns 128 crank .. +127) into its own ring
                             mbar_expect_tx(fb, RSB);
                             bulk_g2s(smem_u32(b_ring + stage * RSB),
-                                     prm.btiles + ((size_t)j * KB + kb) * B_STAGE_BYTES + crank * RSB, RSB, fb);
+                                     prm.btiles + ((size_t)j * KB + kb) * STB + crank * RSB, RSB, fb);
                         } else if (PROF && (xp & 256) && round > 0) {
                             // profiling only (results wrong): no P traffic after the first round
                             mbar_arrive(fb);
-                        } else if (PROF && (xp & 1024)) {
+                        } else if (PROF && (xp & 1024) && !I8) {
                             // profiling only: every P tile fetched twice (doubles the L2->SM stream)
                             mbar_expect_tx(fb, 2 * B_STAGE_BYTES);
                             bulk_g2s(smem_u32(b_ring + stage * B_STAGE_BYTES),
@@ -728,15 +750,14 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
                                      prm.btiles + ((size_t)j * KB + kb) * B_STAGE_BYTES, B_STAGE_BYTES, fb);
                         } else if (CL > 1) {
                             // this CTA's share of the stage, delivered to every CTA of the pair
-                            constexpr uint32_t PART = B_STAGE_BYTES / CL;
-                            mbar_expect_tx(fb, B_STAGE_BYTES);
-                            bulk_g2s_mc(smem_u32(b_ring + stage * B_STAGE_BYTES) + crank * PART,
-                                        prm.btiles + ((size_t)j * KB + kb) * B_STAGE_BYTES + crank * PART, PART, fb,
+                            constexpr uint32_t PART = STB / CL;
+                            mbar_expect_tx(fb, STB);
+                            bulk_g2s_mc(smem_u32(b_ring + stage * STB) + crank * PART,
+                                        prm.btiles + ((size_t)j * KB + kb) * STB + crank * PART, PART, fb,
                                         CMASK);
                         } else {
-                            mbar_expect_tx(fb, B_STAGE_BYTES);
-                            bulk_g2s(smem_u32(b_ring + stage * B_STAGE_BYTES),
-                                     prm.btiles + ((size_t)j * KB + kb) * B_STAGE_BYTES, B_STAGE_BYTES, fb);
+                            mbar_expect_tx(fb, STB);
+                            bulk_g2s(smem_u32(b_ring + stage * STB), prm.btiles + ((size_t)j * KB + kb) * STB, STB, fb);
                         }
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
                     }
@@ -840,7 +861,8 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
         const bool primary = warp < 6;
         const int grp = (warp - 2) >> 2;         // column group: 0 = primary, 1.. = secondary
         const int sec = threadIdx.x - 64 - 128;  // secondary thread index (the pool uses 0..POOL-1)
-        const int ch0 = grp * (WC / 32);         // first 32-column chunk of this warp's columns
+        const int col0 = grp * WC;               // first accumulator column of this warp
+        const int ch0 = col0 / 32;               // ... as a 32-column chunk (f16 screens: WC % 32 == 0)
         const uint32_t t_lane = tmem_base + ((uint32_t)(g * 32) << 16);
         const int count = *prm.s2.count;
         const int ntraj = count * A;
@@ -1153,7 +1175,7 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
                         bulk_g2s(smem_u32(b_ring + (size_t)(ROWS + row) * YP), prm.y + (size_t)xf * n, YB,
                                  smem_u32(&ybar[0]));
                 }
-                const int pbase = j * NT_COLS + h * TW;
+                const int pbase = (j * SUBS + h) * TW;
                 const bool tail = pbase + TW > np_;
                 // slow path (rare per lane once the running best settles): values
                 // below the threshold are inserted in increasing index order (ties
@@ -1223,7 +1245,7 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
                 // two 32-column chunks per step: both TMEM loads in flight together,
                 // then two interleaved min trees
                 constexpr int NCH = WC / 32;
-                const uint32_t tbase = t_lane + buf * TW + ch0 * 32;
+                const uint32_t tbase = t_lane + buf * TW + col0;
                 uint32_t va[32], vb[32];
                 // the accumulator is handed back to the MMA issuer as soon as the
                 // warp's last TMEM loads complete; the scan of the registers then
@@ -1237,36 +1259,82 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
                     }
                 };
                 if constexpr (I8) {
-                    // the warp's TW/2 columns as packed s16 scores (64 per load), one wait
+                    // the warp's WC columns as packed s16 scores: 64 per x32 load (va,
+                    // vb), a 16-column remainder by an x8 load (vc); one wait
                     constexpr int NLD = WC / 64;
+                    constexpr int REM = WC % 64;
+                    static_assert(REM == 0 || REM == 16, "int8 epilogue column split");
+                    uint32_t vc[8];
                     if (PROF && (xp & 2)) {
 #pragma unroll
                         for (int e = 0; e < 32; e++) { va[e] = 0x7FFF7FFFu; vb[e] = va[e]; }
+#pragma unroll
+                        for (int e = 0; e < 8; e++) vc[e] = 0x7FFF7FFFu;
                     } else {
                         TC_LD32P(tbase, va);
                         if constexpr (NLD == 2) TC_LD32P(tbase + 64, vb);
+                        if constexpr (REM == 16) TC_LD8P(tbase + 64 * NLD, vc);
                         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                     }
                     release();   // every column of this warp is in registers
-                    const int pa = pbase + ch0 * 32;
+                    const int pa = pbase + col0;
                     if (tail) {
+                        auto mask = [&](uint32_t& r, int p) {   // s16 max past |P|
+                            if (p >= np_) r = (r & 0xFFFF0000u) | 0x7FFFu;
+                            if (p + 1 >= np_) r = (r & 0xFFFFu) | 0x7FFF0000u;
+                        };
 #pragma unroll
                         for (int e = 0; e < 32; e++) {
-                            if (pa + 2 * e >= np_) va[e] = (va[e] & 0xFFFF0000u) | 0x7FFFu;   // s16 max
-                            if (pa + 2 * e + 1 >= np_) va[e] = (va[e] & 0xFFFFu) | 0x7FFF0000u;
-                            if (pa + 64 + 2 * e >= np_) vb[e] = (vb[e] & 0xFFFF0000u) | 0x7FFFu;
-                            if (pa + 64 + 2 * e + 1 >= np_) vb[e] = (vb[e] & 0xFFFFu) | 0x7FFF0000u;
+                            mask(va[e], pa + 2 * e);
+                            if (NLD == 2) mask(vb[e], pa + 64 + 2 * e);
                         }
+#pragma unroll
+                        for (int e = 0; e < 8; e++)
+                            if (REM == 16) mask(vc[e], pa + 64 * NLD + 2 * e);
                     }
                     if (!(PROF && (xp & 1))) {
                         uint32_t ga[11], gb[11];
                         const int ma = min64_s16(va, ga);
                         const int mb = NLD == 2 ? min64_s16(vb, gb) : 0x7FFF;
+                        int mc = 0x7FFF;
+                        if constexpr (REM == 16) {
+                            uint32_t m2 = min3_s16x2(vc[0], vc[1], vc[2]);
+                            m2 = min3_s16x2(m2, vc[3], vc[4]);
+                            m2 = min3_s16x2(m2, vc[5], vc[6]);
+                            uint32_t r;
+                            asm("min.s16x2 %0, %1, %2;" : "=r"(r) : "r"(m2), "r"(vc[7]));
+                            mc = min((int)(short)(r & 0xFFFFu), (int)(short)(r >> 16));
+                        }
                         if (PROF && (xp & 16)) {
-                            if (ma == -12345 || mb == -12345) tk.k[0] = 0u;
+                            if (ma == -12345 || mb == -12345 || mc == -12345) tk.k[0] = 0u;
                         } else {
                             if (ma < lastq) slow8(va, ga, pa, ma);
                             if (NLD == 2 && mb < lastq) slow8(vb, gb, pa + 64, mb);
+                            if (REM == 16 && mc < lastq) {
+                                // 16 values: one hit mask, a 3-level register select per hit
+                                const int lim = min(lastq, mc + wq);
+                                uint32_t hm = 0;
+#pragma unroll
+                                for (int e = 0; e < 8; e++) {
+                                    hm |= ((int)(short)(vc[e] & 0xFFFFu) < lim ? 1u : 0u) << (2 * e);
+                                    hm |= ((int)(short)(vc[e] >> 16) < lim ? 1u : 0u) << (2 * e + 1);
+                                }
+                                while (hm) {
+                                    const int h = __ffs(hm) - 1;
+                                    hm &= hm - 1;
+                                    const int e = h >> 1;
+                                    const uint32_t r01 = (e & 1) ? vc[1] : vc[0], r23 = (e & 1) ? vc[3] : vc[2];
+                                    const uint32_t r45 = (e & 1) ? vc[5] : vc[4], r67 = (e & 1) ? vc[7] : vc[6];
+                                    const uint32_t rl = (e & 2) ? r23 : r01, rh = (e & 2) ? r67 : r45;
+                                    const uint32_t r = (e & 4) ? rh : rl;
+                                    const int sv = (h & 1) ? (int)(short)(r >> 16) : (int)(short)(r & 0xFFFFu);
+                                    const uint32_t key = make_key(sv, pa + 64 * NLD + h);
+                                    if (key < tk.k[KT - 1] && key > kfl && sv < wbase() + wq) {
+                                        tk.insert_inline(key);
+                                        upd_lastq();
+                                    }
+                                }
+                            }
                         }
                     }
                 }

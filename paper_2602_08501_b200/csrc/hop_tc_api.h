@@ -10,10 +10,10 @@ struct TcPatterns {
     bool ready = false;
     uint8_t* tiles = nullptr;
     int np = 0, ntiles = 0, kb = 0;
-    // int8 screen (N = 128, 256): u8 0/1 images [ntiles][N/128][256 x 128] in the SW128 layout
+    // int8 screen (N = 128, 256): u8 0/1 images [ntiles8][N/128][I8_TILE x 128] in the SW128 layout
     bool ready8 = false;
     uint8_t* tiles8 = nullptr;
-    int kb8 = 0;
+    int kb8 = 0, ntiles8 = 0;   // int8 tiles are tc::I8_TILE patterns wide
 };
 
 bool tc_supported(int n, int np);

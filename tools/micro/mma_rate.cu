@@ -14,17 +14,24 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t addr) {
            ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
 
-template <int KIND, int N, bool ATMEM, int RING = 1>   // KIND 0 = i8, 1 = f16; RING: B stages cycled
+// SYNC: per 4 instructions (one K-block) the hop kernel's bookkeeping -- an
+// mbarrier try_wait (on a completed phase), tcgen05.fence::after_thread_sync,
+// and a tcgen05.commit to a stage barrier
+template <int KIND, int N, bool ATMEM, int RING = 1, int SYNC = 0, int GRP = 4, int NW_ = 1, int NC_ = 1>
 __global__ void __launch_bounds__(128, 1) mma_rate(int iters, unsigned long long* out) {
     extern __shared__ __align__(1024) unsigned char sm[];
     __shared__ uint32_t slot;
     __shared__ __align__(8) uint64_t bar;
+    __shared__ __align__(8) uint64_t done_bar, sink_bar;
     unsigned char* a = sm;            // 2 x 16 KB (two K-blocks)
     unsigned char* b = sm + 32768;    // RING x 32 KB
     const int warp = threadIdx.x >> 5;
     for (int i = threadIdx.x; i < (32768 + RING * 32768) / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0x01010101u * (i & 3);
     if (threadIdx.x == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&done_bar)));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1000000;" ::"r"(smem_u32(&sink_bar)));
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&done_bar)) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 0) {
@@ -44,6 +51,32 @@ __global__ void __launch_bounds__(128, 1) mma_rate(int iters, unsigned long long
         long long t0 = clock64();
         for (int it = 0; it < iters; it++) {
             const int ks = it & 3;
+            if ((SYNC & 8) && ks == 0) {   // plain shared-memory flag poll instead of an mbarrier
+                volatile uint32_t* fl = reinterpret_cast<volatile uint32_t*>(&slot);
+                while (*fl == 0xFFFFFFFFu) {}
+            }
+            if ((SYNC & 16) && ks == 0) {  // mbarrier.test_wait
+                uint32_t ok = 0;
+                while (!ok)
+                    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                                 : "=r"(ok) : "r"(smem_u32(&done_bar)), "r"(0) : "memory");
+            }
+            if ((SYNC & 32) && (it % GRP) == 0) {   // NW_ try_waits + fence per group
+                for (int w = 0; w < NW_; w++) {
+                    uint32_t ok = 0;
+                    while (!ok)
+                        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                                     : "=r"(ok) : "r"(smem_u32(&done_bar)), "r"(0) : "memory");
+                }
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            }
+            if ((SYNC & 1) && ks == 0) {
+                uint32_t ok = 0;
+                while (!ok)
+                    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                                 : "=r"(ok) : "r"(smem_u32(&done_bar)), "r"(0) : "memory");
+            }
+            if ((SYNC & 2) && ks == 0) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const int kb = (it >> 2) & 1;                 // A K-block
             const int stg = (it >> 2) % RING;             // B ring stage
             const uint64_t adk = ad + (uint64_t)(kb * 16384 >> 4), bdk = bd + (uint64_t)(stg * 32768 >> 4);
@@ -61,6 +94,13 @@ __global__ void __launch_bounds__(128, 1) mma_rate(int iters, unsigned long long
                              "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
                              ::"r"(d), "l"(adk + 2 * ks), "l"(bdk + 2 * ks), "r"(idesc), "r"(it));
             }
+            if ((SYNC & 32) && (it % GRP) == GRP - 1)
+                for (int c = 0; c < NC_; c++)
+                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                                 ::"r"(smem_u32(&sink_bar)) : "memory");
+            if ((SYNC & 4) && ks == 3)
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                             ::"r"(smem_u32(&sink_bar)) : "memory");
         }
         // one commit after the last instruction tracks the completion of all of them
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
@@ -79,9 +119,9 @@ __global__ void __launch_bounds__(128, 1) mma_rate(int iters, unsigned long long
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(slot));
 }
 
-template <int KIND, int N, bool ATMEM, int RING = 1>
+template <int KIND, int N, bool ATMEM, int RING = 1, int SYNC = 0, int GRP = 4, int NW_ = 1, int NC_ = 1>
 void run(const char* name, unsigned long long* d) {
-    auto k = mma_rate<KIND, N, ATMEM, RING>;
+    auto k = mma_rate<KIND, N, ATMEM, RING, SYNC, GRP, NW_, NC_>;
     const int smem = 32768 + RING * 32768 + 1024;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     const int iters = 8 * 4096;
@@ -109,5 +149,16 @@ int main() {
     run<0, 256, false, 6>("i8 N256 A smem ring6", d);
     run<0, 256, true, 6>("i8 N256 A tmem ring6", d);
     run<1, 256, false, 5>("f16 N256 A smem ring5", d);
+    run<0, 256, false, 6, 32, 8, 3, 3>("i8 N256 per 8: 3 waits 3 commits", d);
+    run<0, 256, false, 6, 32, 8, 1, 1>("i8 N256 per 8: 1 wait 1 commit", d);
+    run<0, 256, false, 6, 32, 8, 1, 2>("i8 N256 per 8: 1 wait 2 commits", d);
+    run<0, 256, false, 6, 32, 16, 1, 1>("i8 N256 per 16: 1 wait 1 commit", d);
+    run<0, 160, false, 6, 32, 8, 1, 1>("i8 N160 per 8: 1 wait 1 commit", d);
+    run<0, 256, false, 6, 7>("i8 N256 wait+fence+commit", d);
+    run<0, 256, false, 6, 1>("i8 N256 try_wait", d);
+    run<0, 256, false, 6, 16>("i8 N256 test_wait", d);
+    run<0, 256, false, 6, 8>("i8 N256 lds poll", d);
+    run<0, 256, true, 6, 1>("i8 N256 Atmem try_wait", d);
+    run<0, 256, false, 6, 12>("i8 N256 lds poll+commit", d);
     return 0;
 }

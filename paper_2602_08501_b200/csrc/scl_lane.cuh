@@ -10,7 +10,7 @@
 //
 // Shared memory per frame:
 //   llr0[N]            channel LLRs (2y/sigma^2)
-//   llr[L][N-1]        per-path instances of levels 1..M (lazy clone via ptr)
+//   llr[L][INST]       per-path instances of stored levels 3..RL-1 (lazy clone via ptr)
 //   ps[L][NW+1]        partial-sum bits (row padded against bank conflicts)
 //   u[L][NW+1]         leaf decisions
 //   ptr[L][PTRW]       instance index per level (bytes)
@@ -30,9 +30,15 @@ struct SclLane {
     static constexpr int M = (N >= 256) ? 8 : (N >= 128) ? 7 : (N >= 64) ? 6 : (N >= 32) ? 5 : (N >= 16) ? 4 : (N >= 8) ? 3 : (N >= 4) ? 2 : 1;
     static constexpr int NW = N >= 32 ? N / 32 : 1;
     static constexpr int NWP = NW + 1;
-    static constexpr int PTRW = 5;                       // 20 bytes: levels 0..19
+    static constexpr int PTRW = 1;                       // 4 bytes: instance index of shared levels 0..3
     static constexpr int FPW = 32 / L;
-    static constexpr int INST = N / 4 - 1;               // stored doubles per instance (levels 3..M)
+    // Levels of at most 16 values (RL..M) live in registers, one copy per lane
+    // (= per path); a clone copies the source path's pending register levels
+    // with shuffles.  Levels SCL_VIRT+1 .. RL-1 are stored per path instance in
+    // shared memory (N = 256: level 3 only; N <= 128: none).
+    static constexpr int RL = (M - 4 > SCL_VIRT + 1) ? M - 4 : SCL_VIRT + 1;
+    static constexpr int INST = N / 4 - 2 * (N >> RL);   // stored doubles per instance (levels 3..RL-1)
+    static constexpr int RT = 2 * (N >> RL) - 1;         // register doubles (levels RL..M)
     static constexpr size_t LLR0 = 0;
     static constexpr size_t LLR = LLR0 + 8 * (size_t)N;
     static constexpr size_t PS = LLR + 8 * (size_t)L * INST;
@@ -43,8 +49,10 @@ struct SclLane {
     static constexpr size_t SBIT = SSRC + 4 * (size_t)L;
     static constexpr size_t CAND = (SBIT + 4 * (size_t)L + 15) & ~(size_t)15;   // (pm, pm+|dm|) per path
     static constexpr size_t TOTAL = CAND + 16 * (size_t)L;
-    // offset of stored level lvl (3..M) inside an instance
+    // offset of stored level lvl (3..RL-1) inside an instance
     __host__ __device__ static constexpr int off(int lvl) { return N / 4 - 2 * (N >> (lvl > 0 ? lvl : 0)); }
+    // offset of register level lvl (RL..M) inside the lane's register array
+    __host__ __device__ static constexpr int roff(int lvl) { return 2 * (N >> RL) - 2 * (N >> lvl); }
 };
 
 // ---- node kernels with compile-time HALF (one lane = one path)
@@ -120,17 +128,60 @@ __device__ __forceinline__ void lane_node_d2(bool is_g, int n2, const double* __
     }
 }
 
+// One SC node at depth D (writes level D+1), the left (f) or right (g) child.
+// Parent values come from the virtual level 2, a stored instance (via the
+// path's instance pointer) or the lane's registers; the child goes to the
+// path's own instance or to registers.  Same IEEE operations in every case.
+template <int N, int L, int D>
+__device__ __forceinline__ void lane_step(bool is_g, double (&r)[SclLane<N, L>::RT], const double* __restrict__ llr,
+                                          double* __restrict__ myllr, uint8_t* ptrrow,
+                                          const double* __restrict__ llr0, const uint32_t* __restrict__ psrow,
+                                          int n2, int lo, int l) {
+    using Lay = SclLane<N, L>;
+    constexpr int RL = Lay::RL, HALF = N >> (D + 1);
+    if constexpr (D < SCL_VIRT || D >= Lay::M) {
+        return;                                                   // virtual child: nothing to do
+    } else if constexpr (D + 1 < RL) {
+        // shared -> shared
+        if constexpr (D == SCL_VIRT) {
+            lane_node_d2<N>(is_g, n2, llr0, psrow, myllr + Lay::off(3), lo);
+        } else {
+            const double* par = llr + (size_t)ptrrow[D] * Lay::INST + Lay::off(D);
+            if (is_g) lane_g<HALF>(par, myllr + Lay::off(D + 1), psrow, lo);
+            else lane_f<HALF>(par, myllr + Lay::off(D + 1));
+        }
+        ptrrow[D + 1] = (uint8_t)l;
+        __syncwarp();
+    } else {
+        static_assert(HALF <= 16, "register levels hold at most 16 values");
+        const uint32_t word = is_g ? (psrow[lo >> 5] >> (lo & 31)) : 0u;
+        const double* par = nullptr;
+        if constexpr (D > SCL_VIRT && D < RL) par = llr + (size_t)ptrrow[D] * Lay::INST + Lay::off(D);
+#pragma unroll
+        for (int j = 0; j < HALF; j++) {
+            double a, c;
+            if constexpr (D == SCL_VIRT) {
+                a = lv2<N>(llr0, psrow, n2, j);
+                c = lv2<N>(llr0, psrow, n2, j + HALF);
+            } else if constexpr (D < RL) {
+                a = par[j];
+                c = par[j + HALF];
+            } else {
+                a = r[Lay::roff(D) + j];
+                c = r[Lay::roff(D) + j + HALF];
+            }
+            r[Lay::roff(D + 1) + j] = is_g ? c + (((word >> j) & 1u) ? -a : a) : scl_f(a, c);
+        }
+    }
+}
+
 template <int N, int L>
-__device__ __forceinline__ void lane_node(int d, bool is_g, const double* par, double* o,
-                                          const uint32_t* psrow, int lo) {
-    // dispatch on depth so HALF = N >> (d+1) is a compile-time constant
-#define MPW_LANE_CASE(DD)                                                        \
-    case DD:                                                                     \
-        if constexpr ((N >> (DD + 1)) >= 1) {                                   \
-            if (is_g) lane_g<(N >> (DD + 1))>(par, o, psrow, lo);               \
-            else lane_f<(N >> (DD + 1))>(par, o);                               \
-        }                                                                        \
-        break;
+__device__ __forceinline__ void lane_node(int d, bool is_g, double (&r)[SclLane<N, L>::RT], const double* llr,
+                                          double* myllr, uint8_t* ptrrow, const double* llr0,
+                                          const uint32_t* psrow, int n2, int lo, int l) {
+    // dispatch on depth so HALF = N >> (d+1) and the register indices are constants
+#define MPW_LANE_CASE(DD) \
+    case DD: lane_step<N, L, DD>(is_g, r, llr, myllr, ptrrow, llr0, psrow, n2, lo, l); break;
     switch (d) {
         MPW_LANE_CASE(0) MPW_LANE_CASE(1) MPW_LANE_CASE(2) MPW_LANE_CASE(3)
         MPW_LANE_CASE(4) MPW_LANE_CASE(5) MPW_LANE_CASE(6) MPW_LANE_CASE(7)
@@ -139,8 +190,21 @@ __device__ __forceinline__ void lane_node(int d, bool is_g, const double* par, d
 #undef MPW_LANE_CASE
 }
 
+template <int N, int L, int LVL>
+__device__ __forceinline__ void clone_levels(double (&r)[SclLane<N, L>::RT], int phi, int srcl) {
+    using Lay = SclLane<N, L>;
+    if constexpr (LVL < Lay::M) {
+        if (!((phi >> (Lay::M - 1 - LVL)) & 1)) {
+#pragma unroll
+            for (int j = 0; j < (N >> LVL); j++)
+                r[Lay::roff(LVL) + j] = __shfl_sync(MPW_FULL, r[Lay::roff(LVL) + j], srcl);
+        }
+        clone_levels<N, L, LVL + 1>(r, phi, srcl);
+    }
+}
+
 template <int N, int L>
-__global__ void __launch_bounds__(128) scl_lane_kernel(CodeDev code, const float* __restrict__ y,
+__global__ void __launch_bounds__(128, 3) scl_lane_kernel(CodeDev code, const float* __restrict__ y,
                                                        const double* __restrict__ llr64, int F,
                                                        double sigma, int A, int mode, SclOut out,
                                                        S2Dev s2) {
@@ -179,6 +243,9 @@ __global__ void __launch_bounds__(128) scl_lane_kernel(CodeDev code, const float
 #pragma unroll
         for (int w = 0; w < NWP; w++) { psrow[w] = 0u; urow[w] = 0u; }
         double pm = (l == 0) ? 0.0 : CUDART_INF;
+        double r[Lay::RT];                  // register levels RL..M of this path
+#pragma unroll
+        for (int j = 0; j < Lay::RT; j++) r[j] = 0.0;
         __syncwarp();
 
         for (int phi = 0; phi < N; phi++) {
@@ -189,29 +256,12 @@ __global__ void __launch_bounds__(128) scl_lane_kernel(CodeDev code, const float
                 const int t = __ffs(phi) - 1;
                 const int d = M - 1 - t;
                 const int lo = (phi >> (M - d)) << (M - d);
-                if (d == SCL_VIRT) {
-                    lane_node_d2<N>(true, phi >> (M - 2), llr0, psrow, myllr + Lay::off(3), lo);
-                    ptrrow[3] = (uint8_t)l;
-                } else if (d > SCL_VIRT) {
-                    const double* par = llr + (size_t)ptrrow[d] * Lay::INST + Lay::off(d);
-                    lane_node<N, L>(d, true, par, myllr + Lay::off(d + 1), psrow, lo);
-                    ptrrow[d + 1] = (uint8_t)l;
-                }
-                __syncwarp();
+                lane_node<N, L>(d, true, r, llr, myllr, ptrrow, llr0, psrow, phi >> (M - 2), lo, l);
                 dstart = d + 1;
             }
-            for (int d = dstart > SCL_VIRT ? dstart : SCL_VIRT; d < M; d++) {
-                if (d == SCL_VIRT) {
-                    lane_node_d2<N>(false, phi >> (M - 2), llr0, psrow, myllr + Lay::off(3), 0);
-                    ptrrow[3] = (uint8_t)l;
-                } else {
-                    const double* par = llr + (size_t)ptrrow[d] * Lay::INST + Lay::off(d);
-                    lane_node<N, L>(d, false, par, myllr + Lay::off(d + 1), psrow, 0);
-                    ptrrow[d + 1] = (uint8_t)l;
-                }
-                __syncwarp();
-            }
-            const double dm = myllr[Lay::INST - 1];
+            for (int d = dstart > SCL_VIRT ? dstart : SCL_VIRT; d < M; d++)
+                lane_node<N, L>(d, false, r, llr, myllr, ptrrow, llr0, psrow, phi >> (M - 2), 0, l);
+            const double dm = r[Lay::roff(M)];
             const bool frozen = (code.frozen[phi >> 5] >> (phi & 31)) & 1u;
             if (frozen) {
                 pm = pm + fabs(dm) * (double)(dm < 0.0);                      // :216-218
@@ -239,6 +289,9 @@ __global__ void __launch_bounds__(128) scl_lane_kernel(CodeDev code, const float
                 const int src = sel_src[l];
                 const int bit = sel_bit[l];
                 pm = sel_val[l];
+                // register levels still to be read by a g node (this leaf is in the
+                // left subtree of the depth-lvl node) come from the source path
+                clone_levels<N, L, Lay::RL>(r, phi, g0 + src);
                 uint32_t rps[NW], ru[NW], rp[Lay::PTRW];
                 const uint32_t* sps = ps_all + src * NWP;
                 const uint32_t* su = u_all + src * NWP;

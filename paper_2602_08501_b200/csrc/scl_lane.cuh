@@ -12,9 +12,12 @@
 //   llr0[N]            channel LLRs (2y/sigma^2)
 //   llr[L][INST]       per-path instances of stored levels 3..RL-1 (lazy clone via ptr)
 //   ps[L][NW+1]        partial-sum bits (row padded against bank conflicts)
-//   u[L][NW+1]         leaf decisions
 //   ptr[L][PTRW]       instance index per level (bytes)
-//   sel_src/bit/val[L] info-leaf selection scratch
+//   sel[L]             info-leaf selection: source path | bit << 8 | flipped << 9
+//   cand[L]            (pm, pm + |dm|) of every path at an info leaf
+// The leaf decisions u are not stored: after the last leaf the partial sums
+// are combined up to the root, giving the codeword, and u = its polar
+// transform (the transform is an involution over GF(2)).
 #pragma once
 #include "common.cuh"
 #include "scl.cuh"
@@ -42,12 +45,9 @@ struct SclLane {
     static constexpr size_t LLR0 = 0;
     static constexpr size_t LLR = LLR0 + 8 * (size_t)N;
     static constexpr size_t PS = LLR + 8 * (size_t)L * INST;
-    static constexpr size_t U = PS + 4 * (size_t)L * NWP;
-    static constexpr size_t PTR = U + 4 * (size_t)L * NWP;
-    static constexpr size_t SVAL = (PTR + 4 * (size_t)L * PTRW + 7) & ~(size_t)7;
-    static constexpr size_t SSRC = SVAL + 8 * (size_t)L;
-    static constexpr size_t SBIT = SSRC + 4 * (size_t)L;
-    static constexpr size_t CAND = (SBIT + 4 * (size_t)L + 15) & ~(size_t)15;   // (pm, pm+|dm|) per path
+    static constexpr size_t PTR = PS + 4 * (size_t)L * NWP;
+    static constexpr size_t SEL = PTR + 4 * (size_t)L * PTRW;
+    static constexpr size_t CAND = (SEL + 4 * (size_t)L + 15) & ~(size_t)15;   // (pm, pm+|dm|) per path
     static constexpr size_t TOTAL = CAND + 16 * (size_t)L;
     // offset of stored level lvl (3..RL-1) inside an instance
     __host__ __device__ static constexpr int off(int lvl) { return N / 4 - 2 * (N >> (lvl > 0 ? lvl : 0)); }
@@ -204,7 +204,7 @@ __device__ __forceinline__ void clone_levels(double (&r)[SclLane<N, L>::RT], int
 }
 
 template <int N, int L>
-__global__ void __launch_bounds__(128, 3) scl_lane_kernel(CodeDev code, const float* __restrict__ y,
+__global__ void __launch_bounds__(128, 4) scl_lane_kernel(CodeDev code, const float* __restrict__ y,
                                                        const double* __restrict__ llr64, int F,
                                                        double sigma, int A, int mode, SclOut out,
                                                        S2Dev s2) {
@@ -218,14 +218,10 @@ __global__ void __launch_bounds__(128, 3) scl_lane_kernel(CodeDev code, const fl
     double* llr0 = reinterpret_cast<double*>(base + Lay::LLR0);
     double* llr = reinterpret_cast<double*>(base + Lay::LLR);
     uint32_t* ps_all = reinterpret_cast<uint32_t*>(base + Lay::PS);
-    uint32_t* u_all = reinterpret_cast<uint32_t*>(base + Lay::U);
     uint8_t* ptr_all = base + Lay::PTR;
-    double* sel_val = reinterpret_cast<double*>(base + Lay::SVAL);
-    int32_t* sel_src = reinterpret_cast<int32_t*>(base + Lay::SSRC);
-    int32_t* sel_bit = reinterpret_cast<int32_t*>(base + Lay::SBIT);
+    int32_t* sel = reinterpret_cast<int32_t*>(base + Lay::SEL);
     double2* cand = reinterpret_cast<double2*>(base + Lay::CAND);
     uint32_t* psrow = ps_all + l * NWP;
-    uint32_t* urow = u_all + l * NWP;
     uint8_t* ptrrow = ptr_all + l * Lay::PTRW * 4;
     double* myllr = llr + (size_t)l * Lay::INST;
     const double sig2 = sigma * sigma;
@@ -241,7 +237,7 @@ __global__ void __launch_bounds__(128, 3) scl_lane_kernel(CodeDev code, const fl
             llr0[i] = v;
         }
 #pragma unroll
-        for (int w = 0; w < NWP; w++) { psrow[w] = 0u; urow[w] = 0u; }
+        for (int w = 0; w < NWP; w++) psrow[w] = 0u;
         double pm = (l == 0) ? 0.0 : CUDART_INF;
         double r[Lay::RT];                  // register levels RL..M of this path
 #pragma unroll
@@ -283,38 +279,41 @@ __global__ void __launch_bounds__(128, 3) scl_lane_kernel(CodeDev code, const fl
                     rf += (fk < vf) || (fk == vf && k < l);
                 }
                 const int nat = dm < 0.0 ? 1 : 0;
-                if (rn < L) { sel_src[rn] = l; sel_bit[rn] = nat; sel_val[rn] = vn; }
-                if (rf < L) { sel_src[rf] = l; sel_bit[rf] = nat ^ 1; sel_val[rf] = vf; }
+                if (rn < L) sel[rn] = l | (nat << 8);
+                if (rf < L) sel[rf] = l | ((nat ^ 1) << 8) | (1 << 9);
                 __syncwarp();
-                const int src = sel_src[l];
-                const int bit = sel_bit[l];
-                pm = sel_val[l];
+                const int sl = sel[l];
+                const int src = sl & 0xFF;
+                const int bit = (sl >> 8) & 1;
+                {
+                    const double2 cs = cand[src];
+                    pm = (sl >> 9) ? cs.y : cs.x;
+                }
                 // register levels still to be read by a g node (this leaf is in the
                 // left subtree of the depth-lvl node) come from the source path
                 clone_levels<N, L, Lay::RL>(r, phi, g0 + src);
-                uint32_t rps[NW], ru[NW], rp[Lay::PTRW];
+                uint32_t rps[NW], rp[Lay::PTRW];
                 const uint32_t* sps = ps_all + src * NWP;
-                const uint32_t* su = u_all + src * NWP;
                 const uint32_t* sp = reinterpret_cast<const uint32_t*>(ptr_all + src * Lay::PTRW * 4);
 #pragma unroll
-                for (int w = 0; w < NW; w++) { rps[w] = sps[w]; ru[w] = su[w]; }
+                for (int w = 0; w < NW; w++) rps[w] = sps[w];
 #pragma unroll
                 for (int w = 0; w < Lay::PTRW; w++) rp[w] = sp[w];
                 __syncwarp();
                 if (bit) {
 #pragma unroll
                     for (int w = 0; w < NW; w++)
-                        if (w == (phi >> 5)) { rps[w] |= 1u << (phi & 31); ru[w] |= 1u << (phi & 31); }
+                        if (w == (phi >> 5)) rps[w] |= 1u << (phi & 31);
                 }
 #pragma unroll
-                for (int w = 0; w < NW; w++) { psrow[w] = rps[w]; urow[w] = ru[w]; }
+                for (int w = 0; w < NW; w++) psrow[w] = rps[w];
                 uint32_t* mp = reinterpret_cast<uint32_t*>(ptrrow);
 #pragma unroll
                 for (int w = 0; w < Lay::PTRW; w++) mp[w] = rp[w];
                 __syncwarp();
             }
-            if (phi == N - 1) break;
-            const int c = __ffs(~phi) - 1;                                      // :253-259
+            // combine (:253-259); after the last leaf it runs up to the root
+            const int c = __ffs(~phi) - 1;
             for (int d = M - 1; d >= M - c; d--) {
                 const int half = N >> (d + 1);
                 const int lo = (phi >> (M - d)) << (M - d);
@@ -341,8 +340,11 @@ __global__ void __launch_bounds__(128, 3) scl_lane_kernel(CodeDev code, const fl
         const int cnt = __popc(finmask);
         uint32_t cw[NW], uu[NW];
 #pragma unroll
-        for (int w = 0; w < NW; w++) { uu[w] = urow[w]; cw[w] = uu[w]; }
-        polar_transform_words<NW>(cw, NW);
+        for (int w = 0; w < NW; w++) { cw[w] = psrow[w]; uu[w] = cw[w]; }
+        polar_transform_words<NW>(uu, NW);
+        // own partial-sum row := u, read bit by bit by the CRC gate below
+#pragma unroll
+        for (int w = 0; w < NW; w++) psrow[w] = uu[w];
 
         if (mode == 0) {
             if (valid) {
@@ -366,7 +368,7 @@ __global__ void __launch_bounds__(128, 3) scl_lane_kernel(CodeDev code, const fl
         if (code.is_ca) {
             for (int j = 0; j < code.kp; j++) {
                 const int pos = code.info[j];
-                v |= (uint64_t)((urow[pos >> 5] >> (pos & 31)) & 1u) << j;
+                v |= (uint64_t)((psrow[pos >> 5] >> (pos & 31)) & 1u) << j;
             }
         }
         int gwin = 1 << 30;                 // lowest CRC-valid rank in this frame group

@@ -247,16 +247,16 @@ __global__ void __launch_bounds__(128, 4) scl_lane_kernel(CodeDev code, const fl
         for (int phi = 0; phi < N; phi++) {
             // descent to leaf phi: one g at depth M-1-ctz(phi), then f's.  Nodes
             // whose child level is virtual (depth < SCL_VIRT) need no work.
-            int dstart = 0;
+            // descent to leaf phi: one g at depth M-1-ctz(phi), then f's (one call
+            // site, so the unrolled node bodies exist once in the binary)
+            int d0 = SCL_VIRT, lo = 0;
             if (phi) {
-                const int t = __ffs(phi) - 1;
-                const int d = M - 1 - t;
-                const int lo = (phi >> (M - d)) << (M - d);
-                lane_node<N, L>(d, true, r, llr, myllr, ptrrow, llr0, psrow, phi >> (M - 2), lo, l);
-                dstart = d + 1;
+                d0 = M - __ffs(phi);
+                lo = (phi >> (M - d0)) << (M - d0);
             }
-            for (int d = dstart > SCL_VIRT ? dstart : SCL_VIRT; d < M; d++)
-                lane_node<N, L>(d, false, r, llr, myllr, ptrrow, llr0, psrow, phi >> (M - 2), 0, l);
+            for (int d = d0; d < M; d++)
+                lane_node<N, L>(d, phi && d == d0, r, llr, myllr, ptrrow, llr0, psrow, phi >> (M - 2),
+                                d == d0 ? lo : 0, l);
             const double dm = r[Lay::roff(M)];
             const bool frozen = (code.frozen[phi >> 5] >> (phi & 31)) & 1u;
             if (frozen) {

@@ -209,3 +209,37 @@ def test_int8_pair_kernel_vs_oracle(monkeypatch):
     assert set(mism.tolist()) <= set(np.flatnonzero(flags & TIE_FINAL).tolist())
     ok = np.flatnonzero(~(flags & TIE_FINAL).astype(bool))
     np.testing.assert_array_equal(_np(o["iters"])[ok], r["iters"][ok])
+
+
+@pytest.mark.parametrize("quantised", [False, True])
+@pytest.mark.parametrize("n", [64, 128, 256])
+def test_scl_lane_every_list_size_vs_oracle(n, quantised):
+    """Lane-per-path SCL (register-resident small levels, leaf decisions
+    recovered from the root partial sums) against the oracle's scl_decode
+    restatement for every supported list size: list sizes, codewords, leaf
+    decisions u and float64 path metrics bit for bit.  The quantised case uses
+    LLRs on a coarse grid with zeros, so path metrics tie and the check-node f
+    sees zero minima (decoders.py:173-174, 219-228)."""
+    from paper_2602_08501_b200.codes import build_polar_code
+    code = build_polar_code(n, n // 4)
+    rng = np.random.default_rng(1000 + n + int(quantised))
+    F = 48
+    llr = rng.normal(1.0, 1.6, size=(F, n))
+    if quantised:
+        llr = np.round(llr * 2.0) / 2.0
+    dec = DeviceDecoder(code)
+    for L in (4, 8, 16, 32):
+        o = dec.scl_batch(llrs=llr, list_size=L)
+        ln = _np(o["list_n"])
+        cw = words32_to_64(_np(o["list_cw"]).view(np.uint32), n)
+        uw = words32_to_64(_np(o["list_u"]).view(np.uint32), n)
+        pm = _np(o["list_pm"])
+        for f in range(F):
+            u_ref, cw_ref, pm_ref = orc.scl(llr[f], code.info_set, n, L)
+            c = cw_ref.shape[0]
+            assert ln[f] == c, (L, f)
+            np.testing.assert_array_equal(cw[f, :c], cw_ref, err_msg=f"L={L} frame {f}")
+            np.testing.assert_array_equal(pm[f, :c], pm_ref, err_msg=f"L={L} frame {f}")
+            u_bits = np.array([[(int(uw[f, i, j // 64]) >> (j % 64)) & 1 for j in range(n)]
+                               for i in range(c)], dtype=np.uint8)
+            np.testing.assert_array_equal(u_bits, u_ref, err_msg=f"L={L} frame {f}")

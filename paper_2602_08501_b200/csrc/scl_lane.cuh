@@ -154,23 +154,24 @@ __device__ __forceinline__ void lane_step(bool is_g, double (&r)[SclLane<N, L>::
         __syncwarp();
     } else {
         static_assert(HALF <= 16, "register levels hold at most 16 values");
-        const uint32_t word = is_g ? (psrow[lo >> 5] >> (lo & 31)) : 0u;
         const double* par = nullptr;
         if constexpr (D > SCL_VIRT && D < RL) par = llr + (size_t)ptrrow[D] * Lay::INST + Lay::off(D);
+        auto in = [&](int j) -> double {
+            if constexpr (D == SCL_VIRT) return lv2<N>(llr0, psrow, n2, j);
+            else if constexpr (D < RL) return par[j];
+            else return r[Lay::roff(D) + j];
+        };
+        // f and g in separate loops (is_g is warp-uniform): no wasted half
+        if (is_g) {
+            const uint32_t word = psrow[lo >> 5] >> (lo & 31);
 #pragma unroll
-        for (int j = 0; j < HALF; j++) {
-            double a, c;
-            if constexpr (D == SCL_VIRT) {
-                a = lv2<N>(llr0, psrow, n2, j);
-                c = lv2<N>(llr0, psrow, n2, j + HALF);
-            } else if constexpr (D < RL) {
-                a = par[j];
-                c = par[j + HALF];
-            } else {
-                a = r[Lay::roff(D) + j];
-                c = r[Lay::roff(D) + j + HALF];
+            for (int j = 0; j < HALF; j++) {
+                const double a = in(j), c = in(j + HALF);
+                r[Lay::roff(D + 1) + j] = c + (((word >> j) & 1u) ? -a : a);
             }
-            r[Lay::roff(D + 1) + j] = is_g ? c + (((word >> j) & 1u) ? -a : a) : scl_f(a, c);
+        } else {
+#pragma unroll
+            for (int j = 0; j < HALF; j++) r[Lay::roff(D + 1) + j] = scl_f(in(j), in(j + HALF));
         }
     }
 }

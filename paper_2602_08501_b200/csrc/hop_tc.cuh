@@ -354,6 +354,34 @@ __device__ __forceinline__ int min64_s16(const uint32_t (&v)[32], uint32_t (&m)[
     return min((int)(short)(f & 0xFFFFu), (int)(short)(f >> 16));
 }
 
+#ifndef MPW_TC_GRP_SEL
+#define MPW_TC_GRP_SEL 1
+#endif
+// the three registers of packed-score group g (0..10) of a 32-register chunk
+// (group 10 = v[30], v[31] and a +inf pad) by a 4-level select tree
+__device__ __forceinline__ void select_grp(const uint32_t (&v)[32], int g, uint32_t& r0, uint32_t& r1, uint32_t& r2) {
+    uint32_t a[3][8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+        const int hi = k + 8;   // groups 8..10 (11..15 unused)
+#pragma unroll
+        for (int e = 0; e < 3; e++) {
+            const uint32_t lo_v = v[3 * k + e];
+            const uint32_t hi_v = hi < 10 ? v[3 * hi + e] : (hi == 10 ? (e < 2 ? v[30 + e] : 0x7FFF7FFFu) : 0x7FFF7FFFu);
+            a[e][k] = (g & 8) ? hi_v : lo_v;
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < 3; e++) {
+#pragma unroll
+        for (int k = 0; k < 4; k++) a[e][k] = (g & 4) ? a[e][k + 4] : a[e][k];
+#pragma unroll
+        for (int k = 0; k < 2; k++) a[e][k] = (g & 2) ? a[e][k + 2] : a[e][k];
+        a[e][0] = (g & 1) ? a[e][1] : a[e][0];
+    }
+    r0 = a[0][0]; r1 = a[1][0]; r2 = a[2][0];
+}
+
 // int8 screen: a candidate is one 32-bit key (acc + KEY_BIAS) << KEY_IBITS | p,
 // so key order = (score, pattern index) order (ties -> lowest index, as in
 // decoders.py:391) and a top-16 costs 16 registers.  Needs |acc| < KEY_BIAS
@@ -1214,6 +1242,10 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
                         const int g = __ffs(gmask) - 1;
                         gmask &= gmask - 1;
                         uint32_t r0, r1, r2;
+#if MPW_TC_GRP_SEL
+                        // select tree on the group index (no indirect branch, no divergence)
+                        select_grp(v, g, r0, r1, r2);
+#else
                         switch (g) {
 #define MPW_GRP(G) case G: r0 = v[3 * G]; r1 = v[3 * G + 1]; r2 = v[3 * G + 2]; break;
                             MPW_GRP(0) MPW_GRP(1) MPW_GRP(2) MPW_GRP(3) MPW_GRP(4)
@@ -1221,6 +1253,7 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
 #undef MPW_GRP
                             default: r0 = v[30]; r1 = v[31]; r2 = 0x7FFF7FFFu; break;
                         }
+#endif
                         uint32_t hm = 0;
                         hm |= ((int)(short)(r0 & 0xFFFFu) < lim ? 1u : 0u);
                         hm |= ((int)(short)(r0 >> 16) < lim ? 2u : 0u);

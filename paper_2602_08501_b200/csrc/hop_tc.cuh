@@ -354,6 +354,12 @@ __device__ __forceinline__ int min64_s16(const uint32_t (&v)[32], uint32_t (&m)[
     return min((int)(short)(f & 0xFFFFu), (int)(short)(f >> 16));
 }
 
+__device__ __forceinline__ int ld_shared_volatile(const int* p) {
+    int v;
+    asm volatile("ld.volatile.shared.s32 %0, [%1];" : "=r"(v) : "r"((uint32_t)__cvta_generic_to_shared(p)));
+    return v;
+}
+
 #ifndef MPW_TC_GRP_SEL
 #define MPW_TC_GRP_SEL 1
 #endif
@@ -1171,7 +1177,7 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
             const int cb = (int)cst.y;
             // window base: this half's best or the row's best over both halves
             // (published in smem every tile), whichever is lower
-            int shb = 0x7FFFFFFF, pub = 0x7FFFFFFF;
+            int shb = 0x7FFFFFFF, pub = 0x7FFFFFFF, sh_pre = 0x7FFFFFFF;
             auto wbase = [&]() -> int { return kfl ? cb : min(key_val(tk.k[0]), shb); };
             int lastq = kfl ? cb + wq : 0x7FFFFFFF;
             auto upd_lastq = [&]() { lastq = min(key_val(tk.k[KT - 1]) + 1, wbase() + wq); };
@@ -1307,6 +1313,10 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
                         TC_LD32P(tbase, va);
                         if constexpr (NLD == 2) TC_LD32P(tbase + 64, vb);
                         if constexpr (REM == 16) TC_LD8P(tbase + 64 * NLD, vc);
+                        // the other half's published minimum, read while the TMEM
+                        // loads are in flight (at most one tile stale: still an
+                        // achieved score, so a valid window base)
+                        if (!kfl) sh_pre = ld_shared_volatile(&row_best[row]);
                         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                     }
                     release();   // every column of this warp is in registers
@@ -1402,8 +1412,7 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
                     // publish this half's best, take the row's best over both halves
                     const int mine = key_val(tk.k[0]);
                     if (mine < pub) { atomicMin(&row_best[row], mine); pub = mine; }
-                    const int sh = *reinterpret_cast<volatile int*>(&row_best[row]);
-                    if (sh < shb) { shb = sh; upd_lastq(); }
+                    if (sh_pre < shb) { shb = sh_pre; upd_lastq(); }
                 }
               }
                 if (!primary && use_pool && j >= j_claim && j < j_claim + 3) pool_step(j - j_claim);

@@ -1241,9 +1241,12 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
                     const int lim = min(lastq, mn + wq);
                     const uint32_t l16 = (uint32_t)min(lim, 32767) & 0xFFFFu;
                     const uint32_t lim2 = l16 | (l16 << 16);
-                    uint32_t gmask = 0;
+                    // per-halfword compare masks, group g's two halves folded onto bits g
+                    // and g + 16 (one LOP3 per group)
+                    uint32_t gacc = 0;
 #pragma unroll
-                    for (int g = 0; g < 11; g++) gmask |= (__vcmplts2(gm[g], lim2) != 0u ? 1u : 0u) << g;
+                    for (int g = 0; g < 11; g++) gacc |= __vcmplts2(gm[g], lim2) & (0x10001u << g);
+                    uint32_t gmask = (gacc | (gacc >> 16)) & 0x7FFu;
                     while (gmask) {
                         const int g = __ffs(gmask) - 1;
                         gmask &= gmask - 1;

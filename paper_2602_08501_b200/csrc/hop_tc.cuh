@@ -23,7 +23,7 @@
 // tcgen05.mma.kind::i8 (K = 32 per instruction, twice the f16 rate) sums the
 // q_i exactly into s32 TMEM accumulators.  The epilogue works in q units
 // (integer min trees); the frame's bound on |S - s·acc| sets the wider
-// certification window, so the row keeps a top-16 instead of a top-6.
+// certification window, so the row keeps a top-14 instead of a top-6.
 // The smem geometry is unchanged: a 128-byte swizzle row holds 128 int8
 // instead of 64 fp16 elements, so a K-block covers twice the positions.
 #pragma once
@@ -54,7 +54,7 @@ constexpr int SMEM_LIMIT = 232448;   // 227 KB opt-in maximum per CTA
 constexpr int TOPK = MPW_TC_TOPK;    // candidates tracked per row for certification
 static_assert(TOPK <= 8, "top-K hand-over uses 16 TMEM columns");
 #ifndef MPW_TC_TOPK_I8
-#define MPW_TC_TOPK_I8 16
+#define MPW_TC_TOPK_I8 14
 #endif
 constexpr int TOPK_I8 = MPW_TC_TOPK_I8;   // int8 screen: keys per row (window overflow -> continuation pass)
 // int8 screen tile width: 256 patterns, two s32 accumulators.  160 (three
@@ -390,7 +390,7 @@ __device__ __forceinline__ void select_grp(const uint32_t (&v)[32], int g, uint3
 
 // int8 screen: a candidate is one 32-bit key (acc + KEY_BIAS) << KEY_IBITS | p,
 // so key order = (score, pattern index) order (ties -> lowest index, as in
-// decoders.py:391) and a top-16 costs 16 registers.  Needs |acc| < KEY_BIAS
+// decoders.py:391) and a top-14 costs 14 registers.  Needs |acc| < KEY_BIAS
 // (127·wmax < 8192: wmax <= 64) and |P| <= 2^17 (checked on the host).
 constexpr int KEY_IBITS = 17;
 constexpr int KEY_BIAS = 8192;
@@ -1430,7 +1430,7 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
             const uint32_t lastacc = t_lane + ((gtile * SUBS - 1) % NBUF) * TW;
             const uint32_t xaddr = lastacc + grp * WC;
             if (!primary) {
-                // f16: 8 values then 8 indices; int8: 16 keys
+                // f16: 8 values then 8 indices; int8: up to 16 keys (padded)
                 uint32_t xs[16];
 #pragma unroll
                 for (int k = 0; k < 8; k++) {

@@ -1263,13 +1263,12 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
                             default: r0 = v[30]; r1 = v[31]; r2 = 0x7FFF7FFFu; break;
                         }
 #endif
-                        uint32_t hm = 0;
-                        hm |= ((int)(short)(r0 & 0xFFFFu) < lim ? 1u : 0u);
-                        hm |= ((int)(short)(r0 >> 16) < lim ? 2u : 0u);
-                        hm |= ((int)(short)(r1 & 0xFFFFu) < lim ? 4u : 0u);
-                        hm |= ((int)(short)(r1 >> 16) < lim ? 8u : 0u);
-                        hm |= ((int)(short)(r2 & 0xFFFFu) < lim ? 16u : 0u);
-                        hm |= ((int)(short)(r2 >> 16) < lim ? 32u : 0u);
+                        // hit bits 2e (low half) / 2e+1 (high half) of register e from
+                        // the packed compares (same limit as the group test)
+                        const uint32_t hq = (__vcmplts2(r0, lim2) & 0x00010001u) |
+                                            (__vcmplts2(r1, lim2) & 0x00040004u) |
+                                            (__vcmplts2(r2, lim2) & 0x00100010u);
+                        uint32_t hm = (hq & 0x15u) | ((hq >> 15) & 0x2Au);
                         while (hm) {
                             const int h = __ffs(hm) - 1;
                             hm &= hm - 1;

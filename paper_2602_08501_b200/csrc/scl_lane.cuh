@@ -24,8 +24,9 @@
 
 // Levels 1 and 2 are "virtual": never stored, recomputed on demand from the
 // channel LLRs and the path's own partial-sum bits with the same IEEE
-// operations (so the values are bit-identical to stored ones).  Only levels
-// 3..M are stored per path instance: N/4 - 1 doubles instead of N - 1.
+// operations (so the values are bit-identical to stored ones).  Levels
+// 3..RL-1 are stored per path instance in shared memory, levels RL..M in
+// registers (SclLane below).
 constexpr int SCL_VIRT = 2;
 
 template <int N, int L>

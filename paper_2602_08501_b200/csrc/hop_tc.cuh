@@ -160,6 +160,21 @@ __device__ __forceinline__ bool mbar_try_hint(uint32_t bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
+// producer / MMA-issuer waits (and with 2 the epilogue's accumulator-full
+// waits) suspended in hardware instead of spinning, so a waiting warp does
+// not take issue slots from the epilogue warps sharing its SM sub-partition
+// (A/B, three repetitions: spin 108.0, issuer waits 107.8, all 107.8 ms with
+// the least spread)
+#ifndef MPW_TC_SLEEPWAIT
+#define MPW_TC_SLEEPWAIT 2
+#endif
+__device__ __forceinline__ void mbar_wait_issuer(uint32_t bar, uint32_t parity) {
+#if MPW_TC_SLEEPWAIT
+    while (!mbar_try_hint(bar, parity)) {}
+#else
+    mbar_wait(bar, parity);
+#endif
+}
 // ---- cluster (CTA pair sharing the P stream through multicast)
 __device__ __forceinline__ uint32_t cluster_rank() {
     uint32_t r;
@@ -765,7 +780,7 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
                 if (!wait_go(round & 1)) break;
                 for (int j = 0; j < ntiles; j++) {
                     for (int kb = 0; kb < KB; kb++) {
-                        mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+                        mbar_wait_issuer(smem_u32(&empty[stage]), phase ^ 1);
                         const uint32_t fb = smem_u32(&full[stage]);
                         if constexpr (PAIR) {
                             // this CTA's half of the stage (patterns 128 crank .. +127) into its own ring
@@ -838,7 +853,7 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
                     const uint32_t gs = gtile * SUBS + h;
                     const uint32_t buf = gs % NBUF;
                     if (dbg) t0 = clock64();
-                    mbar_wait(smem_u32(&tempty[buf]), ((gs / NBUF) & 1) ^ 1);
+                    mbar_wait_issuer(smem_u32(&tempty[buf]), ((gs / NBUF) & 1) ^ 1);
                     if (dbg) w_tempty += clock64() - t0;
                     const bool tr_on = trace && blockIdx.x == 0 && gs < (uint32_t)TRACE_TILES;
                     if (tr_on) trace[(size_t)gs * TRACE_W] = clock64();
@@ -849,7 +864,7 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
                     for (int kb = 0; kb < KB; kb++) {
                         if (h == 0) {
                             if (dbg) t0 = clock64();
-                            mbar_wait(smem_u32(&full[st]), ph);
+                            mbar_wait_issuer(smem_u32(&full[st]), ph);
                             if (dbg) w_full += clock64() - t0;
                             tc_fence_after();
                         }
@@ -1186,7 +1201,11 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
                 const uint32_t gs = gtile * SUBS + h;
                 const uint32_t buf = gs % NBUF;
                 if (dbg_on && j == 16 && h == 0) t_early += clock64() - t_scan0;
+#if MPW_TC_SLEEPWAIT >= 2
+                while (!mbar_try_hint(smem_u32(&tfull[buf]), (gs / NBUF) & 1)) {}
+#else
                 mbar_wait(smem_u32(&tfull[buf]), (gs / NBUF) & 1);
+#endif
                 tc_fence_after();
                 const bool tr_on = trace && blockIdx.x == 0 && gs < (uint32_t)TRACE_TILES && lane == 0;
                 if (tr_on) trace[(size_t)gs * TRACE_W + warp] = clock64();

@@ -759,7 +759,7 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
     // end of a round for the whole cluster: wait for every CTA's round end
     auto wait_go = [&](uint32_t parity) -> bool {   // returns true while rows are left in the cluster
         if (CL == 1) {
-            mbar_wait(smem_u32(go), parity);
+            mbar_wait_issuer(smem_u32(go), parity);   // the round end runs on the epilogue warps meanwhile
             return *done_flag == 0;
         }
         mbar_wait_acq_cluster(smem_u32(go), parity);

@@ -1372,8 +1372,12 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
                         if (PROF && (xp & 16)) {
                             if (ma == -12345 || mb == -12345 || mc == -12345) tk.k[0] = 0u;
                         } else {
-                            if (ma < lastq) slow8(va, ga, pa, ma);
-                            if (NLD == 2 && mb < lastq) slow8(vb, gb, pa + 64, mb);
+                            // the tile's minimum over all of this warp's columns bounds the
+                            // window of every chunk (after the tile the running best is <= it)
+                            const int mt = min(min(ma, mb), mc);
+                            const int lt = min(lastq, mt + wq);
+                            if (ma < lt) slow8(va, ga, pa, mt);
+                            if (NLD == 2 && mb < lt) slow8(vb, gb, pa + 64, mt);
                             if (REM == 16 && mc < lastq) {
                                 // 16 values: one hit mask, a 3-level register select per hit
                                 const int lim = min(lastq, mc + wq);

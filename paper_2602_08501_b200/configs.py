@@ -74,8 +74,14 @@ CONFIGS = {
                          collector=dict(weight_cap=56, iterations=50_000, seed=20260208, p_max=3)),
 }
 
-# sha256 over the CWS1 member words of each config's P, pinned once generated
-SPHERE_SHA256 = {}
+# sha256 over the CWS1 member words of each config's P (sphere_digest), pinned
+# when the sets were first generated; tests/test_patterns.py regenerates them
+SPHERE_SHA256 = {
+    "cfg1": "66dc251037446d9242f3c308d6e727fc63c4ae7970f536438d1cb373e095dbb4",
+    "cfg2": "2188cdd720549f09b7100c97d3356eb9ed952487f7fdcb2c8c4ddda114d280fd",
+    "cfg3": "758c3ac1cd842bb8d03140b36b1a0af742229a86614d0cc3d53e2256eba1b18f",
+    "cfg4": "3c467a3ce8f8ed44b0cbf286153f3e5299dd242db1af38bba449acc7e4eef855",
+}
 
 _CACHE_DIR = os.environ.get("MPWSD_CACHE", os.path.join(os.path.dirname(os.path.abspath(__file__)), "_spheres"))
 

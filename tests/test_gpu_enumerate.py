@@ -40,3 +40,13 @@ def test_gpu_enumerate_small_codes_and_limits():
         patterns.enumerate_sphere_gpu(codes.build_polar_code(64, 10), 99)
     with pytest.raises(ValueError):
         patterns.weight_spectrum_gpu(configs.CONFIGS["cfg4"].code())
+
+
+@pytest.mark.parametrize("r,size", [(3, 538), (4, 6472)])
+def test_gpu_criterion_1_sphere_sizes_256_16(r, size):
+    """enum_kernel reproduces criterion 1 (reference tests/test_acceptance.py:51-71)
+    member for member against the host walk."""
+    code = codes.build_ca_polar_code(256, 16)
+    a = patterns.enumerate_sphere_gpu(code, r)
+    assert a.size == size
+    assert np.array_equal(np.asarray(a.member_words), np.asarray(patterns.enumerate_sphere(code, r).member_words))

@@ -119,6 +119,27 @@ def _dist_env():
     return ws, rank, local
 
 
+def _spawn_ranks(n: int) -> int:
+    """`bench.py --gpus N` outside torchrun: relaunch this command as N ranks
+    (one process per GPU) through torch.distributed.run on 127.0.0.1."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def _require_devices(n: int):
+    import torch
+    have = torch.cuda.device_count() if torch.cuda.is_available() else 0
+    if have < n:
+        sys.stderr.write(f"bench.py: {n} GPUs requested, {have} visible\n")
+        sys.exit(1)
+
+
 def cpu_oracle_rate(cfg, code, sph, sigma, y, seconds: float, threads: int):
     """Oracle (plain-C float64 restatement of the reference) on a bounded
     prefix of the same workload.  Returns (frames/s, frames, seconds)."""
@@ -184,6 +205,32 @@ def _config(args, cfg, code, sph):
 
 
 def main():
+    args = _parse()
+    ws, rank, local = _dist_env()
+    if args.impl == "ours":
+        if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+            _require_devices(args.gpus)
+            sys.exit(_spawn_ranks(args.gpus))
+        if args.gpus != ws:
+            sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}\n")
+            sys.exit(2)
+        _require_devices(ws)
+
+    from paper_2602_08501_b200 import configs
+    cfg = configs.CONFIGS[args.config]
+    code = cfg.code()
+    sph = configs.build_sphere_for(cfg, code)
+    sigma = cfg.sigma(code=code)
+
+    if args.impl == "reference":
+        run_reference(args, cfg, code, sph, sigma)
+        return
+    line = run_ours(args, cfg, code, sph, sigma)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+
+
+def _parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
@@ -197,29 +244,42 @@ def main():
     ap.add_argument("--ref-step-seconds", type=float, default=10.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    args = ap.parse_args()
+    ap.add_argument("--hop-option", action="append", default=[],
+                    help="key=value tensor-hop launch option (mpw_set_option), for A/B runs")
+    args = ap.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3
+    return args
 
-    from paper_2602_08501_b200 import channel, configs
-    cfg = configs.CONFIGS[args.config]
-    code = cfg.code()
-    sph = configs.build_sphere_for(cfg, code)
-    sigma = cfg.sigma(code=code)
 
-    if args.impl == "reference":
-        run_reference(args, cfg, code, sph, sigma)
-        return
-
+def run_ours(args, cfg, code, sph, sigma, backend: str = "nccl", device_index=None):
+    """One rank of the measured run.  Returns rank 0's JSON line (other ranks:
+    None).  backend "gloo" (tests) reduces through host tensors, so several
+    ranks may share one device (their decodes are independent)."""
     import torch
     import torch.distributed as dist
+    from paper_2602_08501_b200 import channel
     from paper_2602_08501_b200.decoders import DeviceDecoder, words64_to_32
 
     ws, rank, local = _dist_env()
+    local = local if device_index is None else device_index
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if ws > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    if ws > 1 and not dist.is_initialized():
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+
+    def allreduce(t, op):
+        if ws == 1:
+            return t
+        if backend == "nccl":
+            dist.all_reduce(t, op=op)
+            return t
+        h = t.cpu()
+        dist.all_reduce(h, op=op)
+        return h.to(t.device)
 
     F = args.frames
     nb = 2
@@ -231,6 +291,9 @@ def main():
     tx_dev = [torch.from_numpy(words64_to_32(tx[i * F:(i + 1) * F], code.n).view(np.int32)).to(dev)
               for i in range(nb)]
     dec = DeviceDecoder(code, sph, device=dev)
+    for kv in args.hop_option:
+        k, v = kv.split("=", 1)
+        dec.set_option(k, int(v))
     A, T, L = cfg.num_paths, cfg.max_iterations, cfg.list_size
     outs = [dec.alloc_outputs(F, A, T) for _ in range(nb)]
     counters = torch.zeros(8, dtype=torch.int64, device=dev)
@@ -245,6 +308,7 @@ def main():
     counters.zero_()
     dec.set_timing(True)
     dec.read_timing(reset=True)
+    launches0 = dec.launch_count
     clocks = ClockSampler(local)
     clocks.start()
     if ws > 1:
@@ -261,13 +325,19 @@ def main():
         dist.barrier()
     clocks.stop()
     ms = e0.elapsed_time(e1)
+    launches = dec.launch_count - launches0
     kms, klaunch = dec.read_timing(reset=True)
     dec.set_timing(False)
     ctr = counters.clone()
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    rank_ms = [torch.zeros(1, dtype=torch.float64, device=dev if backend == "nccl" else "cpu") for _ in range(ws)]
     if ws > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(ctr, op=dist.ReduceOp.SUM)
+        dist.all_gather(rank_ms, t if backend == "nccl" else t.cpu())
+    else:
+        rank_ms = [t]
+    t = allreduce(t, dist.ReduceOp.MAX)
+    ctr = allreduce(ctr, dist.ReduceOp.SUM)
+    nl = allreduce(torch.tensor([launches], dtype=torch.int64, device=dev), dist.ReduceOp.SUM)
     ms_max = float(t.item())
     ctr = ctr.cpu().numpy()
     frames_all = F * args.steps * ws
@@ -308,9 +378,7 @@ def main():
             host_step(i)
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
-        tw = torch.tensor([wall], dtype=torch.float64, device=dev)
-        if ws > 1:
-            dist.all_reduce(tw, op=dist.ReduceOp.MAX)
+        tw = allreduce(torch.tensor([wall], dtype=torch.float64, device=dev), dist.ReduceOp.MAX)
         e2e = {"value": frames_all / float(tw.item()), "unit": UNIT,
                "h2d_bytes_per_step": int(F * code.n * 4 + F * nw * 4),
                "d2h_bytes_per_step": int(F * nw * 4 + F * 8 + F + 8 * 8),
@@ -374,8 +442,11 @@ def main():
                 "near_tie_frames": int(ctr[5]),
                 "uncertified_frames": int(ctr[6]),
                 "clocks": clocks.summary(),
-                # per step: scl, ebound, hop, finalize, frame (memsets are not kernels)
-                "gpu_launches": int(5 * args.steps),
+                # this library's kernels launched in the timed region, all ranks
+                # (mpw_launch_count: scl, ebound, hop, finalize, frame per step)
+                "gpu_launches": int(nl.item()),
+                "rank_ms_per_step": [float(r.item()) / args.steps for r in rank_ms],
+                "counters": shard.counters_dict(ctr),
                 "e2e": e2e}
         if not args.no_cpu:
             threads = os.cpu_count() or 1
@@ -383,9 +454,12 @@ def main():
             line["cpu_baseline"] = {"value": r, "unit": UNIT, "cores": threads, "kind": "port",
                                     "sample": f"first {fr} frames of the same workload, {dt:.1f}s, oracle/oracle.c "
                                               f"(float64 restatement of feclab two_stage_decode), {threads} threads"}
-        print(json.dumps(line), flush=True)
+    else:
+        line = None
     if ws > 1:
+        dist.barrier()
         dist.destroy_process_group()
+    return line
 
 
 if __name__ == "__main__":

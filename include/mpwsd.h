@@ -10,8 +10,11 @@
  *   mpw_set_patterns     <- CodeWeightSphere.member_words[1:] (wsphere.py:73-112)
  *   mpw_scl_batch        <- scl_decode(llrs, code, list_size)   decoders.py:181-268
  *   mpw_mpwsd_batch      <- mp_wsd(y, init_list, sphere, params) decoders.py:455-514
+ *                           (also wsd_trajectory :420-452, wsd_step :401-417)
  *   mpw_two_stage_batch  <- two_stage_decode(y, code, SclStage(L), params, sphere,
  *                           sigma)                               decoders.py:520-583
+ *   *_f64 variants       <- the same with the reference's float64 y (decoders.py:411,
+ *                           466, 538 coerce y to float64)
  *
  * Conventions
  *   - Plain pointers and sizes; no framework types.  Buffers of the *_batch
@@ -26,8 +29,11 @@
  *     message (thread-local).  No exception crosses the ABI.  Errors mirror the
  *     reference's ValueErrors (crc_gated without CRC, decoders.py:540-541; bad
  *     WsdParams, :80-86) plus device limits (MPW_ERR_UNSUPPORTED).
- *   - A handle is used by one host thread at a time; use one handle per
- *     device (or per thread).
+ *   - A handle is used by one host thread at a time (its stage-2 scratch and
+ *     staging buffers are per handle); concurrent callers use one handle per
+ *     thread, as the Python drop-in does (the reference's sweep calls the
+ *     decoders from a thread pool, simharness.py:318-330).  Handles on
+ *     different devices are independent.
  */
 #ifndef MPWSD_H_
 #define MPWSD_H_
@@ -38,7 +44,7 @@
 extern "C" {
 #endif
 
-#define MPW_ABI_VERSION 1
+#define MPW_ABI_VERSION 2
 
 #define MPW_OK 0
 #define MPW_ERR_ARG (-1)
@@ -54,9 +60,9 @@ extern "C" {
 /* hop kernel selection */
 #define MPW_HOP_AUTO 0
 #define MPW_HOP_GATHER 1  /* shared-memory gather-sum on CUDA cores */
-#define MPW_HOP_TENSOR 2  /* tcgen05, one fp16 limb of t, float64-certified top-4 (default) */
-#define MPW_HOP_TENSOR_2LIMB 3 /* tcgen05, fp16 hi+lo limbs of t, float64-certified top-4 */
-#define MPW_HOP_TENSOR_I8 4 /* tcgen05 kind::i8, per-frame int8 quantisation of t, certified top-16 (N = 128, 256) */
+#define MPW_HOP_TENSOR 2  /* tcgen05, one fp16 limb of t, certified top-6 */
+#define MPW_HOP_TENSOR_2LIMB 3 /* tcgen05, fp16 hi+lo limbs of t, certified top-6 */
+#define MPW_HOP_TENSOR_I8 4 /* tcgen05 kind::i8, per-frame int8 quantisation of t, certified top-14 (N = 128, 256) */
 
 /* counters (int64, accumulated by mpw_two_stage_batch; caller zeroes) */
 #define MPW_CTR_FRAMES 0
@@ -114,6 +120,12 @@ int mpw_scl_batch(mpw_handle* h, const float* y, const double* llr, int F, doubl
 int mpw_mpwsd_batch(mpw_handle* h, const float* y, const uint32_t* anchors, const int32_t* n_anchor,
                     int F, int A, int T, int variant, uint32_t* best, double* best_ed,
                     int32_t* iters, int32_t* hops, uint8_t* flags, void* stream);
+/* Same with float64 received words (F x n): the screens run on their fp32
+ * rounding with error bounds widened by the rounding, every exact re-scoring
+ * and reported ED uses the float64 values (variant AUTO, TENSOR or GATHER). */
+int mpw_mpwsd_batch_f64(mpw_handle* h, const double* y, const uint32_t* anchors, const int32_t* n_anchor,
+                        int F, int A, int T, int variant, uint32_t* best, double* best_ed,
+                        int32_t* iters, int32_t* hops, uint8_t* flags, void* stream);
 
 /* The full two-stage path.  stage[F]: 0 = stage1_crc_pass, 1 = mp_wsd.
  * tx_cw (F x nw, may be NULL) enables the error counter.  best_msg[F]
@@ -124,6 +136,13 @@ int mpw_two_stage_batch(mpw_handle* h, const float* y, int F, double sigma, int 
                         uint64_t* best_msg, double* best_ed, uint8_t* stage, int32_t* iters,
                         int32_t* hops, uint32_t* anchors_out, uint8_t* flags,
                         unsigned long long* counters, void* stream);
+/* Same with float64 received words (F x n): stage 1 from the float64 LLRs
+ * 2.0 * y / (sigma * sigma) (decoders.py:550), stage 2 as mpw_mpwsd_batch_f64. */
+int mpw_two_stage_batch_f64(mpw_handle* h, const double* y, int F, double sigma, int L, int A, int T,
+                            int mode, int variant, const uint32_t* tx_cw, uint32_t* best,
+                            uint64_t* best_msg, double* best_ed, uint8_t* stage, int32_t* iters,
+                            int32_t* hops, uint32_t* anchors_out, uint8_t* flags,
+                            unsigned long long* counters, void* stream);
 
 /* Two-stage decode with order-k OSD as stage 1 (decoders.py:274-317, 555-556;
  * the paper's RM initialiser).  list_cap <= 0 means no cap.  OSD candidates
@@ -159,7 +178,11 @@ int mpw_two_stage_batch_host(mpw_handle* h, const float* y_host, int F, double s
  * {stage 1, stage 2 hops, finalize, frame epilogue}. */
 int mpw_set_timing(mpw_handle* h, int enable);
 /* Options: "scl_generic" (1 = force the warp-per-frame stage-1 kernel instead of
- * the lane-per-path one; both are bit-exact), "timing" (same as mpw_set_timing). */
+ * the lane-per-path one; both are bit-exact), "timing" (same as mpw_set_timing);
+ * tensor-hop variants for A/B runs and tests: "i8_cluster" (2 = CTA pairs
+ * sharing the P stream), "i8_pair" (1 = cta_group::2 pair MMAs), "f16_cluster"
+ * (0 = single CTAs for the 1-limb N = 256 shape), "hop_experiment" (profiling
+ * and test bits of the hop kernel, e.g. 2048 = int8 window overflow at 4 keys). */
 int mpw_set_option(mpw_handle* h, const char* key, int value);
 int mpw_read_timing(mpw_handle* h, double* ms_out, long long* launches_out, int reset);
 
@@ -173,6 +196,8 @@ int mpw_channel_batch(mpw_handle* h, uint64_t seed, int snr_idx, long long first
                       double sigma, float* y, uint32_t* tx, uint64_t* msg, void* stream);
 
 int mpw_num_patterns(mpw_handle* h);
+/* Number of kernels this handle has launched (all entry points). */
+long long mpw_launch_count(mpw_handle* h);
 int mpw_tensor_path_ready(mpw_handle* h);
 /* The hop variant MPW_HOP_AUTO resolves to for the current code and pattern set. */
 int mpw_hop_auto_variant(mpw_handle* h);

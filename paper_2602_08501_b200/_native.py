@@ -35,6 +35,12 @@ _SIGS = {
     "mpw_two_stage_batch": (c_int, [c_void_p, c_void_p, c_int, c_double, c_int, c_int, c_int, c_int,
                                     c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                     c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "mpw_mpwsd_batch_f64": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int,
+                                    c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "mpw_two_stage_batch_f64": (c_int, [c_void_p, c_void_p, c_int, c_double, c_int, c_int, c_int, c_int,
+                                        c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                        c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "mpw_launch_count": (ctypes.c_longlong, [c_void_p]),
     "mpw_two_stage_batch_host": (c_int, [c_void_p, c_void_p, c_int, c_double, c_int, c_int, c_int,
                                          c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p,
                                          c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),

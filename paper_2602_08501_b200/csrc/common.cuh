@@ -55,25 +55,6 @@ __device__ __forceinline__ int getbit32(const uint32_t* w, int j) { return (w[j 
 #define MPW_F_TIE_FINAL 4u
 #define MPW_F_UNRESOLVED 8u
 
-// Running top-3 of a scan (values S_p, ascending; index order breaks ties
-// because patterns are visited in increasing index, decoders.py:391).
-struct Top3 {
-    float b1, b2, b3;
-    int i1, i2;
-    __device__ __forceinline__ void reset() { b1 = b2 = b3 = CUDART_INF_F; i1 = i2 = 0; }
-    __device__ __forceinline__ void push(float s, int p) {
-        if (s < b3) {
-            if (s < b2) {
-                b3 = b2;
-                if (s < b1) { b2 = b1; i2 = i1; b1 = s; i1 = p; }
-                else { b2 = s; i2 = p; }
-            } else {
-                b3 = s;
-            }
-        }
-    }
-};
-
 // Exact (float64) S_p = Σ_{i∈supp p} x_i y_i for the centre c (decoders.py:329-336).
 template <int NW>
 __device__ __forceinline__ double exact_score(const float* __restrict__ yrow, const uint32_t (&c)[NW],
@@ -108,33 +89,22 @@ __device__ __forceinline__ double exact_score(const float* __restrict__ yrow, co
     return s;
 }
 
-// End-of-scan decision with certification.  fp32 scores carry at most `err`
-// absolute error; any pair inside the window is re-scored in float64, so the
-// chosen pattern and the accept test match exact arithmetic unless a third
-// candidate also falls inside the window (flagged MPW_F_UNRESOLVED).
-// Near-tie report (north-star definition): exact relative gaps < tie_rel.
+// The same score from the caller's float64 received word (float64 inputs).
 template <int NW>
-__device__ __forceinline__ void certify_hop(const Top3& t, const float* __restrict__ yrow,
-                                            const uint32_t (&c)[NW], const uint32_t* __restrict__ pbits,
-                                            int nw, int n, float ed, float tie_rel, float err, int& best,
-                                            bool& improve, uint8_t& flags) {
-    const float thr = tie_rel * ed * 0.25f;          // 1e-5 relative ED gap, in S units
-    const float win = thr + 2.0f * err;
-    best = t.i1;
-    improve = t.b1 < 0.0f;
-    const bool pair = (t.b2 - t.b1) < win;
-    const bool zero = fabsf(t.b1) < win;
-    if (!pair && !zero) return;
-    double e1 = exact_score<NW>(yrow, c, pbits + (size_t)t.i1 * nw, nw, n);
-    double eb = e1;
-    if (pair) {
-        const double e2 = exact_score<NW>(yrow, c, pbits + (size_t)t.i2 * nw, nw, n);
-        if (e2 < e1 || (e2 == e1 && t.i2 < t.i1)) { best = t.i2; eb = e2; }
-        if (fabs(e2 - e1) < (double)thr) flags |= MPW_F_TIE_ARGMIN;
-        if ((t.b3 - t.b1) < win) flags |= MPW_F_UNRESOLVED;
+__device__ __forceinline__ double exact_score64(const double* __restrict__ yrow, const uint32_t (&c)[NW],
+                                                const uint32_t* __restrict__ pb, int nw, int n) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; w++) {
+        if (w >= nw) break;
+        const uint32_t bits = pb[w], cw = c[w];
+        for (uint32_t b = bits; b; b &= b - 1) {
+            const int i = __ffs(b) - 1;
+            const double yi = yrow[w * 32 + i];
+            s += ((cw >> i) & 1u) ? -yi : yi;
+        }
     }
-    improve = eb < 0.0;
-    if (fabs(eb) < (double)thr) flags |= MPW_F_TIE_ACCEPT;
+    return s;
 }
 
 // Upper bound on the sum of the w largest of the values x[] spread over the
@@ -171,7 +141,9 @@ __device__ __forceinline__ float warp_topw_bound(const float* xv, int cnt, int w
 //   x: 1-limb tensor (fp16(t)),  y: 2-limb tensor (fp16 hi + fp16 lo),
 //   z: fp32 gather,              w: sum of the wmax largest |y_i|.
 // Each sums the wmax largest per-element representation errors and adds
-// an fp32 accumulation bound of (terms) * 2^-23 * sum|t|.
+// an fp32 accumulation bound of (terms) * 2^-23 * sum|t| (2^-23 = 2u per
+// add: the tensor cores' fp32 accumulation is not guaranteed to round to
+// nearest).
 __device__ __forceinline__ float4 warp_error_bounds(const float* __restrict__ yrow, int n, int wmax) {
     const int lane = threadIdx.x & 31;
     float ay[32], e1[32], e2[32];
@@ -275,11 +247,18 @@ struct TopK {
 // best approximate score is re-scored in float64; the exact argmin (ties ->
 // lowest index) and the exact accept test are used.  If the K-th score is
 // also inside the window the scan is flagged MPW_F_UNRESOLVED.
+// y64row (may be null): the caller's float64 received word, re-scored from
+// instead of yrow (err_row then includes the fp32 rounding of y).
 template <int K, int NW>
 __device__ __forceinline__ void certify_topk(const TopK<K>& t, const float* __restrict__ yrow,
+                                             const double* __restrict__ y64row,
                                              const uint32_t (&c)[NW], const uint32_t* __restrict__ pbits,
                                              int nw, int n, float ed, float tie_rel, float err_row, int& best,
                                              bool& improve, float& best_approx, uint8_t& flags) {
+    auto score = [&](int p) {
+        return y64row ? exact_score64<NW>(y64row, c, pbits + (size_t)p * nw, nw, n)
+                      : exact_score<NW>(yrow, c, pbits + (size_t)p * nw, nw, n);
+    };
     const float thr = tie_rel * ed * 0.25f;
     const float win = thr + 2.0f * err_row;
     best = t.i[0];
@@ -288,12 +267,12 @@ __device__ __forceinline__ void certify_topk(const TopK<K>& t, const float* __re
     const bool pair = (t.b[1] - t.b[0]) < win;
     const bool zero = fabsf(t.b[0]) < err_row + thr;
     if (!pair && !zero) return;
-    double eb = exact_score<NW>(yrow, c, pbits + (size_t)t.i[0] * nw, nw, n);
+    double eb = score(t.i[0]);
     double e_second = CUDART_INF;
 #pragma unroll
     for (int k = 1; k < K - 1; k++) {
         if (!((t.b[k] - t.b[0]) < win)) break;
-        const double e = exact_score<NW>(yrow, c, pbits + (size_t)t.i[k] * nw, nw, n);
+        const double e = score(t.i[k]);
         if (e < eb || (e == eb && t.i[k] < best)) {
             e_second = eb;
             eb = e;

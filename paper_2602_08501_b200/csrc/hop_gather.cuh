@@ -16,6 +16,7 @@
 struct HopParams {
     int n, nw, A, T;
     const float* y;
+    const double* y64;     // float64 inputs: the caller's received words (y = their fp32 rounding), else null
     S2Dev s2;
     PatDev P;
     const uint4* sup;      // padded supports, 8 x uint16 per uint4
@@ -23,7 +24,6 @@ struct HopParams {
     int sup_in_smem;       // supports + offsets cached in shared memory
     int total_sup_u4;
     float tie_rel;         // near-tie threshold (relative), 1e-5
-    float err;             // bound on |S_fp32 - S_exact| (S units)
 };
 
 __host__ __device__ inline size_t gather_warp_smem(int n) { return sizeof(float) * (size_t)(n + 1) * 32; }
@@ -103,8 +103,8 @@ __global__ void __launch_bounds__(256) hop_gather_kernel(HopParams hp) {
                 int i1;
                 bool improve;
                 float sb;
-                certify_topk<4, NW>(top, hp.y + (size_t)f * n, c, hp.P.bits, nw, n, ed, hp.tie_rel, err_row,
-                                    i1, improve, sb, flags);
+                certify_topk<4, NW>(top, hp.y + (size_t)f * n, hp.y64 ? hp.y64 + (size_t)f * n : nullptr, c,
+                                    hp.P.bits, nw, n, ed, hp.tie_rel, err_row, i1, improve, sb, flags);
                 if (improve) {
                     for (int qq = soff[i1]; qq < soff[i1 + 1]; qq++) {
                         const uint4 v = sup[qq];

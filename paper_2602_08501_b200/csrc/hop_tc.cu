@@ -10,29 +10,22 @@
 // ---------------------------------------------------------------------------
 // host side
 
-// CTA-pair P streaming (multicast) for the cfg4 shape; MPW_TC_CLUSTER=0 disables it
-static bool tc_cluster() {
-    const char* e = getenv("MPW_TC_CLUSTER");
-    return !(e && atoi(e) == 0);
-}
+// Launch options (TcOpts, set per handle through mpw_set_option): the
+// defaults are the production choices; the others are kept for A/B runs and
+// the parity tests.  The per-tile clock trace (experiment bit 128) exists
+// only in builds with -DMPW_PROFILE.
 
-// int8 screen: cta_group::2 pair kernel (MPW_TC_PAIR=1)
-static bool tc_pair() {
-    const char* e = getenv("MPW_TC_PAIR");
-    return e && atoi(e) == 1;
+// fp32 certification pass bound: any summation order of at most wmax terms
+// has |fl(S) - S| <= gamma_{wmax-1} sum|t_i| (gamma_k = k u / (1 - k u),
+// u = 2^-24); with float64 inputs the fp32 rounding of y adds u sum|y|.
+// Rounded up by 0.2 % (the float conversion and the product with sum|y|).
+static float cert_gamma(int wmax, bool y64) {
+    const double u = 5.9604644775390625e-8;
+    const double k = wmax > 1 ? wmax - 1 : 0;
+    double g = k * u / (1.0 - k * u);
+    if (y64) g += u;
+    return (float)(g * 1.002);
 }
-
-// int8 screen cluster size (default 1: single CTAs)
-static int tc_i8_cluster() {
-    const char* e = getenv("MPW_TC_I8_CL");
-    return e ? atoi(e) : 1;
-}
-
-static int tc_experiment() {
-    const char* e = getenv("MPW_TC_EXPERIMENT");
-    return e ? atoi(e) : 0;
-}
-
 
 bool tc_supported(int n, int np) { return (n == 64 || n == 128 || n == 256) && np >= 1; }
 bool tc_i8_supported(int n, int np) { return (n == 128 || n == 256) && np >= 1; }
@@ -99,21 +92,24 @@ int tc_build(TcPatterns& t, const uint32_t* bits, int np, int n, int nw) {
 }
 
 template <int KB, int NW, int LIMBS, int MODE, int CL = 1, int PM = 0>
-static int tc_launch_t(const TcPatterns& t, int n, int nw, int A, int T, const float* y, S2Dev s2, PatDev P,
-                       int num_sms, cudaStream_t st) {
+static int tc_launch_t(const TcPatterns& t, int n, int nw, int A, int T, const float* y, const double* y64,
+                       S2Dev s2, PatDev P, int num_sms, const TcOpts& o, cudaStream_t st) {
     tc::Params prm;
     prm.n = n; prm.nw = nw; prm.A = A; prm.T = T; prm.np = t.np; prm.ntiles = LIMBS == 0 ? t.ntiles8 : t.ntiles;
-    prm.y = y; prm.s2 = s2; prm.pbits = P.bits; prm.btiles = LIMBS == 0 ? t.tiles8 : t.tiles; prm.tie_rel = 1e-5f;
-    prm.err = 2e-3f;
-    prm.experiment = tc_experiment();
-    static long long* trace = nullptr;
+    prm.y = y; prm.y64 = MODE == 3 ? y64 : nullptr;
+    prm.s2 = s2; prm.pbits = P.bits; prm.btiles = LIMBS == 0 ? t.tiles8 : t.tiles; prm.tie_rel = 1e-5f;
+    prm.cert_g = cert_gamma(s2.wmax, MODE == 3);
+    prm.experiment = MODE == 2 ? o.experiment : 0;
     prm.trace = nullptr;
+#ifdef MPW_PROFILE
+    static long long* trace = nullptr;
     if (prm.experiment & 128) {
         const size_t tb = sizeof(long long) * tc::TRACE_W * tc::TRACE_TILES;
         if (!trace && cudaMallocManaged(&trace, tb) != cudaSuccess) trace = nullptr;
         if (trace) memset(trace, 0, tb);
         prm.trace = trace;
     }
+#endif
     const size_t smem = tc::smem_bytes(KB, LIMBS, CL, PM);
     auto kern = tc::hop_tc_kernel<KB, NW, LIMBS, MODE, CL, PM>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -141,6 +137,7 @@ static int tc_launch_t(const TcPatterns& t, int n, int nw, int A, int T, const f
         if (e != cudaSuccess) return -(int)e;
     }
     e = cudaGetLastError();
+#ifdef MPW_PROFILE
     if (e == cudaSuccess && prm.trace) {
         // profiling only: dump the trace of this launch (CTA 0), overwriting the previous one
         cudaStreamSynchronize(st);
@@ -150,56 +147,61 @@ static int tc_launch_t(const TcPatterns& t, int n, int nw, int A, int T, const f
             fclose(fh);
         }
     }
+#endif
     return e == cudaSuccess ? 0 : -(int)e;
 }
 
-int tc_launch(const TcPatterns& t, int n, int nw, int A, int T, const float* y, S2Dev s2, PatDev P,
-                     int num_sms, int limbs, cudaStream_t st) {
+#define TCL(...) tc_launch_t<__VA_ARGS__>(t, n, nw, A, T, y, y64, s2, P, num_sms, o, st)
+
+int tc_launch(const TcPatterns& t, int n, int nw, int A, int T, const float* y, const double* y64, S2Dev s2,
+              PatDev P, int num_sms, int limbs, const TcOpts& o, cudaStream_t st) {
     if (!t.ready) return 1;
+    if (y64) {
+        // float64 received words: one fp16 limb, exact re-scoring from y64
+        if (limbs != 1) return 1;
+        switch (n) {
+            case 64: return TCL(1, 2, 1, 3);
+            case 128: return TCL(2, 4, 1, 3);
+            case 256: return TCL(4, 8, 1, 3);
+            default: return 1;
+        }
+    }
+    const int x = o.experiment;
+#ifdef MPW_PROFILE
+    if (x == 128) {   // per-tile clock trace of CTA 0
+        if (limbs == 0 && n == 256)
+            return o.i8_pair ? TCL(2, 8, 0, 1, 2, 1) : o.i8_cluster == 2 ? TCL(2, 8, 0, 1, 2) : TCL(2, 8, 0, 1);
+        if (limbs == 1 && n == 256) return o.f16_cluster ? TCL(4, 8, 1, 1, 2) : TCL(4, 8, 1, 1);
+    }
+#endif
     if (limbs == 0) {
         if (!t.ready8) return 1;
         switch (n) {
-            case 128: return tc_experiment() ? tc_launch_t<1, 4, 0, 2>(t, n, nw, A, T, y, s2, P, num_sms, st)
-                                             : tc_launch_t<1, 4, 0, 0>(t, n, nw, A, T, y, s2, P, num_sms, st);
-            case 256: {
-                // MPW_TC_I8_CL: 1 single CTAs, 2 CTA pairs sharing the P stream by
-                // multicast; MPW_TC_PAIR=1 selects the cta_group::2 pair kernel (correct,
-                // but slower: the pair's MMAs wait for the slower of two epilogues)
-                const int x = tc_experiment();
-                const bool pair = tc_pair();
-                const int cl = tc_i8_cluster();
-                if (x == 128) return pair ? tc_launch_t<2, 8, 0, 1, 2, 1>(t, n, nw, A, T, y, s2, P, num_sms, st)
-                                          : cl == 2 ? tc_launch_t<2, 8, 0, 1, 2>(t, n, nw, A, T, y, s2, P, num_sms, st)
-                                                    : tc_launch_t<2, 8, 0, 1>(t, n, nw, A, T, y, s2, P, num_sms, st);
-                if (x) return tc_launch_t<2, 8, 0, 2>(t, n, nw, A, T, y, s2, P, num_sms, st);
-                if (pair) return tc_launch_t<2, 8, 0, 0, 2, 1>(t, n, nw, A, T, y, s2, P, num_sms, st);
-                return cl == 2 ? tc_launch_t<2, 8, 0, 0, 2>(t, n, nw, A, T, y, s2, P, num_sms, st)
-                               : tc_launch_t<2, 8, 0, 0>(t, n, nw, A, T, y, s2, P, num_sms, st);
-            }
+            case 128: return x ? TCL(1, 4, 0, 2) : TCL(1, 4, 0, 0);
+            case 256:
+                // i8_cluster 2: CTA pairs sharing the P stream by multicast; i8_pair:
+                // the cta_group::2 pair kernel (correct, but slower: the pair's MMAs
+                // wait for the slower of two epilogues); default single CTAs
+                if (x) return TCL(2, 8, 0, 2);
+                if (o.i8_pair) return TCL(2, 8, 0, 0, 2, 1);
+                return o.i8_cluster == 2 ? TCL(2, 8, 0, 0, 2) : TCL(2, 8, 0, 0);
             default: return 1;
         }
     }
     if (limbs == 1) {
         switch (n) {
-            case 64: return tc_launch_t<1, 2, 1, 0>(t, n, nw, A, T, y, s2, P, num_sms, st);
-            case 128: return tc_launch_t<2, 4, 1, 0>(t, n, nw, A, T, y, s2, P, num_sms, st);
-            case 256: {
-                // profiling builds of the cfg4 shape: 128 alone = trace only, other knobs = full
-                const int x = tc_experiment();
-                const bool pair = tc_cluster();
-                if (x == 128) return pair ? tc_launch_t<4, 8, 1, 1, 2>(t, n, nw, A, T, y, s2, P, num_sms, st)
-                                          : tc_launch_t<4, 8, 1, 1>(t, n, nw, A, T, y, s2, P, num_sms, st);
-                if (x) return tc_launch_t<4, 8, 1, 2>(t, n, nw, A, T, y, s2, P, num_sms, st);
-                return pair ? tc_launch_t<4, 8, 1, 0, 2>(t, n, nw, A, T, y, s2, P, num_sms, st)
-                            : tc_launch_t<4, 8, 1, 0>(t, n, nw, A, T, y, s2, P, num_sms, st);
-            }
+            case 64: return TCL(1, 2, 1, 0);
+            case 128: return TCL(2, 4, 1, 0);
+            case 256:
+                if (x) return TCL(4, 8, 1, 2);
+                return o.f16_cluster ? TCL(4, 8, 1, 0, 2) : TCL(4, 8, 1, 0);
             default: return 1;
         }
     }
     switch (n) {
-        case 64: return tc_launch_t<1, 2, 2, 0>(t, n, nw, A, T, y, s2, P, num_sms, st);
-        case 128: return tc_launch_t<2, 4, 2, 0>(t, n, nw, A, T, y, s2, P, num_sms, st);
-        case 256: return tc_launch_t<4, 8, 2, 0>(t, n, nw, A, T, y, s2, P, num_sms, st);
+        case 64: return TCL(1, 2, 2, 0);
+        case 128: return TCL(2, 4, 2, 0);
+        case 256: return TCL(4, 8, 2, 0);
         default: return 1;
     }
 }

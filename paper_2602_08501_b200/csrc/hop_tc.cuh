@@ -475,11 +475,12 @@ __device__ __forceinline__ uint32_t byte_mask4(uint32_t m4) { return ((m4 * 0x00
 struct Params {
     int n, nw, A, T, np, ntiles;
     const float* y;
+    const double* y64;           // MODE 3: the caller's float64 received words (y = their fp32 rounding)
     S2Dev s2;
     const uint32_t* pbits;       // np x nw
     const uint8_t* btiles;       // [ntiles][KB][256 x 64 fp16] swizzled images
     float tie_rel;
-    float err;             // bound on |S_fp32 - S_exact| (S units)
+    float cert_g;          // fp32 certification pass: |fl(S) - S| <= cert_g * sum|y| (cert_gamma)
     long long* trace;      // experiment & 128: per-tile clock64 trace of CTA 0 (TRACE_W per tile)
     int experiment;        // profiling knob: 1 skip epilogue math, 2 skip TMEM loads, 4 force T scans,
                            // 2048 int8 window overflow at 4 keys (exercises the continuation passes),
@@ -497,12 +498,15 @@ struct Params {
 // FORCE: an improving best is always re-scored (the int8 screen's scores are
 // too coarse for the running ED); best_score returns the re-scored value when
 // there is one, else the approximation.
-template <int K, int NW, bool YSMEM, bool FORCE = false>
+// Y64: the exact scores are taken from the caller's float64 received word
+// y64row (yrow holds its fp32 rounding; cert_g then covers the rounding too).
+template <int K, int NW, bool YSMEM, bool FORCE = false, bool Y64 = false>
 __device__ __forceinline__ void certify_window(const TopK<K>& t, const float* __restrict__ yrow,
                                                const uint32_t (&c)[NW], const uint32_t* __restrict__ pbits,
                                                float ed, float tie_rel, float err_row, int& best, bool& improve,
                                                float& best_approx, uint8_t& flags, uint32_t (&best_bits)[NW],
-                                               bool& have_bits, float& best_score, float ay_pre) {
+                                               bool& have_bits, float& best_score, float ay_pre, float cert_g,
+                                               const double* __restrict__ y64row) {
     const float thr = tie_rel * ed * 0.25f;
     const float win = thr + 2.0f * err_row;
     best = t.i[0];
@@ -528,10 +532,11 @@ __device__ __forceinline__ void certify_window(const TopK<K>& t, const float* __
     for (int k = 0; k < K - 1; k++)
         if (k < ncand) asm volatile("prefetch.global.L1 [%0];" ::"l"(pbits + (size_t)ci[k] * NW));
     const float4* y4 = reinterpret_cast<const float4*>(yrow);
-    // pass 1, fp32: S_k = sum over supp p_k of x_i y_i with the recursive-
-    // summation bound |fl(S_k) - S_k| <= gamma_63 * sum|y| (<= 64 terms).  If
-    // every decision below is separated by more than that bound it equals the
-    // exact one; otherwise pass 2 recomputes the sums in float64.
+    // pass 1, fp32: S_k = sum over supp p_k of x_i y_i with the summation
+    // bound |fl(S_k) - S_k| <= gamma_{wmax-1} * sum|y| (any order of at most
+    // wmax terms; cert_gamma).  If every decision below is separated by more
+    // than that bound it equals the exact one; otherwise pass 2 recomputes the
+    // sums in float64.
     {
         float s32[K - 1];
 #pragma unroll
@@ -569,9 +574,8 @@ __device__ __forceinline__ void certify_window(const TopK<K>& t, const float* __
         }
 #pragma unroll
         for (int k = 0; k < K - 1; k++) s32[k] += s32b[k];
-        // any summation order of <= 64 terms: |fl(S) - S| <= gamma_63 * sum|y|; sum|y| of
-        // the frame precomputed (warp_i8_scale, rounded up)
-        const double bnd = (double)ay_pre * (64.0 * 5.9604645e-8 * 1.001) * 1.0001;
+        // sum|y| of the frame precomputed (warp_i8_scale, rounded up)
+        const double bnd = (double)ay_pre * (double)cert_g;
         // argmin (ties -> lowest pattern index) and the runner-up, in fp32
         // (indices and approximations tracked in registers: no runtime indexing
         // of the top-K arrays, which would move them to local memory)
@@ -627,7 +631,7 @@ __device__ __forceinline__ void certify_window(const TopK<K>& t, const float* __
         double yd[16];
 #pragma unroll
         for (int bb = 0; bb < 16; bb++) {
-            const double v = (double)yv[bb];
+            const double v = Y64 ? __ldg(y64row + hw * 16 + bb) : (double)yv[bb];
             yd[bb] = ((cw >> bb) & 1u) ? -v : v;
         }
 #pragma unroll
@@ -665,7 +669,9 @@ __device__ __forceinline__ void certify_window(const TopK<K>& t, const float* __
 
 // ---------------------------------------------------------------------------
 // MODE 0: production.  MODE 1: plus the per-tile clock trace of CTA 0
-// (Params::trace).  MODE 2: plus the profiling knobs of Params::experiment.
+// (Params::trace).  MODE 2: plus the profiling knobs of Params::experiment
+// (MODE 1 and 2 are built only with -DMPW_PROFILE).  MODE 3: production with
+// float64 received words (Params::y64) for the exact re-scoring.
 // CL = 2: the CTA pair of a cluster shares one P stream (each CTA's producer
 // fetches half of every stage and multicasts it to both), halving the L2->SM
 // traffic; the pair runs its rounds in step.
@@ -673,6 +679,8 @@ template <int KB, int NW, int LIMBS, int MODE, int CL, int PM = 0>
 __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params prm) {
     constexpr int STAGES = stages_for(KB, LIMBS, CL, PM);
     constexpr bool PROF = MODE == 2;
+    constexpr bool Y64 = MODE == 3;
+    static_assert(!(Y64 && LIMBS == 0), "float64 received words use the fp16 screens");
     constexpr bool I8 = LIMBS == 0;                  // int8 screen (see the header comment)
     constexpr bool PAIR = pair_mma(LIMBS, CL, PM);   // cta_group::2 MMAs issued by the pair's rank 0
     constexpr int RSB = ring_stage_bytes(LIMBS, CL, PM);   // bytes of one ring stage in this CTA
@@ -691,7 +699,7 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
     // round-end staging of every row's received word in the (then idle) B ring
     constexpr bool YSTAGE = ROWS * (NW * 32 * 4 + 16) <= STAGES * RSB;
     const int xp = PROF ? prm.experiment : 0;
-    long long* const trace = MODE >= 1 ? prm.trace : nullptr;
+    long long* const trace = (MODE == 1 || MODE == 2) ? prm.trace : nullptr;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* sm = reinterpret_cast<unsigned char*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     if (I8 && sm != smem_raw) __trap();   // no slack in the int8 layout
@@ -1557,12 +1565,15 @@ __global__ void __launch_bounds__(threads_for(LIMBS), 1) hop_tc_kernel(Params pr
                     } else {
                         cand = top;
                     }
+                    const double* y64row = Y64 ? prm.y64 + (size_t)frame * n : nullptr;
                     if (YSTAGE)
-                        certify_window<KT, NW, true, I8>(cand, ysm, c, prm.pbits, ed, prm.tie_rel, err_row, i1,
-                                                         improve, sb, flags, pwv, have_bits, sx, ay_row);
+                        certify_window<KT, NW, true, I8, Y64>(cand, ysm, c, prm.pbits, ed, prm.tie_rel, err_row, i1,
+                                                              improve, sb, flags, pwv, have_bits, sx, ay_row,
+                                                              prm.cert_g, y64row);
                     else
-                        certify_window<KT, NW, false, I8>(cand, yrow, c, prm.pbits, ed, prm.tie_rel, err_row, i1,
-                                                          improve, sb, flags, pwv, have_bits, sx, ay_row);
+                        certify_window<KT, NW, false, I8, Y64>(cand, yrow, c, prm.pbits, ed, prm.tie_rel, err_row, i1,
+                                                               improve, sb, flags, pwv, have_bits, sx, ay_row,
+                                                               prm.cert_g, y64row);
                     if (I8) sb = sx;
                 }
                 if (!cont_more) iters++;

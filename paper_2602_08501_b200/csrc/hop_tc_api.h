@@ -16,6 +16,14 @@ struct TcPatterns {
     int kb8 = 0, ntiles8 = 0;   // int8 tiles are tc::I8_TILE patterns wide
 };
 
+// Launch options of the tensor hop (per handle, mpw_set_option)
+struct TcOpts {
+    int experiment = 0;    // Params::experiment bits (profiling / test hooks; MODE 2 kernels)
+    int i8_pair = 0;       // int8, N = 256: cta_group::2 pair kernel
+    int i8_cluster = 1;    // int8, N = 256: 2 = CTA pairs sharing the P stream by multicast
+    int f16_cluster = 1;   // 1-limb, N = 256: CTA pairs sharing the P stream (default on)
+};
+
 bool tc_supported(int n, int np);
 bool tc_i8_supported(int n, int np);
 void tc_release(TcPatterns& t);
@@ -24,5 +32,7 @@ void tc_release(TcPatterns& t);
 int tc_build(TcPatterns& t, const uint32_t* bits, int np, int n, int nw);
 // limbs: 1 or 2 fp16 limbs, 0 = int8 screen.
 // 0 on launch, -cudaError on failure, 1 for an unsupported shape
-int tc_launch(const TcPatterns& t, int n, int nw, int A, int T, const float* y, S2Dev s2, PatDev P,
-              int num_sms, int limbs, cudaStream_t st);
+// y64 (may be null): the caller's float64 received words, y their fp32
+// rounding; only the 1-limb screen takes them.
+int tc_launch(const TcPatterns& t, int n, int nw, int A, int T, const float* y, const double* y64, S2Dev s2,
+              PatDev P, int num_sms, int limbs, const TcOpts& o, cudaStream_t st);

@@ -96,8 +96,21 @@ struct mpw_handle {
     DevBuf<float4> ebound;
     DevBuf<float4> qscale;
     DevBuf<uint8_t> s1_flags;       // OSD stage-1 near-tie flags
+    // float64 inputs: fp32 rounding of y (screens) and float64 channel LLRs (stage 1)
+    DevBuf<float> y32;
+    DevBuf<double> llr64;
+    // mpw_two_stage_batch_host staging (owned by the handle, so on its device)
+    DevBuf<float> hy;
+    DevBuf<uint32_t> htx, hbest;
+    DevBuf<uint64_t> hmsg;
+    DevBuf<double> hed;
+    DevBuf<uint8_t> hstage, hflags;
+    DevBuf<int32_t> hiters;
+    DevBuf<unsigned long long> hctr;
     int wmax = 0;
     int scl_generic = 0;            // force the warp-per-frame SCL kernel
+    TcOpts tco;                     // tensor-hop launch options (mpw_set_option)
+    long long kernel_launches = 0;  // kernels this handle launched (mpw_launch_count)
     // timing
     int timing = 0;
     cudaEvent_t ev[8];
@@ -138,8 +151,8 @@ struct FinalOut {
     uint32_t* anchors; uint8_t* flags; int32_t* best_k;
 };
 
-__global__ void finalize_kernel(int n, int nw, int A, int T, const float* __restrict__ y, S2Dev s2,
-                                FinalOut out, float tie_rel) {
+__global__ void finalize_kernel(int n, int nw, int A, int T, const float* __restrict__ y,
+                                const double* __restrict__ y64, S2Dev s2, FinalOut out, float tie_rel) {
     const int lane = threadIdx.x & 31;
     const int warps = gridDim.x * (blockDim.x >> 5);
     const int count = *s2.count;
@@ -153,7 +166,7 @@ __global__ void finalize_kernel(int n, int nw, int A, int T, const float* __rest
             double acc = 0.0;
             for (int i = lane; i < n; i += 32) {
                 const double x = ((cw[i >> 5] >> (i & 31)) & 1u) ? -1.0 : 1.0;
-                const double d = (double)y[(size_t)f * n + i] - x;
+                const double d = (y64 ? y64[(size_t)f * n + i] : (double)y[(size_t)f * n + i]) - x;
                 acc += d * d;
             }
 #pragma unroll
@@ -261,13 +274,26 @@ __global__ void frame_kernel(FrameArgs fa) {
 
 // mp_wsd API: queue = identity over the given frames
 // (warp per frame: also the per-frame score error bounds the hop kernels use)
+// float64 inputs: every screen bound also covers sum_{supp}|y64_i - y_i| <=
+// the sum of the wmax largest fp32 rounding errors of the frame
+__device__ __forceinline__ float4 widen_for_y64(float4 eb, const float* __restrict__ yrow,
+                                                const double* __restrict__ y64row, int n, int wmax) {
+    float r[32];
+    int cnt = 0;
+    for (int i = threadIdx.x & 31; i < n; i += 32, cnt++)
+        r[cnt] = __double2float_ru(fabs(y64row[i] - (double)yrow[i]));
+    const float R = warp_topw_bound(r, cnt, wmax);
+    return make_float4(eb.x + R, eb.y + R, eb.z + R, eb.w);
+}
+
 __global__ void queue_identity_kernel(int F, int A, int n, const float* __restrict__ y,
-                                      const int32_t* nanchor, S2Dev s2) {
+                                      const double* __restrict__ y64, const int32_t* nanchor, S2Dev s2) {
     const int lane = threadIdx.x & 31;
     const int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (q == 0 && lane == 0) *s2.count = F;
     if (q < F) {
-        const float4 eb = warp_error_bounds(y + (size_t)q * n, n, s2.wmax);
+        float4 eb = warp_error_bounds(y + (size_t)q * n, n, s2.wmax);
+        if (y64) eb = widen_for_y64(eb, y + (size_t)q * n, y64 + (size_t)q * n, n, s2.wmax);
         const float4 qs = warp_i8_scale(y + (size_t)q * n, n, s2.wmax);
         if (lane == 0) {
             s2.frame[q] = q;
@@ -279,19 +305,52 @@ __global__ void queue_identity_kernel(int F, int A, int n, const float* __restri
 }
 
 // per-frame score error bounds of the queued stage-2 frames (warp per entry)
-__global__ void ebound_kernel(int n, const float* __restrict__ y, S2Dev s2) {
+__global__ void ebound_kernel(int n, const float* __restrict__ y, const double* __restrict__ y64, S2Dev s2) {
     const int lane = threadIdx.x & 31;
     const int warps = gridDim.x * (blockDim.x >> 5);
     const int count = *s2.count;
     for (int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); q < count; q += warps) {
         const float* yr = y + (size_t)s2.frame[q] * n;
-        const float4 eb = warp_error_bounds(yr, n, s2.wmax);
+        float4 eb = warp_error_bounds(yr, n, s2.wmax);
+        if (y64) eb = widen_for_y64(eb, yr, y64 + (size_t)s2.frame[q] * n, n, s2.wmax);
         const float4 qs = warp_i8_scale(yr, n, s2.wmax);
         if (lane == 0) { s2.ebound[q] = eb; s2.qscale[q] = qs; }
     }
 }
 
-int ensure_s2(mpw_handle* h, int F, int A, int T) {
+// float64 inputs: fp32 rounding for the screens and float64 channel LLRs
+// 2.0 * y / (sigma * sigma) with the reference's operation order (decoders.py:550)
+__global__ void y64_prep_kernel(long long total, const double* __restrict__ y64, float* __restrict__ y32,
+                                double* __restrict__ llr, double sigma) {
+    const double sig2 = sigma * sigma;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+         i += (long long)gridDim.x * blockDim.x) {
+        const double v = y64[i];
+        y32[i] = __double2float_rn(v);
+        if (llr) llr[i] = 2.0 * v / sig2;
+    }
+}
+
+// float64 inputs: canonical squared EDs of the stage-1 (CRC-pass) frames from y64
+__global__ void stage1_ed64_kernel(int F, int n, int nw, const double* __restrict__ y64, const uint8_t* stage,
+                                   const uint32_t* __restrict__ best, double* best_ed) {
+    const int lane = threadIdx.x & 31;
+    const int f = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (f >= F || stage[f] != 0) return;
+    double acc = 0.0;
+    for (int i = lane; i < n; i += 32) {
+        const double x = ((best[(size_t)f * nw + (i >> 5)] >> (i & 31)) & 1u) ? -1.0 : 1.0;
+        const double d = y64[(size_t)f * n + i] - x;
+        acc += d * d;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(MPW_FULL, acc, o);
+    if (lane == 0) best_ed[f] = acc;
+}
+
+// want_hops: the caller asked for the per-hop pattern log (else the hop
+// kernels skip writing it: s2.traj_hops = null)
+int ensure_s2(mpw_handle* h, int F, int A, int T, bool want_hops) {
     const size_t traj = (size_t)F * A;
     CK(h->s2_count.ensure(1));
     CK(h->work_next.ensure(1));
@@ -300,18 +359,18 @@ int ensure_s2(mpw_handle* h, int F, int A, int T) {
     CK(h->s2_anchors.ensure(traj * h->nw));
     CK(h->traj_cw.ensure(traj * h->nw));
     CK(h->traj_iters.ensure(traj));
-    CK(h->traj_hops.ensure(traj * T));
+    if (want_hops) CK(h->traj_hops.ensure(traj * T));
     CK(h->traj_flags.ensure(traj));
     CK(h->ebound.ensure(F));
     CK(h->qscale.ensure(F));
     return 0;
 }
 
-S2Dev s2_dev(mpw_handle* h, const uint32_t* anchors_override) {
+S2Dev s2_dev(mpw_handle* h, const uint32_t* anchors_override, bool want_hops) {
     S2Dev s;
     s.count = h->s2_count.p; s.frame = h->s2_frame.p; s.nanchor = h->s2_nanchor.p;
     s.anchors = anchors_override ? const_cast<uint32_t*>(anchors_override) : h->s2_anchors.p;
-    s.traj_cw = h->traj_cw.p; s.traj_iters = h->traj_iters.p; s.traj_hops = h->traj_hops.p;
+    s.traj_cw = h->traj_cw.p; s.traj_iters = h->traj_iters.p; s.traj_hops = want_hops ? h->traj_hops.p : nullptr;
     s.traj_flags = h->traj_flags.p; s.work_next = h->work_next.p;
     s.ebound = h->ebound.p; s.qscale = h->qscale.p; s.wmax = h->wmax;
     return s;
@@ -348,6 +407,7 @@ int launch_scl(mpw_handle* h, const float* y, const double* llr64, int F, double
     const int grid = (int)std::max<long long>(1, std::min<long long>(need, (long long)per_sm * h->num_sms * 4));
     scl_kernel<NW><<<grid, 32 * wpb, smem, st>>>(code_dev(h), y, llr64, F, sigma, L, A, mode, out, s2);
     CK(cudaGetLastError());
+    h->kernel_launches++;
     return 0;
 }
 
@@ -359,7 +419,7 @@ int dispatch_scl(mpw_handle* h, const float* y, const double* llr64, int F, doub
     const bool pow2 = L >= 1 && (L & (L - 1)) == 0 && L <= 32;
     if (pow2 && !h->scl_generic) {
         const int rc = scl_lane_launch(h->n, L, code_dev(h), y, llr64, F, sigma, A, mode, out, s2, h->num_sms, st);
-        if (rc == 0) return 0;
+        if (rc == 0) { h->kernel_launches++; return 0; }
         if (rc < 0) return fail(MPW_ERR_CUDA, "SCL lane kernel launch failed: %s", cudaGetErrorString((cudaError_t)-rc));
     }
     switch (h->nw) {
@@ -390,6 +450,7 @@ int launch_gather(mpw_handle* h, HopParams hp, int max_traj, cudaStream_t st) {
     const int grid = (int)std::max<long long>(1, std::min<long long>(need, (long long)per_sm * h->num_sms));
     hop_gather_kernel<NW><<<grid, 32 * wpb, smem, st>>>(hp);
     CK(cudaGetLastError());
+    h->kernel_launches++;
     return 0;
 }
 
@@ -397,30 +458,36 @@ int launch_gather(mpw_handle* h, HopParams hp, int max_traj, cudaStream_t st) {
 // its wider certification window (N = 256 and >= 32 tiles of 256 patterns:
 // cfg4 0.71x the f16 hop time; slower on cfg2/cfg3), else one fp16 limb, else
 // the gather kernel
-int resolve_variant(mpw_handle* h, int variant) {
+// float64 inputs (f64): the 1-limb fp16 screen with float64 re-scoring, else
+// the gather kernel
+int resolve_variant(mpw_handle* h, int variant, bool f64 = false) {
     if (variant != MPW_HOP_AUTO) return variant;
     if (!(tc_supported(h->n, h->np) && h->tcp.ready)) return MPW_HOP_GATHER;
-    if (h->tcp.ready8 && h->n >= 256 && h->tcp.ntiles >= 32) return MPW_HOP_TENSOR_I8;
+    if (!f64 && h->tcp.ready8 && h->n >= 256 && h->tcp.ntiles >= 32) return MPW_HOP_TENSOR_I8;
     return MPW_HOP_TENSOR;
 }
 
-int run_hops(mpw_handle* h, const float* y, int Fmax, int A, int T, int variant, S2Dev s2, cudaStream_t st) {
-    variant = resolve_variant(h, variant);
+int run_hops(mpw_handle* h, const float* y, const double* y64, int Fmax, int A, int T, int variant, S2Dev s2,
+             cudaStream_t st) {
+    variant = resolve_variant(h, variant, y64 != nullptr);
+    if (y64 && (variant == MPW_HOP_TENSOR_2LIMB || variant == MPW_HOP_TENSOR_I8))
+        return fail(MPW_ERR_UNSUPPORTED, "float64 received words use the 1-limb tensor or the gather hop");
     if (variant == MPW_HOP_TENSOR || variant == MPW_HOP_TENSOR_2LIMB || variant == MPW_HOP_TENSOR_I8) {
         if (!h->tcp.ready) return fail(MPW_ERR_UNSUPPORTED, "tensor-core hop operand not built for this pattern set");
         if (variant == MPW_HOP_TENSOR_I8 && !h->tcp.ready8)
             return fail(MPW_ERR_UNSUPPORTED, "int8 tensor-core hop needs N = 128 or 256");
         const int limbs = variant == MPW_HOP_TENSOR ? 1 : variant == MPW_HOP_TENSOR_2LIMB ? 2 : 0;
-        int rc = tc_launch(h->tcp, h->n, h->nw, A, T, y, s2, pat_dev(h), h->num_sms, limbs, st);
+        int rc = tc_launch(h->tcp, h->n, h->nw, A, T, y, y64, s2, pat_dev(h), h->num_sms, limbs, h->tco, st);
         if (rc) return fail(MPW_ERR_CUDA, "tensor-core hop launch failed: %s",
                             rc < 0 ? cudaGetErrorString((cudaError_t)-rc) : "unsupported shape");
+        h->kernel_launches++;
         return 0;
     }
+    if (variant != MPW_HOP_GATHER) return fail(MPW_ERR_ARG, "unknown hop variant %d", variant);
     HopParams hp;
-    hp.n = h->n; hp.nw = h->nw; hp.A = A; hp.T = T; hp.y = y; hp.s2 = s2; hp.P = pat_dev(h);
+    hp.n = h->n; hp.nw = h->nw; hp.A = A; hp.T = T; hp.y = y; hp.y64 = y64; hp.s2 = s2; hp.P = pat_dev(h);
     hp.sup = h->sup.p; hp.soff = h->soff.p; hp.sup_in_smem = 0; hp.total_sup_u4 = h->total_sup_u4;
     hp.tie_rel = 1e-5f;
-    hp.err = 1e-3f;
     const int max_traj = Fmax * A;
     switch (h->nw) {
         case 1: return launch_gather<1>(h, hp, max_traj, st);
@@ -433,10 +500,25 @@ int run_hops(mpw_handle* h, const float* y, int Fmax, int A, int T, int variant,
     }
 }
 
-int finalize(mpw_handle* h, const float* y, int Fmax, int A, int T, S2Dev s2, FinalOut fo, cudaStream_t st) {
+int finalize(mpw_handle* h, const float* y, const double* y64, int Fmax, int A, int T, S2Dev s2, FinalOut fo,
+             cudaStream_t st) {
     const int grid = std::max(1, std::min((Fmax + 7) / 8, h->num_sms * 8));
-    finalize_kernel<<<grid, 256, 0, st>>>(h->n, h->nw, A, T, y, s2, fo, 1e-5f);
+    finalize_kernel<<<grid, 256, 0, st>>>(h->n, h->nw, A, T, y, y64, s2, fo, 1e-5f);
     CK(cudaGetLastError());
+    h->kernel_launches++;
+    return 0;
+}
+
+// float64 inputs: y32 = fp32(y64) into the handle's scratch (and the channel
+// LLRs when llr is wanted)
+int prep_y64(mpw_handle* h, const double* y64, int F, double sigma, bool llr, cudaStream_t st) {
+    const size_t total = (size_t)F * h->n;
+    CK(h->y32.ensure(total));
+    if (llr) CK(h->llr64.ensure(total));
+    const int grid = (int)std::max<size_t>(1, std::min<size_t>((total + 255) / 256, (size_t)h->num_sms * 16));
+    y64_prep_kernel<<<grid, 256, 0, st>>>((long long)total, y64, h->y32.p, llr ? h->llr64.p : nullptr, sigma);
+    CK(cudaGetLastError());
+    h->kernel_launches++;
     return 0;
 }
 
@@ -479,6 +561,9 @@ void mpw_destroy(mpw_handle* h) {
     h->pidx.release(); h->sup.release(); h->s2_count.release(); h->s2_frame.release();
     h->s2_nanchor.release(); h->traj_iters.release(); h->traj_hops.release(); h->work_next.release();
     h->s2_anchors.release(); h->traj_cw.release(); h->traj_flags.release(); h->ebound.release(); h->qscale.release(); h->s1_flags.release();
+    h->y32.release(); h->llr64.release();
+    h->hy.release(); h->htx.release(); h->hbest.release(); h->hmsg.release(); h->hed.release();
+    h->hstage.release(); h->hflags.release(); h->hiters.release(); h->hctr.release();
     tc_release(h->tcp);
     if (h->ev_init) for (int i = 0; i < 8; i++) cudaEventDestroy(h->ev[i]);
     delete h;
@@ -621,25 +706,48 @@ int mpw_scl_batch(mpw_handle* h, const float* y, const double* llr, int F, doubl
     return dispatch_scl(h, y, llr, F, sigma, L, 0, 0, out, s2, st);
 }
 
+extern "C++" {
+namespace {
+int mpwsd_impl(mpw_handle* h, const float* y, const double* y64, const uint32_t* anchors, const int32_t* n_anchor,
+               int F, int A, int T, int variant, uint32_t* best, double* best_ed, int32_t* iters, int32_t* hops,
+               uint8_t* flags, cudaStream_t st) {
+    if (!h->has_pat) return fail(MPW_ERR_STATE, "no pattern set");
+    if (set_device(h)) return MPW_ERR_CUDA;
+    if (y64) {
+        if (int rc = prep_y64(h, y64, F, 1.0, false, st)) return rc;
+        y = h->y32.p;
+    }
+    if (int rc = ensure_s2(h, F, A, T, hops != nullptr)) return rc;
+    S2Dev s2 = s2_dev(h, anchors, hops != nullptr);
+    CK(cudaMemsetAsync(s2.work_next, 0, sizeof(int32_t), st));
+    queue_identity_kernel<<<(F + 7) / 8, 256, 0, st>>>(F, A, h->n, y, y64, n_anchor, s2);
+    CK(cudaGetLastError());
+    h->kernel_launches++;
+    if (int rc = run_hops(h, y, y64, F, A, T, variant, s2, st)) return rc;
+    FinalOut fo{best, best_ed, nullptr, iters, hops, nullptr, flags, nullptr};
+    return finalize(h, y, y64, F, A, T, s2, fo, st);
+}
+}  // namespace
+}  // extern "C++"
+
 int mpw_mpwsd_batch(mpw_handle* h, const float* y, const uint32_t* anchors, const int32_t* n_anchor,
                     int F, int A, int T, int variant, uint32_t* best, double* best_ed,
                     int32_t* iters, int32_t* hops, uint8_t* flags, void* stream) {
     if (!h || F < 0 || A < 1 || T < 1) return fail(MPW_ERR_ARG, "bad arguments");
     if (F == 0) return 0;
     if (!y || !anchors || !best || !best_ed) return fail(MPW_ERR_ARG, "bad arguments");
-    if (!h->has_pat) return fail(MPW_ERR_STATE, "no pattern set");
+    return mpwsd_impl(h, y, nullptr, anchors, n_anchor, F, A, T, variant, best, best_ed, iters, hops, flags,
+                      (cudaStream_t)stream);
+}
+
+int mpw_mpwsd_batch_f64(mpw_handle* h, const double* y, const uint32_t* anchors, const int32_t* n_anchor,
+                        int F, int A, int T, int variant, uint32_t* best, double* best_ed,
+                        int32_t* iters, int32_t* hops, uint8_t* flags, void* stream) {
+    if (!h || F < 0 || A < 1 || T < 1) return fail(MPW_ERR_ARG, "bad arguments");
     if (F == 0) return 0;
-    if (set_device(h)) return MPW_ERR_CUDA;
-    cudaStream_t st = (cudaStream_t)stream;
-    if (int rc = ensure_s2(h, F, A, T)) return rc;
-    S2Dev s2 = s2_dev(h, anchors);
-    if (!hops) s2.traj_hops = h->traj_hops.p;
-    CK(cudaMemsetAsync(s2.work_next, 0, sizeof(int32_t), st));
-    queue_identity_kernel<<<(F + 7) / 8, 256, 0, st>>>(F, A, h->n, y, n_anchor, s2);
-    CK(cudaGetLastError());
-    if (int rc = run_hops(h, y, F, A, T, variant, s2, st)) return rc;
-    FinalOut fo{best, best_ed, nullptr, iters, hops, nullptr, flags, nullptr};
-    return finalize(h, y, F, A, T, s2, fo, st);
+    if (!y || !anchors || !best || !best_ed) return fail(MPW_ERR_ARG, "bad arguments");
+    return mpwsd_impl(h, nullptr, y, anchors, n_anchor, F, A, T, variant, best, best_ed, iters, hops, flags,
+                      (cudaStream_t)stream);
 }
 
 extern "C++" {
@@ -669,6 +777,7 @@ int launch_osd_nw(mpw_handle* h, const OsdArgs& a, cudaStream_t st) {
     const int grid = std::max(1, std::min((a.F + OSD_WARPS - 1) / OSD_WARPS, h->num_sms * std::max(per_sm, 1)));
     osd_kernel<NW><<<grid, 32 * OSD_WARPS, smem, st>>>(a);
     CK(cudaGetLastError());
+    h->kernel_launches++;
     return 0;
 }
 
@@ -692,15 +801,19 @@ int osd_check(mpw_handle* h, int order) {
     return 0;
 }
 
-int two_stage_impl(mpw_handle* h, const float* y, int F, const Stage1& s1, int A, int T, int mode, int variant,
-                   const uint32_t* tx_cw, uint32_t* best, uint64_t* best_msg, double* best_ed, uint8_t* stage,
-                   int32_t* iters, int32_t* hops, uint32_t* anchors_out, uint8_t* flags,
-                   unsigned long long* counters, cudaStream_t st) {
+// y64 (may be null): float64 received words; y is then ignored and replaced by
+// their fp32 rounding (screens), stage 1 runs from float64 LLRs, and the exact
+// re-scoring and every reported ED use y64.
+int two_stage_impl(mpw_handle* h, const float* y, const double* y64, int F, const Stage1& s1, int A, int T,
+                   int mode, int variant, const uint32_t* tx_cw, uint32_t* best, uint64_t* best_msg,
+                   double* best_ed, uint8_t* stage, int32_t* iters, int32_t* hops, uint32_t* anchors_out,
+                   uint8_t* flags, unsigned long long* counters, cudaStream_t st) {
     if (mode != MPW_MODE_CRC_GATED && mode != MPW_MODE_ALWAYS_ON) return fail(MPW_ERR_ARG, "unknown activation mode %d", mode);
     if (mode == MPW_MODE_CRC_GATED && !h->is_ca) return fail(MPW_ERR_ARG, "crc_gated mode requires a CRC-concatenated code");
+    if (y64 && s1.osd) return fail(MPW_ERR_UNSUPPORTED, "OSD stage 1 takes float32 received words");
     if (set_device(h)) return MPW_ERR_CUDA;
-    if (int rc = ensure_s2(h, F, A, T)) return rc;
-    S2Dev s2 = s2_dev(h, nullptr);
+    if (int rc = ensure_s2(h, F, A, T, hops != nullptr)) return rc;
+    S2Dev s2 = s2_dev(h, nullptr, hops != nullptr);
     if (h->timing && !h->ev_init) {
         for (int i = 0; i < 8; i++) CK(cudaEventCreate(&h->ev[i]));
         h->ev_init = true;
@@ -708,11 +821,16 @@ int two_stage_impl(mpw_handle* h, const float* y, int F, const Stage1& s1, int A
     CK(cudaMemsetAsync(s2.count, 0, sizeof(int32_t), st));
     CK(cudaMemsetAsync(s2.work_next, 0, sizeof(int32_t), st));
     timing_mark(h, 0, st);
+    if (y64) {
+        if (int rc = prep_y64(h, y64, F, s1.sigma, true, st)) return rc;
+        y = h->y32.p;
+    }
     SclOut out{nullptr, nullptr, nullptr, nullptr, stage, best, best_ed};
     const int smode = (mode == MPW_MODE_CRC_GATED) ? 1 : 2;
     const uint8_t* s1flags = nullptr;
     if (!s1.osd) {
-        if (int rc = dispatch_scl(h, y, nullptr, F, s1.sigma, s1.L, A, smode, out, s2, st)) return rc;
+        if (int rc = dispatch_scl(h, y, y64 ? h->llr64.p : nullptr, F, s1.sigma, s1.L, A, smode, out, s2, st))
+            return rc;
     } else {
         CK(h->s1_flags.ensure(F));
         OsdArgs a{};
@@ -725,13 +843,19 @@ int two_stage_impl(mpw_handle* h, const float* y, int F, const Stage1& s1, int A
         if (int rc = launch_osd(h, a, st)) return rc;
         s1flags = h->s1_flags.p;
     }
-    ebound_kernel<<<std::max(1, std::min((F + 7) / 8, h->num_sms * 16)), 256, 0, st>>>(h->n, y, s2);
+    ebound_kernel<<<std::max(1, std::min((F + 7) / 8, h->num_sms * 16)), 256, 0, st>>>(h->n, y, y64, s2);
     CK(cudaGetLastError());
+    h->kernel_launches++;
     timing_mark(h, 1, st);
-    if (int rc = run_hops(h, y, F, A, T, variant, s2, st)) return rc;
+    if (int rc = run_hops(h, y, y64, F, A, T, variant, s2, st)) return rc;
     timing_mark(h, 2, st);
     FinalOut fo{best, best_ed, stage, iters, hops, anchors_out, flags, nullptr};
-    if (int rc = finalize(h, y, F, A, T, s2, fo, st)) return rc;
+    if (int rc = finalize(h, y, y64, F, A, T, s2, fo, st)) return rc;
+    if (y64) {
+        stage1_ed64_kernel<<<(F + 7) / 8, 256, 0, st>>>(F, h->n, h->nw, y64, stage, best, best_ed);
+        CK(cudaGetLastError());
+        h->kernel_launches++;
+    }
     timing_mark(h, 3, st);
     FrameArgs fa;
     fa.F = F; fa.A = A; fa.T = T; fa.nw = h->nw; fa.k = h->k; fa.np = h->np;
@@ -739,6 +863,7 @@ int two_stage_impl(mpw_handle* h, const float* y, int F, const Stage1& s1, int A
     fa.msg_out = best_msg; fa.s1flags = s1flags; fa.counters = counters; fa.pivots = h->pivots.p; fa.mix = h->mix.p;
     frame_kernel<<<(F + 255) / 256, 256, 0, st>>>(fa);
     CK(cudaGetLastError());
+    h->kernel_launches++;
     timing_mark(h, 4, st);
     return timing_close(h);
 }
@@ -756,8 +881,22 @@ int mpw_two_stage_batch(mpw_handle* h, const float* y, int F, double sigma, int 
     if (!h->has_code || !h->has_pat) return fail(MPW_ERR_STATE, "code and pattern set must be set first");
     if (L < 1 || L > SCL_MAX_L) return fail(MPW_ERR_UNSUPPORTED, "list size %d outside [1,%d]", L, SCL_MAX_L);
     Stage1 s1{0, sigma, L, 0, 0};
-    return two_stage_impl(h, y, F, s1, A, T, mode, variant, tx_cw, best, best_msg, best_ed, stage, iters, hops,
-                          anchors_out, flags, counters, (cudaStream_t)stream);
+    return two_stage_impl(h, y, nullptr, F, s1, A, T, mode, variant, tx_cw, best, best_msg, best_ed, stage, iters,
+                          hops, anchors_out, flags, counters, (cudaStream_t)stream);
+}
+
+int mpw_two_stage_batch_f64(mpw_handle* h, const double* y, int F, double sigma, int L, int A, int T,
+                            int mode, int variant, const uint32_t* tx_cw, uint32_t* best, uint64_t* best_msg,
+                            double* best_ed, uint8_t* stage, int32_t* iters, int32_t* hops,
+                            uint32_t* anchors_out, uint8_t* flags, unsigned long long* counters, void* stream) {
+    if (!h || F < 0 || A < 1 || T < 1) return fail(MPW_ERR_ARG, "bad arguments");
+    if (F == 0) return 0;
+    if (!y || !best || !best_ed || !stage) return fail(MPW_ERR_ARG, "bad arguments");
+    if (!h->has_code || !h->has_pat) return fail(MPW_ERR_STATE, "code and pattern set must be set first");
+    if (L < 1 || L > SCL_MAX_L) return fail(MPW_ERR_UNSUPPORTED, "list size %d outside [1,%d]", L, SCL_MAX_L);
+    Stage1 s1{0, sigma, L, 0, 0};
+    return two_stage_impl(h, nullptr, y, F, s1, A, T, mode, variant, tx_cw, best, best_msg, best_ed, stage, iters,
+                          hops, anchors_out, flags, counters, (cudaStream_t)stream);
 }
 
 int mpw_two_stage_osd_batch(mpw_handle* h, const float* y, int F, int order, int list_cap, int A, int T,
@@ -771,8 +910,8 @@ int mpw_two_stage_osd_batch(mpw_handle* h, const float* y, int F, int order, int
     if (int rc = osd_check(h, order)) return rc;
     if (A > OSD_MAX_KEEP - 1) return fail(MPW_ERR_UNSUPPORTED, "num_paths %d > %d", A, OSD_MAX_KEEP - 1);
     Stage1 s1{1, 1.0, 0, order, list_cap};
-    return two_stage_impl(h, y, F, s1, A, T, mode, variant, tx_cw, best, best_msg, best_ed, stage, iters, hops,
-                          anchors_out, flags, counters, (cudaStream_t)stream);
+    return two_stage_impl(h, y, nullptr, F, s1, A, T, mode, variant, tx_cw, best, best_msg, best_ed, stage, iters,
+                          hops, anchors_out, flags, counters, (cudaStream_t)stream);
 }
 
 extern "C++" {
@@ -805,6 +944,7 @@ int osd_full_list(mpw_handle* h, OsdArgs a, cudaStream_t st) {
     if (int rc = launch_osd_nw<NW>(h, a, st)) { cleanup(); return rc; }
     osd_iota_kernel<<<std::max(1, std::min<int>((int)((total + 255) / 256), h->num_sms * 8)), 256, 0, st>>>(
         vals.p, offs.p, a.C, a.F);
+    h->kernel_launches++;
     if (a.F + 1 > h->num_sms * 8 * 256) { cleanup(); return fail(MPW_ERR_UNSUPPORTED, "batch too large"); }
     size_t tb = 0;
     e = cub::DeviceSegmentedSort::StableSortPairs(nullptr, tb, keys.p, keys_out.p, vals.p, vals_out.p, (int)total,
@@ -817,6 +957,7 @@ int osd_full_list(mpw_handle* h, OsdArgs a, cudaStream_t st) {
         const int grid = std::max(1, std::min((a.F + OSD_WARPS - 1) / OSD_WARPS, h->num_sms * 4));
         osd_materialize_kernel<NW><<<grid, 32 * OSD_WARPS, 0, st>>>(a, vals_out.p, keys_out.p);
         e = cudaGetLastError();
+        h->kernel_launches++;
     }
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);    // scratch is freed below
     cleanup();
@@ -861,13 +1002,14 @@ int mpw_two_stage_batch_host(mpw_handle* h, const float* y_host, int F, double s
     if (set_device(h)) return MPW_ERR_CUDA;
     cudaStream_t st = (cudaStream_t)stream;
     const int n = h->n, nw = h->nw;
-    static thread_local DevBuf<float> dy;
-    static thread_local DevBuf<uint32_t> dtx, dbest;
-    static thread_local DevBuf<uint64_t> dmsg;
-    static thread_local DevBuf<double> ded;
-    static thread_local DevBuf<uint8_t> dstage, dflags;
-    static thread_local DevBuf<int32_t> diters;
-    static thread_local DevBuf<unsigned long long> dctr;
+    // staging buffers owned by the handle (allocated on its device)
+    DevBuf<float>& dy = h->hy;
+    DevBuf<uint32_t>&dtx = h->htx, &dbest = h->hbest;
+    DevBuf<uint64_t>& dmsg = h->hmsg;
+    DevBuf<double>& ded = h->hed;
+    DevBuf<uint8_t>&dstage = h->hstage, &dflags = h->hflags;
+    DevBuf<int32_t>& diters = h->hiters;
+    DevBuf<unsigned long long>& dctr = h->hctr;
     CK(dy.ensure((size_t)F * n)); CK(dbest.ensure((size_t)F * nw)); CK(dmsg.ensure(F)); CK(ded.ensure(F));
     CK(dstage.ensure(F)); CK(dflags.ensure(F)); CK(diters.ensure((size_t)F * A)); CK(dctr.ensure(MPW_NUM_COUNTERS));
     CK(cudaMemcpyAsync(dy.p, y_host, sizeof(float) * (size_t)F * n, cudaMemcpyHostToDevice, st));
@@ -903,6 +1045,7 @@ int mpw_channel_batch(mpw_handle* h, uint64_t seed, int snr_idx, long long first
     const int grid = std::max(1, std::min((F + 7) / 8, h->num_sms * 32));
     channel_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(a);
     CK(cudaGetLastError());
+    h->kernel_launches++;
     return 0;
 }
 
@@ -918,6 +1061,7 @@ cudaError_t launch_enum(const mpw_handle* h, int lb, const uint32_t* table, int 
     const long long want = (nhigh + 255) / 256;
     const int grid = (int)std::max(1ll, std::min<long long>(want, (long long)h->num_sms * 8));
     enum_kernel<NW><<<grid, 256, smem>>>(h->gen.p, h->k, h->n, lb, table, nhigh, cap, spec, out, cnt, out_cap);
+    const_cast<mpw_handle*>(h)->kernel_launches++;
     return cudaGetLastError();
 }
 }  // namespace
@@ -987,6 +1131,15 @@ int mpw_set_option(mpw_handle* h, const char* key, int value) {
     if (!h || !key) return fail(MPW_ERR_ARG, "null argument");
     if (!strcmp(key, "scl_generic")) { h->scl_generic = value ? 1 : 0; return 0; }
     if (!strcmp(key, "timing")) { h->timing = value ? 1 : 0; return 0; }
+    // tensor-hop launch options (TcOpts): A/B variants and test hooks
+    if (!strcmp(key, "hop_experiment")) { h->tco.experiment = value; return 0; }
+    if (!strcmp(key, "i8_pair")) { h->tco.i8_pair = value ? 1 : 0; return 0; }
+    if (!strcmp(key, "i8_cluster")) {
+        if (value != 1 && value != 2) return fail(MPW_ERR_ARG, "i8_cluster must be 1 or 2");
+        h->tco.i8_cluster = value;
+        return 0;
+    }
+    if (!strcmp(key, "f16_cluster")) { h->tco.f16_cluster = value ? 1 : 0; return 0; }
     return fail(MPW_ERR_ARG, "unknown option '%s'", key);
 }
 
@@ -1007,6 +1160,8 @@ int mpw_read_timing(mpw_handle* h, double* ms_out /*4*/, long long* launches_out
 }
 
 int mpw_num_patterns(mpw_handle* h) { return h ? h->np : -1; }
+
+long long mpw_launch_count(mpw_handle* h) { return h ? h->kernel_launches : -1; }
 
 int mpw_tensor_path_ready(mpw_handle* h) { return (h && h->tcp.ready) ? 1 : 0; }
 

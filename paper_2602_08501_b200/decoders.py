@@ -13,10 +13,19 @@ Same names, arguments, return types and errors as
 plus the throughput entry point `DeviceDecoder.two_stage_batch` /
 `two_stage_decode_batch` over [F, N] batches.  Every call runs the sm_100a
 kernels of libmpwsd.so; there is no CPU fallback (a missing library or GPU
-raises).  Received words are float32 on the device (the path's dtype);
-stage 1 computes LLRs and path metrics in float64 and is bit-exact with the
-reference; hop decisions agree with the reference except at near-ties
-(|ΔED| gaps < 1e-5 relative), which are flagged per frame.
+raises).  Batches of float32 received words run the float32 path (the
+bench's dtype); float64 received words -- what the per-frame API receives,
+since the reference coerces y to float64 (decoders.py:411, 466, 538) -- run
+the *_f64 entry points: stage 1 from the float64 LLRs, hop screens on the
+fp32 rounding with widened error bounds, exact re-scoring and every ED from
+the float64 values.  Stage 1 is bit-exact with the reference (float64 path
+metrics); hop decisions equal exact arithmetic, near-ties (|ΔED| gaps < 1e-5
+relative) are reported per frame.
+
+Thread safety: the reference's sweep calls these functions from a thread
+pool (simharness.py:318-330).  A libmpwsd handle serves one host thread at a
+time, so the per-frame functions keep one DeviceDecoder per (thread, code,
+sphere) and issue their work on that thread's current torch stream.
 
 Code and sphere arguments may be this package's objects or the reference's
 (duck-typed on n, k, kind, info_set, crc, inner, generator.words,
@@ -27,6 +36,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import threading
 import weakref
 from dataclasses import dataclass
 
@@ -176,6 +186,17 @@ def _dev_tensor(a, dtype, device):
     return torch.from_numpy(arr).to(device=device, dtype=dtype).contiguous()
 
 
+def _is_f64(y) -> bool:
+    """float64 received words select the *_f64 entry points."""
+    dt = getattr(y, "dtype", None)
+    if dt is None:
+        return False
+    torch = _torch() if "torch" in str(type(y)) else None
+    if torch is not None:
+        return dt == torch.float64
+    return np.dtype(dt) == np.float64
+
+
 def _ptr(t):
     return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
 
@@ -295,13 +316,15 @@ class DeviceDecoder:
             raise ValueError("crc_gated mode requires a CRC-concatenated code")
         if not self.scl_ok:
             raise ValueError("SCL stage requires a polar or CRC-polar code")
-        yd = _dev_tensor(y, torch.float32, self.device)
+        f64 = _is_f64(y)
+        yd = _dev_tensor(y, torch.float64 if f64 else torch.float32, self.device)
         F = int(yd.shape[0])
         A, T, nw = int(num_paths), int(max_iterations), self.nw
         o = out if out is not None else self.alloc_outputs(F, A, T, want_hops, want_anchors)
         txd = None if tx_words is None else _dev_tensor(tx_words, torch.int32, self.device)
         ctr = counters if counters is not None else o.get("counters")
-        rc = _native.lib().mpw_two_stage_batch(
+        fn = _native.lib().mpw_two_stage_batch_f64 if f64 else _native.lib().mpw_two_stage_batch
+        rc = fn(
             self._h, _ptr(yd), F, float(sigma), int(list_size), A, T,
             _native.MODE_CRC_GATED if activation_mode == "crc_gated" else _native.MODE_ALWAYS_ON,
             _HOP[variant], _ptr(txd), _ptr(o["best"]), _ptr(o["best_msg"]), _ptr(o["best_ed"]),
@@ -381,7 +404,8 @@ class DeviceDecoder:
                      variant: str = "auto", stream=None):
         """anchors: [F, A, nw] uint32 device layout.  Returns dict of device tensors."""
         torch = _torch()
-        yd = _dev_tensor(y, torch.float32, self.device)
+        f64 = _is_f64(y)
+        yd = _dev_tensor(y, torch.float64 if f64 else torch.float32, self.device)
         ad = _dev_tensor(anchors_words32, torch.int32, self.device)
         F, A = int(ad.shape[0]), int(ad.shape[1])
         T = int(max_iterations)
@@ -392,7 +416,8 @@ class DeviceDecoder:
                  iters=torch.empty((F, A), dtype=torch.int32, device=d),
                  hops=torch.empty((F, A, T), dtype=torch.int32, device=d),
                  flags=torch.empty((F,), dtype=torch.uint8, device=d))
-        rc = _native.lib().mpw_mpwsd_batch(
+        fn = _native.lib().mpw_mpwsd_batch_f64 if f64 else _native.lib().mpw_mpwsd_batch
+        rc = fn(
             self._h, _ptr(yd), _ptr(ad), _ptr(nad), F, A, T, _HOP[variant], _ptr(o["best"]),
             _ptr(o["best_ed"]), _ptr(o["iters"]), _ptr(o["hops"]), _ptr(o["flags"]), self._stream(stream))
         _native.value_error_check(rc, "mpw_mpwsd_batch")
@@ -425,6 +450,17 @@ class DeviceDecoder:
     def message_of_words(self, cw_words64: np.ndarray) -> np.ndarray:
         return message_words(self._pivots, self._mix, unpack_bits(cw_words64, self.n))
 
+    def set_option(self, key: str, value: int):
+        """mpw_set_option (include/mpwsd.h): stage-1 kernel choice, timing, and
+        the tensor hop's A/B launch variants and test hooks."""
+        _native.value_error_check(_native.lib().mpw_set_option(self._h, key.encode(), int(value)),
+                                  "mpw_set_option")
+
+    @property
+    def launch_count(self) -> int:
+        """Kernels launched through this handle so far (mpw_launch_count)."""
+        return int(_native.lib().mpw_launch_count(self._h))
+
     # -- timing -------------------------------------------------------------
     def set_timing(self, enable: bool):
         _native.check(_native.lib().mpw_set_timing(self._h, int(bool(enable))))
@@ -439,24 +475,33 @@ class DeviceDecoder:
 # ---------------------------------------------------------------------------
 # Per-frame drop-in API
 
-_cache: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
-_code_only: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+class _ThreadCaches(threading.local):
+    """Decoders of one host thread: a handle is never shared between threads
+    (its scratch and launch order are per handle), keyed weakly on the
+    caller's code and sphere objects as the reference keys its caches
+    (decoders.py:124, 339-350)."""
+
+    def __init__(self):
+        self.by_sphere = weakref.WeakKeyDictionary()    # sphere -> {code -> DeviceDecoder}
+        self.code_only = weakref.WeakKeyDictionary()    # code -> DeviceDecoder (stage 1 / OSD lists)
+        self.ml_spheres = weakref.WeakKeyDictionary()   # code -> full-codebook sphere (ml_decode)
 
 
-_code_only = weakref.WeakKeyDictionary()
+_tls = _ThreadCaches()
 
 
 def get_decoder(code, sphere) -> DeviceDecoder:
-    if sphere is None:                  # stage-1 only (OSD lists, ML)
-        dec = _code_only.get(code)
+    """This thread's DeviceDecoder for (code, sphere); sphere None = stage 1 only."""
+    if sphere is None:
+        dec = _tls.code_only.get(code)
         if dec is None:
             dec = DeviceDecoder(code, None)
-            _code_only[code] = dec
+            _tls.code_only[code] = dec
         return dec
-    per = _cache.get(sphere)
+    per = _tls.by_sphere.get(sphere)
     if per is None:
         per = weakref.WeakKeyDictionary()
-        _cache[sphere] = per
+        _tls.by_sphere[sphere] = per
     dec = per.get(code)
     if dec is None:
         dec = DeviceDecoder(code, sphere)
@@ -513,11 +558,11 @@ def _step_counters(counters, sphere, m, n):
 
 
 def _run_hops(dec, y, anchors64, T):
-    """Device mp_wsd over one frame's anchors; returns host arrays."""
+    """Device mp_wsd over one frame's anchors (float64 y); returns host arrays."""
     n = dec.n
-    y32 = np.asarray(y, dtype=np.float64).astype(np.float32)[None, :]
+    y64 = np.ascontiguousarray(y, dtype=np.float64)[None, :]
     a32 = words64_to_32(np.asarray(anchors64, dtype=np.uint64), n)[None, :, :]
-    o = dec.mp_wsd_batch(y32, a32, T)
+    o = dec.mp_wsd_batch(y64, a32, T)
     return {k: v.cpu().numpy() for k, v in o.items()}
 
 
@@ -603,17 +648,26 @@ def wsd_trajectory(y, c0, sphere, params, counters=None, force_full_iterations=F
 
 
 def wsd_step(y, center, x_center, sphere, m, counters=None):
-    """decoders.py:401-417.  The hop is taken from the modulated `center`."""
+    """decoders.py:401-417.  The step is scored on t = y * x_center
+    (decoders.py:374): every decision of `_wsd_step_core` -- the argmin of the
+    survivor EDs and the strict accept test best_ed < ed_center -- depends on
+    t alone (ED(x_center * s_p) - ED(x_center) = 4 sum_{supp p} t_i), so the
+    device hop runs from the sign pattern of x_center on the magnitudes
+    |y * x_center|, and the returned words are center ^ member as in the
+    reference (decoders.py:396-397)."""
     if m < 1:
         raise ValueError("m must be >= 1")
     if counters is None:
         counters = OpCounter()
     y = np.asarray(y, dtype=np.float64)
+    xc = np.asarray(x_center, dtype=np.float64)
     n = int(sphere.n)
+    if xc.shape != (n,) or y.shape != (n,):
+        raise ValueError(f"expected {n} channel values")
     counters.ed_evaluations += 1
     dec = _hop_decoder(sphere)
-    anc = np.asarray(center.words, dtype=np.uint64)[None, :]
-    r = _run_hops(dec, y, anc, 1)
+    anc = pack_bits((xc < 0).astype(np.uint8)[None, :])
+    r = _run_hops(dec, np.abs(y * xc), anc, 1)
     _step_counters(counters, sphere, m, n)
     mem = int(r["hops"][0, 0, 0])
     if mem > 0:
@@ -633,10 +687,7 @@ def scl_decode(llrs, code, list_size, counters=None) -> CandidateList:
         raise ValueError("LLR length mismatch")
     if counters is None:
         counters = OpCounter()
-    dec = _code_only.get(code)
-    if dec is None:
-        dec = DeviceDecoder(code, None)
-        _code_only[code] = dec
+    dec = get_decoder(code, None)
     o = dec.scl_batch(llrs=llrs[None, :], list_size=list_size)
     cnt = int(o["list_n"][0].item())
     cw = words32_to_64(o["list_cw"][0, :cnt].cpu().numpy().view(np.uint32), n)
@@ -646,7 +697,6 @@ def scl_decode(llrs, code, list_size, counters=None) -> CandidateList:
 
 
 ML_DIM_LIMIT = 26
-_ml_spheres = weakref.WeakKeyDictionary()
 
 
 def ml_decode(y, code, counters=None):
@@ -661,14 +711,14 @@ def ml_decode(y, code, counters=None):
     n = int(code.n)
     if y.shape != (n,):
         raise ValueError(f"expected {n} channel values, got {y.shape}")
-    sph = _ml_spheres.get(code)
+    sph = _tls.ml_spheres.get(code)
     if sph is None:
         from .patterns import enumerate_sphere_gpu, weight_spectrum_gpu
         spec = weight_spectrum_gpu(code)
         sph = enumerate_sphere_gpu(code, int((spec[1:] > 0).sum()))
-        _ml_spheres[code] = sph
+        _tls.ml_spheres[code] = sph
     dec = get_decoder(code, sph)
-    o = dec.mp_wsd_batch(y.astype(np.float32)[None, :], np.zeros((1, 1, dec.nw), np.uint32), 1)
+    o = dec.mp_wsd_batch(y[None, :], np.zeros((1, 1, dec.nw), np.uint32), 1)
     best64 = words32_to_64(o["best"].cpu().numpy().view(np.uint32), n)[0]
     if counters is not None:
         counters.ed_evaluations += 1 << int(code.k)
@@ -752,7 +802,7 @@ def two_stage_decode(y, code, stage1, params, sphere, sigma=1.0, counters=None) 
     n = int(code.n)
     dec = get_decoder(code, sphere)
     A, T = params.num_paths, params.max_iterations
-    o = dec.two_stage_batch(y.astype(np.float32)[None, :], sigma, stage1.list_size, A, T,
+    o = dec.two_stage_batch(y[None, :], sigma, stage1.list_size, A, T,
                             params.activation_mode, want_hops=True, want_anchors=True)
     h = {k: v.cpu().numpy() for k, v in o.items()}
     counters.scl_node_ops += int(stage1.list_size) * n * (n.bit_length() - 1)

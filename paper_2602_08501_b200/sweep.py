@@ -16,7 +16,13 @@ reference's own rules, so the CSV is the reference's byte for byte:
   :478), mean iterations per path, fixed CSV schema (:32-33, 365-376).
 
 Both stage-1 kinds run on the device: CA-SCL and order-k OSD (csrc/osd.cuh).
-Inputs are rounded to float32 (the path's dtype) before decoding.
+Trial-stream inputs are decoded as the reference's float64 values (the
+*_f64 entry points); device-stream inputs are float32.  Under torchrun the
+trials shard by range over the ranks (_Ranks) with one all-reduce of the
+per-block statistics per round:
+
+    python -m torch.distributed.run --nproc-per-node 8 -m paper_2602_08501_b200.sweep \
+        --config X.cfg --out X.csv
 """
 
 from __future__ import annotations
@@ -243,46 +249,116 @@ def _scan_cost(n, sphere_size, support_total, m):
     return (m_eff, gain, sort, n + m_eff)
 
 
+class _Ranks:
+    """Frame-range sharding of a sweep over the ranks of torch.distributed
+    (one process per GPU).  Every round of world x batch trials, rank r
+    decodes trials [t0 + r batch, t0 + (r+1) batch); the per-64-trial block
+    statistics of the round are summed over ranks (one all-reduce), so every
+    rank folds the identical sequence and takes the identical stopping
+    decision -- the CSV equals a single process's byte for byte."""
+
+    def __init__(self):
+        self.world, self.rank, self.backend = 1, 0, None
+        try:
+            import torch.distributed as dist
+        except ImportError:     # pragma: no cover
+            return
+        if dist.is_available() and dist.is_initialized():
+            self.dist = dist
+            self.world, self.rank = dist.get_world_size(), dist.get_rank()
+            self.backend = dist.get_backend()
+
+    def sum(self, arr: np.ndarray) -> np.ndarray:
+        if self.world == 1:
+            return arr
+        import torch
+        t = torch.from_numpy(np.ascontiguousarray(arr))
+        if self.backend == "nccl":
+            t = t.cuda()
+        self.dist.all_reduce(t)
+        return t.cpu().numpy()
+
+
+def _check_batch(batch: int):
+    # the fold consumes whole 64-trial blocks at absolute trial positions
+    if batch < BATCH or batch % BATCH:
+        raise ConfigError(f"batch must be a positive multiple of {BATCH} (got {batch})")
+
+
+def _block_sums(per_trial: np.ndarray) -> np.ndarray:
+    """[cnt, C] per-trial statistics -> [ceil(cnt/64), C] sums per 64-trial block."""
+    cnt, c = per_trial.shape
+    nb = (cnt + BATCH - 1) // BATCH
+    pad = np.zeros((nb * BATCH, c), np.int64)
+    pad[:cnt] = per_trial
+    return pad.reshape(nb, BATCH, c).sum(axis=1)
+
+
+def _fold(blocks: np.ndarray, state: list, cfg) -> bool:
+    """Fold 64-trial blocks in trial order with the reference's stopping rule
+    (the error target is checked before every block, simharness.py:318-330).
+    state[0] = trials, state[1] = errors, state[2:] = the other columns.
+    Returns True when the point is finished."""
+    for blk in blocks:
+        if blk[0] == 0:                 # past max_trials
+            return True
+        if not (state[0] < cfg.max_trials and state[1] < cfg.min_block_errors):
+            return True
+        for c in range(len(state)):
+            state[c] += int(blk[c])
+    return False
+
+
+def _sweep_rounds(cfg, batch, ranks, decode_range, ncols, on_point_start=None):
+    """Rounds of world x batch trials for one SNR point: decode_range(first,
+    count) returns this rank's [count, ncols] per-trial statistics."""
+    state = [0] * ncols
+    t0 = 0
+    per_round = ranks.world * batch
+    while True:
+        first = t0 + ranks.rank * batch
+        cnt = max(0, min(batch, cfg.max_trials - first))
+        blocks = np.zeros((per_round // BATCH, ncols), np.int64)
+        if cnt:
+            b = _block_sums(decode_range(first, cnt))
+            off = ranks.rank * batch // BATCH
+            blocks[off:off + len(b)] = b
+        blocks = ranks.sum(blocks)
+        done = _fold(blocks, state, cfg)
+        t0 += per_round
+        if done or t0 >= cfg.max_trials or not (state[0] < cfg.max_trials and state[1] < cfg.min_block_errors):
+            return state
+
+
 def run_sweep_ml(cfg: ExperimentConfig, batch: int = 8192, device=None, variant="auto"):
     """simharness.run_sweep(decoder_kind='ml'): exact ML on the same trial
     streams (decoders.py:140-167).  ML = one hop from the zero codeword over
     P = every nonzero codeword (the reference's criterion 3 identity), so it
     runs on the same tensor-core scan; ties (measure zero) go to the lowest
-    member index instead of the lowest message index."""
+    member index instead of the lowest message index.  Shards across the
+    ranks of torch.distributed when initialised (_Ranks)."""
     from .decoders import DeviceDecoder, words32_to_64
     from .patterns import enumerate_sphere, weight_spectrum
+    _check_batch(batch)
     code = build_code(cfg)
     if code.k > 26:
         raise ConfigError(f"K = {code.k} exceeds the ML enumeration budget of 26")
     spec = weight_spectrum(code)
     sphere = enumerate_sphere(code, int((spec[1:] > 0).sum()))
     dec = DeviceDecoder(code, sphere, device=device)
+    ranks = _Ranks()
     n, nw = code.n, (code.n + 31) // 32
     records = []
     for snr_idx, snr_db in enumerate(cfg.snr_db_grid):
         sigma = _sigma(cfg, snr_db)
-        trials = errors = 0
-        t0 = 0
-        done = False
-        while not done:
-            cnt = min(batch, cfg.max_trials - t0)
-            _, tx, y = trial_inputs(code, cfg.seed, snr_idx, range(t0, t0 + cnt), sigma)
-            anchors = np.zeros((cnt, 1, nw), np.uint32)
-            o = dec.mp_wsd_batch(y.astype(np.float32), anchors, 1, variant=variant)
+
+        def decode_range(first, cnt):
+            _, tx, y = trial_inputs(code, cfg.seed, snr_idx, range(first, first + cnt), sigma)
+            o = dec.mp_wsd_batch(y, np.zeros((cnt, 1, nw), np.uint32), 1, variant=variant)
             best = words32_to_64(o["best"].cpu().numpy().view(np.uint32), n)
-            err = (best != tx).any(axis=1)
-            i = 0
-            while i < cnt:
-                if not (trials < cfg.max_trials and errors < cfg.min_block_errors):
-                    done = True
-                    break
-                j = min(i + BATCH, cnt, cfg.max_trials - t0)
-                trials += j - i
-                errors += int(err[i:j].sum())
-                i = j
-            t0 += cnt
-            if t0 >= cfg.max_trials or not (trials < cfg.max_trials and errors < cfg.min_block_errors):
-                done = True
+            return np.stack([np.ones(cnt, np.int64), (best != tx).any(axis=1)], axis=1)
+
+        trials, errors = _sweep_rounds(cfg, batch, ranks, decode_range, 2)
         lo, hi = wilson_interval(errors, trials)
         records.append(SweepRecord(
             code_label=code.label(), stage1_label="ml", wsd_r=0, wsd_m=0, wsd_j=0, num_paths=0,
@@ -297,12 +373,16 @@ def run_sweep(cfg: ExperimentConfig, sphere=None, batch: int = 8192, device=None
     """simharness.run_sweep (decoder_kind='two_stage') over the GPU path.
 
     input_mode 'trial' reproduces the reference's per-trial streams (host
-    numpy, byte-identical CSVs); 'device' draws the counter-based stream on
-    the GPU (mpw_channel_batch) for 10^6-10^7-trial points; `on_batch(snr_idx,
-    first_trial, y, tx, outputs)` sees every device batch (oracle subsamples)."""
+    numpy, float64 received words decoded through the *_f64 path, CSVs byte
+    for byte); 'device' draws the counter-based float32 stream on the GPU
+    (mpw_channel_batch) for 10^6-10^7-trial points; `on_batch(snr_idx,
+    first_trial, y, tx, outputs)` sees every device batch of this rank
+    (oracle subsamples).  When torch.distributed is initialised the trials
+    are sharded over its ranks (_Ranks); every rank returns the same records."""
     from .decoders import DeviceDecoder, default_filter_size, device_channel, words32_to_64
     if input_mode not in ("trial", "device"):
         raise ConfigError(f"unknown input mode {input_mode!r}")
+    _check_batch(batch)
     from .patterns import enumerate_sphere
     from .sphere import load_sphere
 
@@ -322,65 +402,43 @@ def run_sweep(cfg: ExperimentConfig, sphere=None, batch: int = 8192, device=None
         stage1_flops = 4 * L * n * (n.bit_length() - 1)
         label = f"scl{L}"
     dec = DeviceDecoder(code, sphere, device=device)
-
-    def decode(y):
-        if osd:
-            return dec.two_stage_osd_batch(y, cfg.osd_order, cfg.stage1_list_cap, A, T,
-                                           cfg.activation_mode, variant=variant)
-        return dec.two_stage_batch(y, sigma, L, A, T, cfg.activation_mode, variant=variant)
+    ranks = _Ranks()
 
     records = []
     for snr_idx, snr_db in enumerate(cfg.snr_db_grid):
         sigma = _sigma(cfg, snr_db)
-        trials = errors = activated = 0
-        path_iters = paths = 0
-        ed_ev = gain = sort = misc = 0
-        ties = unres = 0
-        done = False
-        t0 = 0
-        while not done:
-            cnt = min(batch, cfg.max_trials - t0)
+
+        def decode(y):
+            if osd:
+                return dec.two_stage_osd_batch(y, cfg.osd_order, cfg.stage1_list_cap, A, T,
+                                               cfg.activation_mode, variant=variant)
+            return dec.two_stage_batch(y, sigma, L, A, T, cfg.activation_mode, variant=variant)
+
+        def decode_range(first, cnt):
             if input_mode == "trial":
-                _, tx, y = trial_inputs(code, cfg.seed, snr_idx, range(t0, t0 + cnt), sigma)
-                o = decode(y.astype(np.float32))
+                _, tx, y = trial_inputs(code, cfg.seed, snr_idx, range(first, first + cnt), sigma)
+                o = decode(y)
                 best = words32_to_64(o["best"].cpu().numpy().view(np.uint32), n)
                 err = (best != tx).any(axis=1)
             else:   # device-resident counter-based inputs (mpw_channel_batch)
-                yd, txd, _ = device_channel(dec, cfg.seed, snr_idx, t0, cnt, sigma)
+                yd, txd, _ = device_channel(dec, cfg.seed, snr_idx, first, cnt, sigma)
                 o = decode(yd)
                 err = (o["best"] != txd).any(dim=1).cpu().numpy()
                 if on_batch is not None:
-                    on_batch(snr_idx, t0, yd, txd, o)
-            stage = o["stage"].cpu().numpy()
+                    on_batch(snr_idx, first, yd, txd, o)
+            act = o["stage"].cpu().numpy() == 1
             iters = o["iters"].cpu().numpy()
             flags = o["flags"].cpu().numpy()
-            nanch = (iters > 0).sum(axis=1)
-            sit = iters.sum(axis=1)
-            # fold in trial order with the reference's 64-trial batches
-            i = 0
-            while i < cnt:
-                if not (trials < cfg.max_trials and errors < cfg.min_block_errors):
-                    done = True
-                    break
-                j = min(i + BATCH, cnt, cfg.max_trials - t0)
-                sl = slice(i, j)
-                act = stage[sl] == 1
-                trials += j - i
-                errors += int(err[sl].sum())
-                activated += int(act.sum())
-                path_iters += int(sit[sl][act].sum())
-                paths += int(nanch[sl][act].sum())
-                ns = int(sit[sl][act].sum())
-                ed_ev += int(nanch[sl][act].sum()) + ns * scan[0]
-                gain += ns * scan[1]
-                sort += ns * scan[2]
-                misc += ns * scan[3]
-                ties += int(((flags[sl] & 23) != 0).sum())
-                unres += int(((flags[sl] & 8) != 0).sum())
-                i = j
-            t0 += cnt
-            if t0 >= cfg.max_trials or not (trials < cfg.max_trials and errors < cfg.min_block_errors):
-                done = True
+            # per trial: trials, errors, activated, path iterations, paths, near-ties, unresolved
+            return np.stack([np.ones(cnt, np.int64), err, act, iters.sum(axis=1) * act,
+                             (iters > 0).sum(axis=1) * act, (flags & 23) != 0, (flags & 8) != 0],
+                            axis=1).astype(np.int64)
+
+        trials, errors, activated, path_iters, paths, ties, unres = _sweep_rounds(
+            cfg, batch, ranks, decode_range, 7)
+        # operation counts (decoders.py:375-389, :478): path_iters executed scans
+        ed_ev = paths + path_iters * scan[0]
+        gain, sort, misc = path_iters * scan[1], path_iters * scan[2], path_iters * scan[3]
         flops = 3 * n * ed_ev + gain + sort + stage1_flops * trials + misc   # complexity.py:47-57
         lo, hi = wilson_interval(errors, trials)
         records.append(SweepRecord(
@@ -393,6 +451,19 @@ def run_sweep(cfg: ExperimentConfig, sphere=None, batch: int = 8192, device=None
     return records
 
 
+def _init_ranks():
+    """torchrun launch (WORLD_SIZE > 1): one rank per GPU over NCCL."""
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws <= 1:
+        return None, 0
+    import torch
+    import torch.distributed as dist
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return dist, dist.get_rank()
+
+
 def main(argv=None):
     import argparse
     ap = argparse.ArgumentParser(description="GPU sweep with the reference's config/CSV formats")
@@ -400,12 +471,18 @@ def main(argv=None):
     ap.add_argument("--out", required=True)
     ap.add_argument("--batch", type=int, default=8192)
     args = ap.parse_args(argv)
+    dist, rank = _init_ranks()
     try:
         cfg = load_config(args.config)
         recs = run_sweep(cfg, batch=args.batch)
     except (ConfigError, ValueError, OSError) as e:
         print(f"error: {e}", file=sys.stderr)
         return 2
+    finally:
+        if dist is not None:
+            dist.destroy_process_group()
+    if rank:
+        return 0
     write_csv(recs, args.out)
     for r in recs:
         print(f"snr {r.snr_db:5.2f} dB  bler {r.bler:.4g} [{r.bler_lo:.4g}, {r.bler_hi:.4g}]  "

@@ -162,7 +162,7 @@ def test_scl_kernels_agree_bit_exact(name, generic):
 
 
 @pytest.mark.parametrize("name", ["cfg4", "cfg2"])
-def test_int8_window_overflow_continuation(name, monkeypatch):
+def test_int8_window_overflow_continuation(name):
     """int8 screen: with the overflow threshold forced down to 4 keys (profiling
     knob 2048), most scans take continuation passes; decisions must still equal
     the oracle's, with no frame left unresolved."""
@@ -172,8 +172,9 @@ def test_int8_window_overflow_continuation(name, monkeypatch):
     sigma = cfg.sigma(code=code)
     F = 128 if name == "cfg4" else 256
     _, cw, y = channel.bulk_inputs(code, 12, 0, 0, F, sigma)
-    monkeypatch.setenv("MPW_TC_EXPERIMENT", "2048")
-    o = decoder(cfg).two_stage_batch(y, sigma, cfg.list_size, cfg.num_paths, cfg.max_iterations,
+    dec = DeviceDecoder(code, sph)
+    dec.set_option("hop_experiment", 2048)      # window overflow at 4 keys
+    o = dec.two_stage_batch(y, sigma, cfg.list_size, cfg.num_paths, cfg.max_iterations,
                                      cfg.activation_mode, variant="tensor_i8")
     r = orc.two_stage_batch(y, code, sph, cfg.list_size, cfg.num_paths, cfg.max_iterations,
                             cfg.activation_mode == "crc_gated", sigma, nthreads=8)
@@ -187,8 +188,8 @@ def test_int8_window_overflow_continuation(name, monkeypatch):
     np.testing.assert_array_equal(_np(o["iters"])[ok], r["iters"][ok])
 
 
-def test_int8_pair_kernel_vs_oracle(monkeypatch):
-    """The cta_group::2 variant of the int8 screen (MPW_TC_PAIR=1: one M = 256 MMA
+def test_int8_pair_kernel_vs_oracle():
+    """The cta_group::2 variant of the int8 screen (option i8_pair: one M = 256 MMA
     per K step for a CTA pair, each CTA holding half of every P stage) decodes
     like the oracle."""
     cfg = configs.CONFIGS["cfg4"]
@@ -197,8 +198,9 @@ def test_int8_pair_kernel_vs_oracle(monkeypatch):
     sigma = cfg.sigma(code=code)
     F = 192
     _, cw, y = channel.bulk_inputs(code, 13, 0, 0, F, sigma)
-    monkeypatch.setenv("MPW_TC_PAIR", "1")
-    o = decoder(cfg).two_stage_batch(y, sigma, cfg.list_size, cfg.num_paths, cfg.max_iterations,
+    dec = DeviceDecoder(code, sph)
+    dec.set_option("i8_pair", 1)
+    o = dec.two_stage_batch(y, sigma, cfg.list_size, cfg.num_paths, cfg.max_iterations,
                                      cfg.activation_mode, variant="tensor_i8")
     r = orc.two_stage_batch(y, code, sph, cfg.list_size, cfg.num_paths, cfg.max_iterations,
                             cfg.activation_mode == "crc_gated", sigma, nthreads=8)

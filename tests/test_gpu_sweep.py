@@ -47,3 +47,42 @@ def test_gpu_rm_osd_sweep_csv_matches_reference_bytes(tmp_path):
     sweep.write_csv(recs, out)
     with open(os.path.join(GOLDEN, "sweep_rm_osd.csv"), "rb") as fh:
         assert out.read_bytes() == fh.read()
+
+
+def _sweep_rank(rank, world, port, name, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = sweep.load_config(os.path.join(GOLDEN, name + ".cfg"))
+    recs = sweep.run_sweep(cfg, batch=1024)
+    q.put((rank, [(r.trials, r.block_errors, r.activation_rate, r.ed_units_mean, r.avg_iterations)
+                  for r in recs], recs if rank == 0 else None))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name", ["sweep_two_stage", "sweep_stage1"])
+def test_gpu_sweep_two_ranks_csv_matches_reference_bytes(name, tmp_path):
+    """The trial range sharded over two ranks (block-aligned, one all-reduce
+    of the block statistics per round): both ranks fold identical records and
+    the CSV equals the reference's byte for byte.  The ranks share the one
+    visible GPU (independent decodes) and reduce over gloo."""
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_sweep_rank, args=(r, 2, port, name, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict((r, (summ, recs)) for r, summ, recs in (q.get(timeout=600) for _ in range(2)))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert got[0][0] == got[1][0]
+    out = tmp_path / (name + ".csv")
+    sweep.write_csv(got[0][1], out)
+    with open(os.path.join(GOLDEN, name + ".csv"), "rb") as fh:
+        assert out.read_bytes() == fh.read()

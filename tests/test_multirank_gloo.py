@@ -1,7 +1,8 @@
-"""World-size-2 gloo test of the N>1 path's host logic: block-aligned frame
-shards, per-rank decoding, and the single counter all-reduce give the same
-totals as one process decoding the union (the CPU oracle stands in for the
-per-GPU decoder here)."""
+"""World-size-2 gloo test of the N>1 path's host logic on CPU: block-aligned
+frame shards of the block-keyed input stream, per-rank decoding and the single
+counter all-reduce give the same totals as ONE decode of the whole contiguous
+range in one call (the CPU oracle stands in for the per-GPU decoder here; the
+GPU version, tests/test_gpu_multirank.py, runs bench.py's own rank code)."""
 import os
 import socket
 
@@ -13,7 +14,7 @@ import torch.multiprocessing as mp
 
 from paper_2602_08501_b200 import channel, configs, shard
 
-FRAMES_PER_RANK = 2 * channel.BLOCK + 512   # ragged last block
+TOTAL = 3 * channel.BLOCK + 512   # ragged last block
 
 
 def _free_port():
@@ -42,7 +43,7 @@ def _worker(rank, world, port, q):
     code = cfg.code()
     sph = configs.build_sphere_for(cfg, code)
     sigma = cfg.sigma(code=code)
-    sh = shard.shard_for(rank, world, FRAMES_PER_RANK)
+    sh = shard.split_range(TOTAL, rank, world)
     c = torch.from_numpy(_decode_counts(cfg, code, sph, sigma, sh.first, sh.count))
     shard.reduce_counters(c, dist)
     t = torch.tensor([float(rank + 1)], dtype=torch.float64)
@@ -69,10 +70,7 @@ def test_two_rank_shards_and_reduction_match_single_process():
     code = cfg.code()
     sph = configs.build_sphere_for(cfg, code)
     sigma = cfg.sigma(code=code)
-    ref = np.zeros(8, np.int64)
-    for r in range(world):
-        sh = shard.shard_for(r, world, FRAMES_PER_RANK)
-        ref += _decode_counts(cfg, code, sph, sigma, sh.first, sh.count)
+    ref = _decode_counts(cfg, code, sph, sigma, 0, TOTAL)
     assert got == ref.tolist()
     assert tmax == 2.0
 

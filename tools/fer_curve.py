@@ -9,6 +9,11 @@ per-point subsample of the very same received words:
     interval from the subsample (simharness.py:208-217).
 
     python tools/fer_curve.py [--frames 1000000] [--oracle-frames 4000] [--out profiles/...]
+    python -m torch.distributed.run --nproc-per-node 8 tools/fer_curve.py --frames 10000000
+
+Under torchrun the trials of every point shard by range over the ranks
+(sweep._Ranks: one all-reduce of the per-block statistics per round); rank 0
+holds the first batch, runs the oracle subsample and writes the outputs.
 """
 
 from __future__ import annotations
@@ -74,6 +79,7 @@ def main():
     ap.add_argument("--batch", type=int, default=1 << 18)
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "fer_curve"))
     args = ap.parse_args()
+    dist, rank = sweep._init_ranks()
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     idx = np.arange(128)
     ranking = idx[np.lexsort((idx, np.array([bin(i).count("1") for i in idx])))]
@@ -84,7 +90,8 @@ def main():
                        "one miss is expected by chance; the decoders themselves are compared exactly on "
                        "the subsample (gpu_errors_on_subsample == oracle_errors, codeword mismatches).",
                "frames_per_point": args.frames, "oracle_frames_per_point": args.oracle_frames,
-               "input": "device counter-based Philox4x32-10 stream (mpw_channel_batch)", "runs": {}}
+               "input": "device counter-based Philox4x32-10 stream (mpw_channel_batch)",
+               "ranks": 1 if dist is None else dist.get_world_size(), "runs": {}}
     for name, (text, cfgname) in setups(args.frames, rank_path).items():
         cfg = sweep.parse_config(text)
         code = sweep.build_code(cfg)
@@ -101,6 +108,8 @@ def main():
         t0 = time.time()
         recs = sweep.run_sweep(cfg, sphere=sph, batch=args.batch, input_mode="device", on_batch=on_batch)
         gpu_s = time.time() - t0
+        if rank:
+            continue
         sweep.write_csv(recs, f"{args.out}_{name}.csv")
         points = []
         for i, r in enumerate(recs):
@@ -124,6 +133,10 @@ def main():
         summary["runs"][name] = dict(gpu_seconds=gpu_s, frames_per_second=len(recs) * args.frames / gpu_s,
                                      points=points)
         print(json.dumps({name: summary["runs"][name]}, indent=1), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    if rank:
+        return
     with open(args.out + ".json", "w") as fh:
         json.dump(summary, fh, indent=1)
 

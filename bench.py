@@ -47,6 +47,21 @@ def _peaks():
             "sm_max_mhz": 1965.0}, "fallback"
 
 
+def _micro_peaks():
+    """Per-SM rates measured by tools/micro/peaks.cu on this pool's B200s
+    (profiles/r02_micro_peaks.json): tcgen05 kind::i8 / kind::f16 ops per
+    clock per SM, LDS bytes per clock per SM."""
+    p = os.path.join(ROOT, "profiles", "r02_micro_peaks.json")
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        return {"i8": float(d["tc_i8"]["ops_per_clk_per_sm"]), "f16": float(d["tc_f16"]["flop_per_clk_per_sm"]),
+                "smem": float(d["smem_lds128"]["bytes_per_clk_per_sm"]), "sms": int(d["sms"]),
+                "source": "profiles/r02_micro_peaks.json (tools/micro/peaks.cu)"}
+    except (OSError, ValueError, KeyError):
+        return {"i8": 16384.0, "f16": 8192.0, "smem": 128.0, "sms": 148, "source": "nominal per-clock rates"}
+
+
 def _ncu_traffic(key):
     """DRAM bytes (read + write) per launch of the dominant kernel from one
     committed `ncu --set full` capture of the same command
@@ -386,6 +401,11 @@ def run_ours(args, cfg, code, sph, sigma, backend: str = "nccl", device_index=No
 
     if rank == 0:
         peaks, peak_kind = _peaks()
+        micro = _micro_peaks()
+        clk = clocks.summary()
+        mhz = clk["sm_mhz"] or peaks.get("sm_max_mhz", 1965.0)
+        # peak of the dominant kernel's pipe at the SM clock observed in the timed region
+        per_sm_clk = lambda rate: rate * micro["sms"] * mhz * 1e6
         evals = int(ctr[4])
         hop_ms = float(kms[1])
         variant_used = args.variant
@@ -394,36 +414,36 @@ def run_ours(args, cfg, code, sph, sigma, backend: str = "nccl", device_index=No
         if variant_used == "tensor_i8":
             ops = evals / ws * 2.0 * code.n                # 2N int8 tensor ops per evaluation
             ach = ops / (hop_ms / 1000.0) / 1e12
-            peak = 2.0 * peaks["bf16_tflops"]              # the i8 MMA rate is twice the f16 rate per SM
+            peak = per_sm_clk(micro["i8"]) / 1e12
             traffic, tsrc = _ncu_traffic(f"hop_tc_i8_{args.frames}")
             roof = {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TOP/s",
                     "frac": ach / peak, "traffic": traffic, "traffic_source": tsrc,
                     "kernel": "hop_tc_kernel<LIMBS=0> (kind::i8)", "op_per_eval": 2 * code.n,
-                    "peak_source": f"2 x {peak_kind} bf16_tflops (no measured int8 peak; kind::i8 issues at twice "
-                                   "the kind::f16 rate)",
-                    "nominal_peak": 4500.0, "frac_of_nominal": ach / 4500.0}
+                    "peak_source": f"measured kind::i8 rate {micro['i8']:.0f} ops/clk/SM ({micro['source']}) x "
+                                   f"{micro['sms']} SMs x {mhz:.0f} MHz (median SM clock of the timed region)",
+                    "frac_of_2x_bf16_burst": ach / (2.0 * peaks["bf16_tflops"])}
         elif variant_used in ("tensor", "tensor2"):
             limbs = 1 if variant_used == "tensor" else 2
             flop = evals / ws * 2.0 * limbs * code.n  # limbs x 2N FLOP per evaluation
             ach = flop / (hop_ms / 1000.0) / 1e12
-            peak = peaks["bf16_tflops"]
+            peak = per_sm_clk(micro["f16"]) / 1e12
             traffic, tsrc = _ncu_traffic(f"hop_tc_{limbs}limb_{args.frames}")
             roof = {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
                     "frac": ach / peak, "traffic": traffic, "traffic_source": tsrc,
                     "kernel": f"hop_tc_kernel<LIMBS={limbs}>",
                     "flop_per_eval": 2 * limbs * code.n,
-                    "peak_source": f"{peak_kind} bf16_tflops (burst cuBLAS 8192^3)",
-                    # the measured cuBLAS burst is below the dense f16 tensor-core
-                    # rate; the fraction of the nominal 2250 TF/s is given beside it
-                    "nominal_peak": 2250.0, "frac_of_nominal": ach / 2250.0}
+                    "peak_source": f"measured kind::f16 rate {micro['f16']:.0f} flop/clk/SM ({micro['source']}) x "
+                                   f"{micro['sms']} SMs x {mhz:.0f} MHz (median SM clock of the timed region)",
+                    "frac_of_bf16_burst": ach / peaks["bf16_tflops"]}
         else:
             wbar = float(sph.mean_nonzero_weight)
             byt = evals / ws * 4.0 * wbar                # smem bytes of the gather per evaluation
             ach = byt / (hop_ms / 1000.0) / 1e9
-            peak = 128.0 * 148 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e9
+            peak = per_sm_clk(micro["smem"]) / 1e9
             roof = {"bound": "smem", "achieved": ach, "peak": peak, "unit": "GB/s",
                     "frac": ach / peak, "traffic": None, "kernel": "hop_gather_kernel",
-                    "peak_source": "theoretical shared-memory bandwidth 128 B/clk/SM x 148 SMs x max SM clock"}
+                    "peak_source": f"measured LDS.128 bandwidth {micro['smem']:.1f} B/clk/SM ({micro['source']}) x "
+                                   f"{micro['sms']} SMs x {mhz:.0f} MHz"}
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None,
@@ -441,7 +461,7 @@ def run_ours(args, cfg, code, sph, sigma, backend: str = "nccl", device_index=No
                 "avg_iters": float(ctr[3]) / max(1, int(ctr[2]) * A),
                 "near_tie_frames": int(ctr[5]),
                 "uncertified_frames": int(ctr[6]),
-                "clocks": clocks.summary(),
+                "clocks": clk,
                 # this library's kernels launched in the timed region, all ranks
                 # (mpw_launch_count: scl, ebound, hop, finalize, frame per step)
                 "gpu_launches": int(nl.item()),

@@ -14,6 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(CSRC, "build")
 LIB = os.path.join(HERE, "libmpwsd.so")
+PROF_LIB = os.path.join(HERE, "libmpwsd_prof.so")
 SOURCES = ["mpwsd.cu", "hop_tc.cu", "scl_lane.cu", "sphere_tools.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -34,14 +35,14 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in _deps() if os.path.exists(d))
 
 
-def _obj(src: str) -> str:
-    return os.path.join(OBJ, os.path.splitext(src)[0] + ".o")
+def _obj(src: str, obj_dir: str = OBJ) -> str:
+    return os.path.join(obj_dir, os.path.splitext(src)[0] + ".o")
 
 
-def _obj_stale(src: str) -> bool:
+def _obj_stale(src: str, obj_dir: str = OBJ) -> bool:
     """An object is stale when it or its dependency file is missing, or any
     file the dependency file lists (nvcc -MD) is newer."""
-    o, d = _obj(src), _obj(src)[:-2] + ".d"
+    o, d = _obj(src, obj_dir), _obj(src, obj_dir)[:-2] + ".d"
     if not (os.path.exists(o) and os.path.exists(d)):
         return True
     t = os.path.getmtime(o)
@@ -50,16 +51,21 @@ def _obj_stale(src: str) -> bool:
     return any(not os.path.exists(f) or os.path.getmtime(f) > t for f in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, profile: bool = False) -> str:
+    """profile=True: the profiling library (-DMPW_PROFILE: per-tile clock
+    trace of the hop kernel) as libmpwsd_prof.so, selected with MPW_LIB."""
+    lib, obj_dir = (PROF_LIB, OBJ + "_prof") if profile else (LIB, OBJ)
+    if not force and not profile and not _stale():
         return LIB
-    os.makedirs(OBJ, exist_ok=True)
+    os.makedirs(obj_dir, exist_ok=True)
     extra = ["-Xptxas=-v"] if verbose else []
-    todo = [s for s in SOURCES if force or _obj_stale(s)]
+    if profile:
+        extra.append("-DMPW_PROFILE")
+    todo = [s for s in SOURCES if force or _obj_stale(s, obj_dir)]
 
     def compile_one(src):
-        cmd = [NVCC, *CFLAGS, *extra, "-MD", "-MF", _obj(src)[:-2] + ".d", "-c", os.path.join(CSRC, src),
-               "-o", _obj(src)]
+        cmd = [NVCC, *CFLAGS, *extra, "-MD", "-MF", _obj(src, obj_dir)[:-2] + ".d", "-c", os.path.join(CSRC, src),
+               "-o", _obj(src, obj_dir)]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         r = subprocess.run(cmd, cwd=HERE, capture_output=True, text=True)
@@ -72,12 +78,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
             sys.stderr.write(r.stdout + r.stderr)
         if r.returncode:
             raise subprocess.CalledProcessError(r.returncode, f"nvcc {src}")
-    cmd = [NVCC, *ARCH, "-shared", "-o", LIB + ".tmp", *[_obj(s) for s in SOURCES], "-lpthread"]
+    cmd = [NVCC, *ARCH, "-shared", "-o", lib + ".tmp", *[_obj(s, obj_dir) for s in SOURCES], "-lpthread"]
     subprocess.run(cmd, check=True, cwd=HERE)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(lib + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, profile="--profile" in sys.argv))

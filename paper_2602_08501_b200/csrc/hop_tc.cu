@@ -99,7 +99,7 @@ static int tc_launch_t(const TcPatterns& t, int n, int nw, int A, int T, const f
     prm.y = y; prm.y64 = MODE == 3 ? y64 : nullptr;
     prm.s2 = s2; prm.pbits = P.bits; prm.btiles = LIMBS == 0 ? t.tiles8 : t.tiles; prm.tie_rel = 1e-5f;
     prm.cert_g = cert_gamma(s2.wmax, MODE == 3);
-    prm.experiment = MODE == 2 ? o.experiment : 0;
+    prm.experiment = (MODE == 1 || MODE == 2) ? o.experiment : 0;
     prm.trace = nullptr;
 #ifdef MPW_PROFILE
     static long long* trace = nullptr;

@@ -652,9 +652,9 @@ def wsd_step(y, center, x_center, sphere, m, counters=None):
     (decoders.py:374): every decision of `_wsd_step_core` -- the argmin of the
     survivor EDs and the strict accept test best_ed < ed_center -- depends on
     t alone (ED(x_center * s_p) - ED(x_center) = 4 sum_{supp p} t_i), so the
-    device hop runs from the sign pattern of x_center on the magnitudes
-    |y * x_center|, and the returned words are center ^ member as in the
-    reference (decoders.py:396-397)."""
+    device hop runs from the sign pattern of x_center on the received word
+    y * |x_center| (so that x' * y' = y * x_center), and the returned words
+    are center ^ member as in the reference (decoders.py:396-397)."""
     if m < 1:
         raise ValueError("m must be >= 1")
     if counters is None:
@@ -667,7 +667,7 @@ def wsd_step(y, center, x_center, sphere, m, counters=None):
     counters.ed_evaluations += 1
     dec = _hop_decoder(sphere)
     anc = pack_bits((xc < 0).astype(np.uint8)[None, :])
-    r = _run_hops(dec, np.abs(y * xc), anc, 1)
+    r = _run_hops(dec, y * np.abs(xc), anc, 1)
     _step_counters(counters, sphere, m, n)
     mem = int(r["hops"][0, 0, 0])
     if mem > 0:
@@ -760,7 +760,7 @@ def _two_stage_osd(y, code, stage1, params, sphere, counters) -> DecodeResult:
                                 params.activation_mode, want_hops=True, want_anchors=True)
     h = {k: v.cpu().numpy() for k, v in o.items()}
     counters.osd_reencodes += osd_candidate_count(stage1.order, code.k)
-    best64 = words32_to_64(h["best"][0].view(np.uint32), n)[0]
+    best64 = words32_to_64(h["best"][:1].view(np.uint32), n)[0]
     if h["stage"][0] == 0:
         return DecodeResult(best_codeword=BitVector(n, best64),
                             best_message=BitVector(int(code.k), dec.message_of_words(best64)),
@@ -806,7 +806,7 @@ def two_stage_decode(y, code, stage1, params, sphere, sigma=1.0, counters=None) 
                             params.activation_mode, want_hops=True, want_anchors=True)
     h = {k: v.cpu().numpy() for k, v in o.items()}
     counters.scl_node_ops += int(stage1.list_size) * n * (n.bit_length() - 1)
-    best64 = words32_to_64(h["best"][0].view(np.uint32), n)[0]
+    best64 = words32_to_64(h["best"][:1].view(np.uint32), n)[0]
     best = BitVector(n, best64)
     msg = BitVector(int(code.k), dec.message_of_words(best64))
     if h["stage"][0] == 0:

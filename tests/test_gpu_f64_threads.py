@@ -64,13 +64,16 @@ def test_two_stage_float64_vs_reference(fx, variant):
     np.testing.assert_allclose(_np(o["best_ed"])[ok], g["squared_ed"][ok], rtol=1e-12)
 
 
-def test_two_stage_float64_per_frame_dropin():
-    g = load("f64_two_stage_cfg3_crc_gated_1p0dB.npz")
-    cfg = configs.CONFIGS["cfg3"]
+@pytest.mark.parametrize("fx,step", [("f64_two_stage_cfg3_crc_gated_1p0dB.npz", 5),
+                                     ("f64_two_stage_cfg2_always_on_3p0dB.npz", 6),
+                                     ("f64_two_stage_cfg4_always_on_1p5dB.npz", 4)])
+def test_two_stage_float64_per_frame_dropin(fx, step):
+    g = load(fx)
+    cfg = configs.CONFIGS[fx.split("_")[3]]
     code, sph = code_and_sphere(cfg)
     params = WsdParams(radius_index=sph.radius_index, max_iterations=cfg.max_iterations,
-                       num_paths=cfg.num_paths, activation_mode="crc_gated")
-    for f in range(0, 200, 5):
+                       num_paths=cfg.num_paths, activation_mode="crc_gated" if int(g["gated"]) else "always_on")
+    for f in range(0, g["y64"].shape[0], step):
         r = two_stage_decode(g["y64"][f], code, SclStage(cfg.list_size), params, sph, sigma=float(g["sigma"]))
         assert (r.stage == "mp_wsd") == bool(g["stage"][f])
         np.testing.assert_array_equal(np.asarray(r.best_codeword.words), g["best"][f])

@@ -253,7 +253,7 @@ def _parse(argv=None):
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg4")
     ap.add_argument("--frames", type=int, default=1 << 17)
-    ap.add_argument("--variant", default="auto", choices=["auto", "gather", "tensor", "tensor2", "tensor_i8"])
+    ap.add_argument("--variant", default="auto", choices=["auto", "gather", "tensor", "tensor2", "tensor_i8", "tensor_i8a"])
     ap.add_argument("--seed", type=int, default=2026)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-step-seconds", type=float, default=10.0)
@@ -373,7 +373,7 @@ def run_ours(args, cfg, code, sph, sigma, backend: str = "nccl", device_index=No
         stage_h = torch.empty((F,), dtype=torch.uint8).pin_memory()
         ctr_h = torch.zeros((8,), dtype=torch.int64).pin_memory()
         mode = _native.MODE_CRC_GATED if cfg.activation_mode == "crc_gated" else _native.MODE_ALWAYS_ON
-        var = {"auto": 0, "gather": 1, "tensor": 2, "tensor2": 3, "tensor_i8": 4}[args.variant]
+        var = {"auto": 0, "gather": 1, "tensor": 2, "tensor2": 3, "tensor_i8": 4, "tensor_i8a": 5}[args.variant]
         stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
 
         def host_step(i):
@@ -411,14 +411,16 @@ def run_ours(args, cfg, code, sph, sigma, backend: str = "nccl", device_index=No
         variant_used = args.variant
         if variant_used == "auto":
             variant_used = dec.auto_variant
-        if variant_used == "tensor_i8":
+        if variant_used in ("tensor_i8", "tensor_i8a"):
             ops = evals / ws * 2.0 * code.n                # 2N int8 tensor ops per evaluation
             ach = ops / (hop_ms / 1000.0) / 1e12
             peak = per_sm_clk(micro["i8"]) / 1e12
-            traffic, tsrc = _ncu_traffic(f"hop_tc_i8_{args.frames}")
+            asyn = variant_used == "tensor_i8a"
+            traffic, tsrc = _ncu_traffic(f"hop_{'ar' if asyn else 'tc'}_i8_{args.frames}")
             roof = {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TOP/s",
                     "frac": ach / peak, "traffic": traffic, "traffic_source": tsrc,
-                    "kernel": "hop_tc_kernel<LIMBS=0> (kind::i8)", "op_per_eval": 2 * code.n,
+                    "kernel": "hop_ar_kernel (kind::i8, asynchronous rows)" if asyn
+                              else "hop_tc_kernel<LIMBS=0> (kind::i8)", "op_per_eval": 2 * code.n,
                     "peak_source": f"measured kind::i8 rate {micro['i8']:.0f} ops/clk/SM ({micro['source']}) x "
                                    f"{micro['sms']} SMs x {mhz:.0f} MHz (median SM clock of the timed region)",
                     "frac_of_2x_bf16_burst": ach / (2.0 * peaks["bf16_tflops"])}
@@ -450,7 +452,8 @@ def run_ours(args, cfg, code, sph, sigma, backend: str = "nccl", device_index=No
                 "dtype": {"gather": "f64 (stage 1) / f32 (stage 2 hop)",
                           "tensor": "f64 (stage 1) / f16 1-limb f32-accum screen + f64 certify (stage 2 hop)",
                           "tensor2": "f64 (stage 1) / f16 2-limb f32-accum + f64 certify (stage 2 hop)",
-                          "tensor_i8": "f64 (stage 1) / int8 s32-accum screen + f32/f64 certify (stage 2 hop)"}[variant_used],
+                          "tensor_i8": "f64 (stage 1) / int8 s32-accum screen + f32/f64 certify (stage 2 hop)",
+                          "tensor_i8a": "f64 (stage 1) / int8 s32-accum screen + f32/f64 certify (stage 2 hop)"}[variant_used],
                 "data": "synthetic (seeded block-keyed Philox AWGN, host-generated)",
                 "config": _config(args, cfg, code, sph),
                 "evals_per_s": evals / (ms_max / 1000.0),

@@ -15,7 +15,7 @@ c_int, c_double, c_void_p, c_uint32, c_int64, c_uint64 = (
     ctypes.c_int, ctypes.c_double, ctypes.c_void_p, ctypes.c_uint32, ctypes.c_int64, ctypes.c_uint64)
 
 MODE_CRC_GATED, MODE_ALWAYS_ON = 0, 1
-HOP_AUTO, HOP_GATHER, HOP_TENSOR, HOP_TENSOR_2LIMB, HOP_TENSOR_I8 = 0, 1, 2, 3, 4
+HOP_AUTO, HOP_GATHER, HOP_TENSOR, HOP_TENSOR_2LIMB, HOP_TENSOR_I8, HOP_TENSOR_I8_ASYNC = 0, 1, 2, 3, 4, 5
 CTR_FRAMES, CTR_ERRORS, CTR_ACTIVATIONS, CTR_ITERATIONS, CTR_EVALS, CTR_NEAR_TIE, CTR_UNRESOLVED = range(7)
 FLAG_TIE_ARGMIN, FLAG_TIE_ACCEPT, FLAG_TIE_FINAL, FLAG_UNRESOLVED = 1, 2, 4, 8
 FLAG_TIE_STAGE1 = 16

@@ -15,7 +15,7 @@ CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(CSRC, "build")
 LIB = os.path.join(HERE, "libmpwsd.so")
 PROF_LIB = os.path.join(HERE, "libmpwsd_prof.so")
-SOURCES = ["mpwsd.cu", "hop_tc.cu", "scl_lane.cu", "sphere_tools.cpp"]
+SOURCES = ["mpwsd.cu", "hop_tc.cu", "hop_ar.cu", "scl_lane.cu", "sphere_tools.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CFLAGS = [*ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3"]

@@ -1,0 +1,79 @@
+// Asynchronous-row int8 tensor hop: host side (launch, statistics).
+#include <cstdio>
+#include <cstring>
+
+#include "hop_ar.cuh"
+#include "hop_tc_api.h"
+
+static float ar_cert_gamma(int wmax) {
+    // any summation order of at most wmax terms: |fl(S) - S| <= gamma_{wmax-1} sum|t_i|
+    const double u = 5.9604644775390625e-8;
+    const double k = wmax > 1 ? wmax - 1 : 0;
+    return (float)(k * u / (1.0 - k * u) * 1.002);
+}
+
+bool ar_supported(const TcPatterns& t, int n) {
+    // u8 images present (|P| <= 2^17, 127 wmax < 8192), 64-pattern chunk ids fit 16 bits
+    return t.ready8 && (n == 128 || n == 256) && t.np <= (1 << 17);
+}
+
+template <int KB, int NW, bool STATS>
+static int ar_launch_t(const TcPatterns& t, int n, int A, int T, const float* y, S2Dev s2, PatDev P, int num_sms,
+                       cudaStream_t st) {
+    ar::Params prm;
+    prm.n = n; prm.nw = NW; prm.A = A; prm.T = T; prm.np = t.np; prm.ntiles = t.ntiles8;
+    prm.y = y; prm.s2 = s2; prm.pbits = P.bits; prm.btiles = t.tiles8;
+    prm.tie_rel = 1e-5f;
+    prm.cert_g = ar_cert_gamma(s2.wmax);
+    prm.stats = nullptr;
+    static unsigned long long* stats = nullptr;
+    if (STATS) {
+        if (!stats && cudaMallocManaged(&stats, sizeof(unsigned long long) * ar::ST_N) != cudaSuccess) return -1;
+        memset(stats, 0, sizeof(unsigned long long) * ar::ST_N);
+        prm.stats = stats;
+    }
+    const size_t smem = ar::smem_bytes(KB);
+    auto kern = ar::hop_ar_kernel<KB, NW, STATS>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return -(int)e;
+    kern<<<num_sms, ar::THREADS, smem, st>>>(prm);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return -(int)e;
+    if (STATS) {
+        cudaStreamSynchronize(st);
+        const unsigned long long* s = stats;
+        const double tiles = (double)s[ar::ST_TILES] / 32.0 / 8.0;   // per-lane counts of 8 scan warps
+        fprintf(stderr,
+                "[hop_ar] CTA-tiles %.0f, live row-halves %.4f, row cycles %llu (finished %llu), hit chunks/cycle %.3f, "
+                "entries/thread-cycle %.2f, f64 decisions %llu, overflow re-scans %llu, worker busy cycles/row-cycle %.0f\n",
+                tiles, s[ar::ST_TILES] ? (double)s[ar::ST_LIVE] / (double)s[ar::ST_TILES] : 0.0, s[ar::ST_ROWCYC],
+                s[ar::ST_FINISHED], s[ar::ST_ROWCYC] ? (double)s[ar::ST_CHUNKS] / (double)s[ar::ST_ROWCYC] : 0.0,
+                s[ar::ST_ROWCYC] ? (double)s[ar::ST_ENTRIES] / (2.0 * (double)s[ar::ST_ROWCYC]) : 0.0, s[ar::ST_F64],
+                s[ar::ST_OVF], s[ar::ST_ROWCYC] ? (double)s[ar::ST_BUSY] / (double)s[ar::ST_ROWCYC] : 0.0);
+        fprintf(stderr,
+                "[hop_ar] cycles per tile %.0f; issuer waits: B stage %.3f, accumulator %.3f of its time; scan warps wait "
+                "for the accumulator %.3f of their time\n",
+                tiles > 0 ? (double)s[ar::ST_ISS_TOT] / tiles : 0.0,
+                s[ar::ST_ISS_TOT] ? (double)s[ar::ST_ISS_FULL] / (double)s[ar::ST_ISS_TOT] : 0.0,
+                s[ar::ST_ISS_TOT] ? (double)s[ar::ST_ISS_TEMPTY] / (double)s[ar::ST_ISS_TOT] : 0.0,
+                s[ar::ST_SCAN_TOT] ? (double)s[ar::ST_SCAN_WAIT] / (double)s[ar::ST_SCAN_TOT] : 0.0);
+        const double rc = s[ar::ST_ROWCYC] ? (double)s[ar::ST_ROWCYC] : 1.0;
+        fprintf(stderr,
+                "[hop_ar] worker cycles per row cycle: lists+t %.0f, chunk scores %.0f, decision+move %.0f, claim+build %.0f, "
+                "publish %.0f, pocket refill %.0f\n",
+                s[ar::ST_W_LIST] / rc, s[ar::ST_W_CHUNK] / rc, s[ar::ST_W_DECIDE] / rc, s[ar::ST_W_CLAIM] / rc,
+                s[ar::ST_W_PUBLISH] / rc, s[ar::ST_W_POCKET] / rc);
+    }
+    return 0;
+}
+
+int ar_launch(const TcPatterns& t, int n, int nw, int A, int T, const float* y, S2Dev s2, PatDev P, int num_sms,
+              const TcOpts& o, cudaStream_t st) {
+    if (!ar_supported(t, n) || nw != n / 32) return 1;
+    const bool stats = o.experiment != 0;
+    if (n == 256)
+        return stats ? ar_launch_t<2, 8, true>(t, n, A, T, y, s2, P, num_sms, st)
+                     : ar_launch_t<2, 8, false>(t, n, A, T, y, s2, P, num_sms, st);
+    return stats ? ar_launch_t<1, 4, true>(t, n, A, T, y, s2, P, num_sms, st)
+                 : ar_launch_t<1, 4, false>(t, n, A, T, y, s2, P, num_sms, st);
+}

@@ -1,0 +1,679 @@
+// Stage 2, asynchronous-row int8 tensor hop (MPW_HOP_TENSOR_I8_ASYNC).
+//
+// Same contraction as the int8 screen of hop_tc.cuh (decoders.py:329-357):
+//     Q[r, p] = Σ_i q[r, i] · P[p, i],   t = x ⊙ y ≈ s·q,   ΔED = 4 S
+// with tcgen05.mma.kind::i8 into s32 TMEM accumulators, but without rounds:
+// the P tiles stream cyclically and never stop, and every trajectory row runs
+// its own scan cycle (ntiles consecutive tiles starting at any tile).  The
+// scan warps do no insertion and take no data-dependent branch per tile: per
+// 64-pattern chunk they keep the chunk minimum, the row's running minimum, and
+// append the chunks whose minimum lies inside the certification window of the
+// running minimum to a per-thread hit list in shared memory (a predicated
+// store).  When a row's cycle ends, a worker warp (four per CTA, rows
+// statically partitioned) filters the row's hit chunks against the final
+// minimum, scores every pattern of those chunks from y in fp32 (supports in
+// ascending position), certifies the argmin / accept decision
+// (decoders.py:385-398) with the recursive-summation bound or re-scores the
+// finalists in float64, applies the move to the row's int8 image (or stores
+// the trajectory and builds the next one from the stage-2 queue), and
+// publishes the tile at which the row's next cycle starts.  Rows are dead only
+// between their cycle end and that tile (a few tiles); no CTA-wide round end
+// exists, so the MMA stream is continuous.
+//
+// Exactness: a pattern outside every recorded chunk has Q_p >= m + wq for the
+// row's final minimum m, hence S_p > S_best + thr by the frame's quantisation
+// bound (same window as the synchronous int8 screen, common.cuh warp_i8_scale);
+// all patterns of the recorded chunks are scored from y, so the decision is
+// the exact one.  A hit list that overflows (CAP entries per thread and cycle)
+// makes the row scan once more with the achieved minimum as the seed of the
+// running minimum (then only true window chunks are recorded); the extra scan
+// is not counted in iterations_used.
+//
+// CTA = 14 warps, persistent, one per SM:
+//   warp 0       producer: cp.async.bulk of 32 KB pre-swizzled u8 P stages
+//   warp 1       TMEM allocator + tcgen05.mma issuer
+//   warps 2..9   scan: two per TMEM lane quarter (columns [0,128) / [128,256))
+//   warps 10..13 workers: decisions, moves, refills
+#pragma once
+#include "hop_tc.cuh"
+
+namespace ar {
+using namespace tc;
+
+constexpr int NWORK = 4;                       // worker warps
+constexpr int SCAN_T = 256;                    // scan threads (two per row)
+constexpr int THREADS = 64 + SCAN_T + 32 * NWORK;
+constexpr int CAP = 30;                        // hit-list entries per scan thread and cycle
+constexpr int AR_STAGES = 5;                   // P ring stages (one 128-position K-block of a tile each)
+constexpr int WSCR = 2 * 32 * 2;               // worker scratch: the row's hit chunks (uint16)
+constexpr int Q_INF = 0x7FFF;                  // s16 maximum: "no score"
+constexpr int MARGIN = 2;                      // tiles between the issue counter read and a row's first live tile
+static_assert(CAP <= 32, "one hit entry per worker lane");
+// a hit entry names a group of 32 patterns in 16 bits: |P| <= 2^17 gives 4096 groups
+static_assert(WSCR % 16 == 0, "worker scratch alignment");
+
+struct Params {
+    int n, nw, A, T, np, ntiles;
+    const float* y;
+    S2Dev s2;
+    const uint32_t* pbits;       // np x nw
+    const uint8_t* btiles;       // [ntiles][KB][256 x 128 u8] swizzled images
+    float tie_rel;
+    float cert_g;                // fp32 summation bound factor (cert_gamma)
+    unsigned long long* stats;   // STATS builds: counters (see hop_ar.cu)
+};
+
+__host__ __device__ constexpr size_t smem_bytes(int kb) {
+    return (size_t)kb * A_KBLK_BYTES + (size_t)AR_STAGES * I8_STAGE_BYTES + (size_t)CAP * SCAN_T * 4 +
+           ROWS * 8 /*row_ctl*/ + ROWS * 4 /*row_best*/ + ROWS * 4 /*row_done*/ + SCAN_T /*hit_cnt*/ +
+           NWORK * WSCR + (2 * AR_STAGES + 4) * 8 /*barriers*/ + 16 /*tmem slot, stop tile, issue counter, rows left*/;
+}
+
+__device__ __forceinline__ uint2 ld_shared_volatile_v2(const uint2* p) {
+    uint2 v;
+    asm volatile("ld.volatile.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(smem_u32(p)));
+    return v;
+}
+__device__ __forceinline__ void st_shared_volatile_v2(uint2* p, uint2 v) {
+    asm volatile("st.volatile.shared.v2.u32 [%0], {%1, %2};" ::"r"(smem_u32(p)), "r"(v.x), "r"(v.y) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_shared_volatile_u32(const volatile uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(const_cast<const uint32_t*>(p))));
+    return v;
+}
+__device__ __forceinline__ void st_shared_volatile_u32(volatile uint32_t* p, uint32_t v) {
+    asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"(smem_u32(const_cast<uint32_t*>(p))), "r"(v) : "memory");
+}
+
+// minimum of 32 packed s16 values (registers o .. o + 15): 8 three-input instructions
+__device__ __forceinline__ int min32_s16(const uint32_t (&v)[32], int o) {
+    const uint32_t a = min3_s16x2(v[o], v[o + 1], v[o + 2]), b = min3_s16x2(v[o + 3], v[o + 4], v[o + 5]);
+    const uint32_t c = min3_s16x2(v[o + 6], v[o + 7], v[o + 8]), d = min3_s16x2(v[o + 9], v[o + 10], v[o + 11]);
+    const uint32_t e = min3_s16x2(v[o + 12], v[o + 13], v[o + 14]);
+    const uint32_t f = min3_s16x2(a, b, c), g = min3_s16x2(d, e, v[o + 15]);
+    uint32_t r;
+    asm("min.s16x2 %0, %1, %2;" : "=r"(r) : "r"(f), "r"(g));
+    return min((int)(short)(r & 0xFFFFu), (int)(short)(r >> 16));
+}
+
+// minimum of 64 packed s16 values (32 registers): 16 three-input instructions
+__device__ __forceinline__ int min64_s16_only(const uint32_t (&v)[32]) {
+    uint32_t m[11];
+#pragma unroll
+    for (int e = 0; e < 10; e++) m[e] = min3_s16x2(v[3 * e], v[3 * e + 1], v[3 * e + 2]);
+    uint32_t r;
+    asm("min.s16x2 %0, %1, %2;" : "=r"(r) : "r"(v[30]), "r"(v[31]));
+    m[10] = r;
+    const uint32_t q0 = min3_s16x2(m[0], m[1], m[2]), q1 = min3_s16x2(m[3], m[4], m[5]);
+    const uint32_t q2 = min3_s16x2(m[6], m[7], m[8]), q3 = min3_s16x2(m[9], m[10], q0);
+    const uint32_t f = min3_s16x2(q1, q2, q3);
+    return min((int)(short)(f & 0xFFFFu), (int)(short)(f >> 16));
+}
+
+// stats slots
+enum { ST_TILES = 0, ST_LIVE, ST_ROWCYC, ST_CHUNKS, ST_F64, ST_OVF, ST_BUSY, ST_FINISHED, ST_ENTRIES,
+       ST_SCAN_WAIT, ST_SCAN_TOT, ST_ISS_FULL, ST_ISS_TEMPTY, ST_ISS_TOT, ST_W_LIST, ST_W_CHUNK, ST_W_DECIDE, ST_W_CLAIM,
+       ST_W_PUBLISH, ST_W_POCKET, ST_N };
+
+template <int KB, int NW, bool STATS>
+__global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
+    constexpr int STAGES = AR_STAGES;
+    constexpr int STB = I8_STAGE_BYTES;
+    extern __shared__ __align__(1024) unsigned char sm[];
+    if ((smem_u32(sm) & 1023u) != 0u) __trap();   // SW128 operands need 1024-byte alignment
+    unsigned char* a_rows = sm;
+    unsigned char* b_ring = sm + KB * A_KBLK_BYTES;
+    uint32_t* hits = reinterpret_cast<uint32_t*>(b_ring + STAGES * STB);    // [CAP][SCAN_T], slot-major
+    uint2* row_ctl = reinterpret_cast<uint2*>(hits + CAP * SCAN_T);         // [ROWS] {start tile, wq << 16 | seed + 8192}
+    int* row_best = reinterpret_cast<int*>(row_ctl + ROWS);                 // [ROWS] running minimum over both halves
+    int* row_done = row_best + ROWS;                                        // [ROWS] halves that finished the cycle
+    uint8_t* hit_cnt = reinterpret_cast<uint8_t*>(row_done + ROWS);         // [SCAN_T] entries recorded in the cycle
+    unsigned char* wscr = reinterpret_cast<unsigned char*>(hit_cnt + SCAN_T);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(wscr + NWORK * WSCR);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + STAGES;
+    uint64_t* tfull = bars + 2 * STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    volatile uint32_t* stop_tile = tmem_slot + 1;    // first tile nobody processes (0xFFFFFFFF while rows are left)
+    volatile uint32_t* issue_ctr = tmem_slot + 2;    // tile whose MMAs the issuer is about to issue
+    int* rows_left = reinterpret_cast<int*>(tmem_slot + 3);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n = prm.n, A = prm.A, T = prm.T, np_ = prm.np, ntiles = prm.ntiles;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; s++) { mbar_init(smem_u32(&full[s]), 1); mbar_init(smem_u32(&empty[s]), 1); }
+        for (int b = 0; b < 2; b++) { mbar_init(smem_u32(&tfull[b]), 1); mbar_init(smem_u32(&tempty[b]), 8); }
+        *stop_tile = 0xFFFFFFFFu;
+        *issue_ctr = 0u;
+        *rows_left = ROWS;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (int r = threadIdx.x; r < ROWS; r += THREADS) {
+        row_ctl[r] = make_uint2(0x80000000u, 0u);
+        row_best[r] = 0x7FFFFFFF;
+        row_done[r] = 0;
+    }
+    for (int r = threadIdx.x; r < SCAN_T; r += THREADS) hit_cnt[r] = 0;
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ===== producer: the P tiles, cyclically, until the stop tile
+        if (lane == 0) {
+            int stage = 0, j = 0;
+            uint32_t phase = 0;
+            for (uint32_t gt = 0;; gt++) {
+                if (gt >= ld_shared_volatile_u32(stop_tile)) break;
+                for (int kb = 0; kb < KB; kb++) {
+                    mbar_wait_issuer(smem_u32(&empty[stage]), phase ^ 1);
+                    const uint32_t fb = smem_u32(&full[stage]);
+                    mbar_expect_tx(fb, STB);
+                    bulk_g2s(smem_u32(b_ring + stage * STB), prm.btiles + ((size_t)j * KB + kb) * STB, STB, fb);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+                if (++j == ntiles) j = 0;
+            }
+        }
+    } else if (warp == 1) {
+        // ===== MMA issuer: one M128 N256 tile per step, K = 32 per instruction
+        if (lane == 0) {
+            const uint32_t idesc = (2u << 4) | (1u << 7) | ((uint32_t)(I8_TILE >> 3) << 17) | ((uint32_t)(ROWS >> 4) << 24);
+            const uint32_t abase = smem_u32(a_rows), bring = smem_u32(b_ring);
+            int stage = 0;
+            uint32_t phase = 0;
+            long long w_full = 0, w_tempty = 0, t_0 = 0, t_a = 0;
+            if (STATS) t_0 = clock64();
+            for (uint32_t gt = 0;; gt++) {
+                if (gt >= ld_shared_volatile_u32(stop_tile)) break;
+                const uint32_t buf = gt & 1u;
+                if (STATS) t_a = clock64();
+                mbar_wait_issuer(smem_u32(&tempty[buf]), ((gt >> 1) & 1u) ^ 1u);
+                if (STATS) w_tempty += clock64() - t_a;
+                tc_fence_after();
+                // published before the tile's MMAs are issued: a worker that reads v knows
+                // that no MMA of tile v + 1 has been issued yet
+                st_shared_volatile_u32(issue_ctr, gt);
+                const uint32_t d = tmem_base + buf * I8_TILE;
+                for (int kb = 0; kb < KB; kb++) {
+                    if (STATS) t_a = clock64();
+                    mbar_wait_issuer(smem_u32(&full[stage]), phase);
+                    if (STATS) w_full += clock64() - t_a;
+                    tc_fence_after();
+                    const uint64_t bd = sw128_desc(bring + stage * STB);
+                    const uint64_t ad = sw128_desc(abase + kb * A_KBLK_BYTES);
+#pragma unroll
+                    for (int ks = 0; ks < 4; ks++) tc_mma_i8(d, ad + 2 * ks, bd + 2 * ks, idesc, (kb | ks) != 0);
+                    tc_commit(smem_u32(&empty[stage]));
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+                tc_commit(smem_u32(&tfull[buf]));
+            }
+            if (STATS) {
+                atomicAdd(&prm.stats[ST_ISS_FULL], (unsigned long long)w_full);
+                atomicAdd(&prm.stats[ST_ISS_TEMPTY], (unsigned long long)w_tempty);
+                atomicAdd(&prm.stats[ST_ISS_TOT], (unsigned long long)(clock64() - t_0));
+            }
+        }
+    } else if (warp < 2 + SCAN_T / 32) {
+        // ===== scan: thread = (row, column half); no data-dependent branch per tile
+        const int g = warp & 3;                      // TMEM lane quarter of this warp
+        const int half = (warp - 2) >> 2;
+        const int row = g * 32 + lane;
+        const int thr = half * ROWS + row;
+        const int col0 = half * (I8_TILE / 2);
+        const uint32_t t_lane = tmem_base + ((uint32_t)(g * 32) << 16);
+        const bool ragged = (np_ % I8_TILE) != 0;
+        uint32_t seen = 0x80000000u;                 // start tile of the cycle this thread knows
+        int cnt = 0, m_run = Q_INF, pub = 0x7FFFFFFF, wq = 0;
+        int j = 0;
+        unsigned long long st_live = 0, st_tiles = 0, st_entries = 0;
+        long long sw_wait = 0, sw_0 = 0, sw_a = 0;
+        if (STATS) sw_0 = clock64();
+        for (uint32_t gt = 0;; gt++) {
+            if (gt >= ld_shared_volatile_u32(stop_tile)) break;
+            const uint32_t buf = gt & 1u;
+            if (STATS) sw_a = clock64();
+            while (!mbar_try_hint(smem_u32(&tfull[buf]), (gt >> 1) & 1u)) {}
+            if (STATS) sw_wait += clock64() - sw_a;
+            tc_fence_after();
+            uint32_t va[32], vb[32];
+            const uint32_t tbase = t_lane + buf * I8_TILE + col0;
+            TC_LD32P(tbase, va);
+            TC_LD32P(tbase + 64, vb);
+            // the row's control word, then the other half's published minimum (in this
+            // order: a new control word implies the reset of the minimum is visible)
+            const uint2 ctl = ld_shared_volatile_v2(&row_ctl[row]);
+            const int shb = ld_shared_volatile(&row_best[row]);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            // the accumulator goes back to the issuer; the scan below overlaps the next MMAs
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&tempty[buf]));
+            const int pa = j * I8_TILE + col0;
+            if (ragged && j == ntiles - 1) {
+                auto mask = [&](uint32_t& r, int p) {   // s16 maximum past |P|
+                    if (p >= np_) r = (r & 0xFFFF0000u) | 0x7FFFu;
+                    if (p + 1 >= np_) r = (r & 0xFFFFu) | 0x7FFF0000u;
+                };
+#pragma unroll
+                for (int e = 0; e < 32; e++) {
+                    mask(va[e], pa + 2 * e);
+                    mask(vb[e], pa + 64 + 2 * e);
+                }
+            }
+            // minima of the thread's four 32-pattern groups (16 packed registers each)
+            const int m0 = min32_s16(va, 0), m1 = min32_s16(va, 16), m2 = min32_s16(vb, 0), m3 = min32_s16(vb, 16);
+            const bool isnew = ctl.x != seen;
+            seen = ctl.x;
+            if (isnew) {
+                cnt = 0;
+                m_run = (int)(ctl.y & 0xFFFFu) - KEY_BIAS;
+                pub = 0x7FFFFFFF;
+                wq = (int)(ctl.y >> 16);
+                if (gt > ctl.x) __trap();   // the start tile was observed late: protocol violation, fail the launch
+            }
+            const uint32_t age = gt - seen;
+            const bool live = age < (uint32_t)ntiles;
+            const int mt = min(min(m0, m1), min(m2, m3));
+            if (live) m_run = min(m_run, min(mt, shb));
+            const int lim = m_run + wq;
+            const uint32_t grp0 = (uint32_t)pa >> 5;
+            auto record = [&](int m, uint32_t grp) {
+                const bool h = live && m < lim;
+                if (h && cnt < CAP) hits[cnt * SCAN_T + thr] = ((uint32_t)(m + KEY_BIAS) << 16) | grp;
+                cnt += h ? 1 : 0;
+            };
+            record(m0, grp0);
+            record(m1, grp0 + 1u);
+            record(m2, grp0 + 2u);
+            record(m3, grp0 + 3u);
+            if (live && mt < pub) { atomicMin(&row_best[row], mt); pub = mt; }
+            if (STATS) { st_tiles++; st_live += live ? 1 : 0; }
+            if (live && age == (uint32_t)(ntiles - 1)) {
+                // cycle end: hand the hit list to the row's worker
+                if (STATS) st_entries += cnt;
+                hit_cnt[thr] = (uint8_t)min(cnt, 255);
+                __threadfence_block();
+                atomicAdd(&row_done[row], 1);
+            }
+            if (++j == ntiles) j = 0;
+        }
+        if (STATS) {
+            atomicAdd(&prm.stats[ST_TILES], st_tiles);
+            atomicAdd(&prm.stats[ST_LIVE], st_live);
+            atomicAdd(&prm.stats[ST_ENTRIES], st_entries);
+            if (lane == 0) {
+                atomicAdd(&prm.stats[ST_SCAN_WAIT], (unsigned long long)sw_wait);
+                atomicAdd(&prm.stats[ST_SCAN_TOT], (unsigned long long)(clock64() - sw_0));
+            }
+        }
+    } else {
+        // ===== workers: worker w owns rows lane * NWORK + w; the row state lives in
+        // the registers of the lane that owns the row and is broadcast by shuffles
+        const int w = warp - (2 + SCAN_T / 32);
+        uint16_t* chl = reinterpret_cast<uint16_t*>(wscr + w * WSCR);       // hit chunks of the row [2 CAP]
+        const int myrow = lane * NWORK + w;
+        int tr = -1, frame = 0, iters = 0, wq = 0;
+        uint32_t flags = 0;
+        float ed = 0.f, err = 0.f, inv_s = 1.f, ay = 0.f;
+        uint32_t c[NW];
+#pragma unroll
+        for (int k = 0; k < NW; k++) c[k] = 0u;
+        bool fresh = true, exhausted = false, recyc = false;
+        const int count = *prm.s2.count;
+        const int ntraj = count * A;
+        // the worker's pocket: the next trajectory of the stage-2 queue, claimed ahead of
+        // its use (queue slot x anchor; short lists skip), its frame's y and anchor on
+        // their way into L2.  pk_tr: -1 queue exhausted
+        int pk_tr = -1, pk_frame = 0;
+        float4 pk_qs = make_float4(1.f, 1.f, 0.f, 0.f);
+        auto refill_pocket = [&]() {
+            int ntr = -1, nq = 0;
+            if (lane == 0) {
+                for (;;) {
+                    const int cand = atomicAdd(prm.s2.work_next, 1);
+                    if (cand >= ntraj) break;
+                    const int q = cand / A, a = cand - q * A;
+                    if (a >= prm.s2.nanchor[q]) continue;
+                    ntr = cand;
+                    nq = q;
+                    break;
+                }
+            }
+            ntr = __shfl_sync(MPW_FULL, ntr, 0);
+            nq = __shfl_sync(MPW_FULL, nq, 0);
+            pk_tr = ntr;
+            if (ntr >= 0) {
+                pk_frame = prm.s2.frame[nq];
+                pk_qs = prm.s2.qscale[nq];
+                if (lane * 128 < n * 4) prefetch_l2(reinterpret_cast<const char*>(prm.y + (size_t)pk_frame * n) + lane * 128);
+                if (lane == 31) prefetch_l2(prm.s2.anchors + (size_t)ntr * NW);
+            }
+        };
+        refill_pocket();
+        unsigned long long st_rowcyc = 0, st_chunks = 0, st_f64 = 0, st_ovf = 0, st_busy = 0, st_fin = 0;
+        long long ph[6] = {0, 0, 0, 0, 0, 0}, t_ph = 0;
+#define PH(k) if (STATS) { const long long t_ = clock64(); ph[k] += t_ - t_ph; t_ph = t_; }
+        for (;;) {
+            if (ld_shared_volatile_u32(stop_tile) != 0xFFFFFFFFu) break;
+            const int d = fresh ? 2 : (exhausted ? 0 : ld_shared_volatile(&row_done[myrow]));
+            const unsigned ready = __ballot_sync(MPW_FULL, d == 2);
+            if (!ready) { __nanosleep(64); continue; }
+            long long t_busy0 = 0;
+            if (STATS) { t_busy0 = clock64(); t_ph = t_busy0; }
+            const int L = __ffs(ready) - 1;
+            const int row = L * NWORK + w;
+            // the row's state, broadcast from its owner lane
+            int tr_ = __shfl_sync(MPW_FULL, tr, L), frame_ = __shfl_sync(MPW_FULL, frame, L);
+            int iters_ = __shfl_sync(MPW_FULL, iters, L), wq_ = __shfl_sync(MPW_FULL, wq, L);
+            uint32_t flags_ = __shfl_sync(MPW_FULL, flags, L);
+            float ed_ = __shfl_sync(MPW_FULL, ed, L), err_ = __shfl_sync(MPW_FULL, err, L);
+            float inv_ = __shfl_sync(MPW_FULL, inv_s, L), ay_ = __shfl_sync(MPW_FULL, ay, L);
+            bool recyc_ = __shfl_sync(MPW_FULL, (int)recyc, L) != 0;
+            uint32_t c_[NW];
+#pragma unroll
+            for (int k = 0; k < NW; k++) c_[k] = __shfl_sync(MPW_FULL, c[k], L);
+            int seed = Q_INF;
+            bool need_claim = tr_ < 0;
+            bool exhausted_ = false;
+            bool used_pocket = false;
+            if (tr_ >= 0) {
+                // the frame's y (this lane's 8 positions) is on its way while the hit lists are read
+                const float* yr = prm.y + (size_t)frame_ * n;
+                float4 ya = make_float4(0.f, 0.f, 0.f, 0.f), yb = ya;
+                if (lane * 8 < n) {
+                    const float4* y4 = reinterpret_cast<const float4*>(yr) + lane * 2;
+                    ya = __ldg(y4);
+                    yb = __ldg(y4 + 1);
+                }
+                __threadfence_block();
+                const int mfin = ld_shared_volatile(&row_best[row]);
+                const int cnt0 = hit_cnt[row], cnt1 = hit_cnt[ROWS + row];
+                const bool ovf = cnt0 > CAP || cnt1 > CAP;
+                if (STATS) st_rowcyc++;
+                if (ovf && !recyc_) {
+                    // hit list overflow: scan once more, recording only the chunks inside
+                    // the window of the achieved minimum
+                    if (STATS) st_ovf++;
+                    recyc_ = true;
+                    seed = mfin;
+                } else {
+                    if (ovf) flags_ |= MPW_F_UNRESOLVED;
+                    recyc_ = false;
+                    // the row's hit groups (32 patterns): entries of both halves inside the window of the final minimum
+                    const int limit = mfin + wq_;
+                    int nh = 0;
+#pragma unroll
+                    for (int hf = 0; hf < 2; hf++) {
+                        const int cnt = min(hf ? cnt1 : cnt0, CAP);
+                        const uint32_t ent = lane < cnt ? hits[lane * SCAN_T + hf * ROWS + row] : 0xFFFFFFFFu;
+                        const bool ok = lane < cnt && (int)(ent >> 16) - KEY_BIAS < limit;
+                        const unsigned m = __ballot_sync(MPW_FULL, ok);
+                        if (ok) chl[nh + __popc(m & ((1u << lane) - 1u))] = (uint16_t)(ent & 0xFFFFu);
+                        nh += __popc(m);
+                    }
+                    __syncwarp();
+                    PH(0);
+                    const double bnd = (double)ay_ * (double)prm.cert_g;   // |fl(S) - S| of the fp32 sums
+                    const float thr = prm.tie_rel * ed_ * 0.25f;
+                    const double Md = 2.0 * bnd + (double)thr;
+                    float Bs = CUDART_INF_F;
+                    int Bi = 0x7FFFFFFF, nf = 0;
+                    float fs = CUDART_INF_F;   // finalist `lane`: fp32 score, pattern
+                    int fi = 0x7FFFFFFF;
+                    uint32_t pw = 0u;      // lanes < NW: word `lane` of the running best pattern
+                    // per hit group (32 patterns, one per lane): the exact integer score Q_p
+                    // by DP4A of the row's int8 image (broadcast from shared memory) with the
+                    // pattern's bits expanded to 0/1 bytes; the patterns inside the window of
+                    // the final minimum are then scored from y in fp32, the warp summing one
+                    // pattern at a time (8 positions per lane, butterfly sum)
+                    auto load_bits = [&](int grp, uint32_t (&bw)[NW]) {
+                        const int p = grp * 32 + lane;
+#pragma unroll
+                        for (int k = 0; k < NW; k++) bw[k] = 0u;
+                        if (p < np_) {
+                            const uint4* s4 = reinterpret_cast<const uint4*>(prm.pbits + (size_t)p * NW);
+#pragma unroll
+                            for (int k = 0; k < NW / 4; k++) {
+                                const uint4 v = __ldg(s4 + k);
+                                bw[4 * k] = v.x; bw[4 * k + 1] = v.y; bw[4 * k + 2] = v.z; bw[4 * k + 3] = v.w;
+                            }
+                        }
+                    };
+                    uint32_t bwn[NW];
+                    if (nh > 0) load_bits((int)chl[0], bwn);
+#pragma unroll 1
+                    for (int ih = 0; ih < nh; ih++) {
+                        const int grp = (int)chl[ih];
+                        uint32_t bw[NW];
+#pragma unroll
+                        for (int k = 0; k < NW; k++) bw[k] = bwn[k];
+                        if (ih + 1 < nh) load_bits((int)chl[ih + 1], bwn);   // in flight during this group
+                        int Q0 = 0, Q1 = 0;
+#pragma unroll
+                        for (int cc = 0; cc < NW * 2; cc++) {
+                            const uint4 qv = *reinterpret_cast<const uint4*>(a_rows + (cc >> 3) * A_KBLK_BYTES +
+                                                                             sw128_chunk(row, cc & 7));
+                            const uint32_t b16 = bw[cc >> 1] >> (16 * (cc & 1));
+                            auto ex = [](uint32_t nib) { return (int)(((nib & 0xFu) * 0x00204081u) & 0x01010101u); };
+                            Q0 = __dp4a((int)qv.x, ex(b16), Q0);
+                            Q1 = __dp4a((int)qv.y, ex(b16 >> 4), Q1);
+                            Q0 = __dp4a((int)qv.z, ex(b16 >> 8), Q0);
+                            Q1 = __dp4a((int)qv.w, ex(b16 >> 12), Q1);
+                        }
+                        unsigned cm = __ballot_sync(MPW_FULL, grp * 32 + lane < np_ && Q0 + Q1 < limit);
+                        if (STATS) st_chunks++;
+                        while (cm) {
+                            const int src_l = __ffs(cm) - 1;
+                            cm &= cm - 1;
+                            const int pc = grp * 32 + src_l;
+                            // the candidate's bits from the lane that holds them
+                            uint32_t myw = 0u, pwc = 0u;
+#pragma unroll
+                            for (int k = 0; k < NW; k++) {
+                                const uint32_t x = __shfl_sync(MPW_FULL, bw[k], src_l);
+                                if (k == (lane >> 2)) myw = x;
+                                if (k == lane) pwc = x;
+                            }
+                            const uint32_t byte = (myw >> ((lane & 3) * 8)) & 0xFFu;
+                            const uint32_t cw = select_word<NW>(c_, (lane >> 2) & (NW - 1)) >> ((lane & 3) * 8);
+                            const float yv[8] = {ya.x, ya.y, ya.z, ya.w, yb.x, yb.y, yb.z, yb.w};
+                            float sp = 0.f;
+#pragma unroll
+                            for (int k = 0; k < 8; k++)
+                                if ((byte >> k) & 1u) sp += __uint_as_float(__float_as_uint(yv[k]) ^ (((cw >> k) & 1u) << 31));
+#pragma unroll
+                            for (int o = 16; o > 0; o >>= 1) sp += __shfl_xor_sync(MPW_FULL, sp, o);
+                            if (sp < Bs || (sp == Bs && pc < Bi)) { Bs = sp; Bi = pc; pw = pwc; }
+                            // finalists: everything within the certification margin of the running best
+                            if ((double)sp < (double)Bs + Md) {
+                                if (lane == nf) { fs = sp; fi = pc; }
+                                nf++;
+                            }
+                        }
+                    }
+                    PH(1);
+                    if (nf > 32) flags_ |= MPW_F_UNRESOLVED;   // more near-equal scores than lanes
+                    const bool keep = (double)fs < (double)Bs + Md;
+                    const int nk = __popc(__ballot_sync(MPW_FULL, keep));
+                    int best = Bi;
+                    bool improve = false;
+                    float sb = 0.f;
+                    const double aB = fabs((double)Bs);
+                    if (nk == 1 && aB > bnd && fabs(aB - (double)thr) > bnd) {
+                        // the fp32 decision is the exact one
+                        improve = Bs < 0.f;
+                        sb = Bs;
+                        if (aB < (double)thr) flags_ |= MPW_F_TIE_ACCEPT;
+                    } else if (nk >= 1) {
+                        // float64 scores of the finalists (ascending positions), one per lane
+                        if (STATS) st_f64++;
+                        double e = CUDART_INF;
+                        if (keep) e = exact_score<NW>(yr, c_, prm.pbits + (size_t)fi * NW, NW, n);
+                        double be = e;
+                        int bi = keep ? fi : 0x7FFFFFFF;
+#pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) {
+                            const double oe = __shfl_xor_sync(MPW_FULL, be, o);
+                            const int oi = __shfl_xor_sync(MPW_FULL, bi, o);
+                            if (oe < be || (oe == be && oi < bi)) { be = oe; bi = oi; }
+                        }
+                        double e2 = (keep && fi != bi) ? e : CUDART_INF;
+#pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) e2 = fmin(e2, __shfl_xor_sync(MPW_FULL, e2, o));
+                        best = bi;
+                        if (e2 - be < (double)thr) flags_ |= MPW_F_TIE_ARGMIN;
+                        improve = be < 0.0;
+                        if (fabs(be) < (double)thr) flags_ |= MPW_F_TIE_ACCEPT;
+                        sb = (float)be;
+                    }
+                    iters_++;
+                    if (improve) {
+                        // the move: c ^= p, the moved positions' int8 values negated
+                        if (best != Bi) pw = lane < NW ? __ldg(prm.pbits + (size_t)best * NW + lane) : 0u;
+#pragma unroll
+                        for (int k = 0; k < NW; k++) c_[k] ^= __shfl_sync(MPW_FULL, pw, k);
+                        const uint32_t word = __shfl_sync(MPW_FULL, pw, (lane >> 2) & (NW - 1));
+                        const uint32_t b8 = (word >> ((lane & 3) * 8)) & 0xFFu;
+                        if (b8 && lane * 8 < n) {
+                            uint2* pq = reinterpret_cast<uint2*>(a_rows + (lane >> 4) * A_KBLK_BYTES +
+                                                                 sw128_chunk(row, (lane & 15) >> 1) + (lane & 1) * 8);
+                            uint2 v = *pq;
+                            uint32_t m = byte_mask4(b8 & 0xFu);
+                            v.x = (v.x & ~m) | (__vsub4(0u, v.x) & m);
+                            m = byte_mask4(b8 >> 4);
+                            v.y = (v.y & ~m) | (__vsub4(0u, v.y) & m);
+                            *pq = v;
+                        }
+                        ed_ += 4.f * sb;
+                        if (prm.s2.traj_hops && lane == 0) prm.s2.traj_hops[(size_t)tr_ * T + iters_ - 1] = best + 1;
+                    }
+                    if (!improve || iters_ == T) {
+                        // the trajectory is complete (decoders.py:441-451)
+                        if (prm.s2.traj_hops && lane == 0)
+                            for (int h = iters_ - (improve ? 0 : 1); h < T; h++) prm.s2.traj_hops[(size_t)tr_ * T + h] = -1;
+                        if (lane < NW) prm.s2.traj_cw[(size_t)tr_ * NW + lane] = select_word<NW>(c_, lane);
+                        if (lane == 0) {
+                            prm.s2.traj_iters[tr_] = iters_;
+                            prm.s2.traj_flags[tr_] = (uint8_t)flags_;
+                        }
+                        if (STATS) st_fin++;
+                        need_claim = true;
+                    }
+                }
+            }
+            PH(2);
+            if (need_claim) {
+                tr_ = pk_tr;
+                if (pk_tr < 0) {
+                    exhausted_ = true;
+                    if (lane == 0 && atomicSub(rows_left, 1) == 1) {
+                        // the CTA's last row: everybody stops a few tiles past the issuer
+                        // (beyond the producer's look-ahead of STAGES / KB tiles)
+                        st_shared_volatile_u32(stop_tile, ld_shared_volatile_u32(issue_ctr) + 4u + STAGES);
+                    }
+                } else {
+                    used_pocket = true;
+                    frame_ = pk_frame;
+                    inv_ = pk_qs.x;
+                    err_ = pk_qs.z;
+                    ay_ = pk_qs.w;
+                    const uint32_t aw = lane < NW ? __ldg(prm.s2.anchors + (size_t)tr_ * NW + lane) : 0u;
+                    float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+                    if (lane * 8 < n) {
+                        const float4* y4 = reinterpret_cast<const float4*>(prm.y + (size_t)frame_ * n) + lane * 2;
+                        a = __ldg(y4);
+                        b = __ldg(y4 + 1);
+                    }
+#pragma unroll
+                    for (int k = 0; k < NW; k++) c_[k] = __shfl_sync(MPW_FULL, aw, k);
+                    // the row's int8 image q_i = ±rint(|y_i| inv_s) and the fp32 canonical ED
+                    float syy = 0.f, sxy = 0.f;
+                    if (lane * 8 < n) {
+                        const float yv[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+                        const uint32_t cw = select_word<NW>(c_, lane >> 2) >> ((lane & 3) * 8);
+                        uint32_t qw[2] = {0u, 0u};
+#pragma unroll
+                        for (int b_ = 0; b_ < 8; b_++) {
+                            const float v = yv[b_];
+                            const int q = i8_quant(fabsf(v), inv_);
+                            const bool neg = (((cw >> b_) & 1u) != 0u) != (v < 0.0f);
+                            qw[b_ >> 2] |= ((uint32_t)(neg ? -q : q) & 0xFFu) << (8 * (b_ & 3));
+                            syy = fmaf(v, v, syy);
+                            sxy += __uint_as_float(__float_as_uint(v) ^ (((cw >> b_) & 1u) << 31));
+                        }
+                        *reinterpret_cast<uint2*>(a_rows + (lane >> 4) * A_KBLK_BYTES + sw128_chunk(row, (lane & 15) >> 1) +
+                                                  (lane & 1) * 8) = make_uint2(qw[0], qw[1]);
+                    }
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) {
+                        syy += __shfl_xor_sync(MPW_FULL, syy, o);
+                        sxy += __shfl_xor_sync(MPW_FULL, sxy, o);
+                    }
+                    ed_ = syy + (float)n - 2.0f * sxy;
+                    iters_ = 0;
+                    flags_ = 0u;
+                    recyc_ = false;
+                }
+            }
+            PH(3);
+            if (!exhausted_) {
+                // window of the next cycle in q units (rounded up; >= 16384 records everything)
+                const float wf = (2.0f * err_ + prm.tie_rel * ed_ * 0.25f) * inv_ * 1.00001f + 1.0f;
+                wq_ = wf < 16384.f ? __float2int_ru(wf) : 16384;
+                // the row image is complete and visible to the tensor core's reads of
+                // every MMA issued from now on
+                fence_proxy_async();
+                __syncwarp();
+                if (lane == 0) {
+                    row_best[row] = 0x7FFFFFFF;
+                    row_done[row] = 0;
+                    __threadfence_block();
+                    const uint32_t v = ld_shared_volatile_u32(issue_ctr);
+                    st_shared_volatile_v2(&row_ctl[row],
+                                          make_uint2(v + MARGIN, ((uint32_t)wq_ << 16) | (uint32_t)(seed + KEY_BIAS)));
+                }
+            }
+            if (lane == L) {
+                tr = tr_; frame = frame_; iters = iters_; wq = wq_; flags = flags_;
+                ed = ed_; err = err_; inv_s = inv_; ay = ay_;
+                recyc = recyc_;
+                fresh = false;
+                exhausted = exhausted_;
+#pragma unroll
+                for (int k = 0; k < NW; k++) c[k] = c_[k];
+            }
+            PH(4);
+            if (used_pocket) refill_pocket();   // after the row is live again
+            PH(5);
+            if (STATS) st_busy += clock64() - t_busy0;
+        }
+#undef PH
+        if (STATS && lane == 0) {
+            atomicAdd(&prm.stats[ST_ROWCYC], st_rowcyc);
+            atomicAdd(&prm.stats[ST_CHUNKS], st_chunks);
+            atomicAdd(&prm.stats[ST_F64], st_f64);
+            atomicAdd(&prm.stats[ST_OVF], st_ovf);
+            atomicAdd(&prm.stats[ST_BUSY], st_busy);
+            atomicAdd(&prm.stats[ST_FINISHED], st_fin);
+            for (int k = 0; k < 6; k++) atomicAdd(&prm.stats[ST_W_LIST + k], (unsigned long long)ph[k]);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+    }
+}
+
+}  // namespace ar

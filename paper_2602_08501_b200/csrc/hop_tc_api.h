@@ -36,3 +36,10 @@ int tc_build(TcPatterns& t, const uint32_t* bits, int np, int n, int nw);
 // rounding; only the 1-limb screen takes them.
 int tc_launch(const TcPatterns& t, int n, int nw, int A, int T, const float* y, const double* y64, S2Dev s2,
               PatDev P, int num_sms, int limbs, const TcOpts& o, cudaStream_t st);
+
+// Asynchronous-row int8 hop (hop_ar.cuh): rows scan P in their own cycles, worker
+// warps decide; needs the u8 images of TcPatterns.
+// o.experiment != 0 launches the statistics build (one line on stderr per launch).
+bool ar_supported(const TcPatterns& t, int n);
+int ar_launch(const TcPatterns& t, int n, int nw, int A, int T, const float* y, S2Dev s2, PatDev P, int num_sms,
+              const TcOpts& o, cudaStream_t st);

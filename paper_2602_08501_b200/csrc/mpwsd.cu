@@ -472,6 +472,16 @@ int run_hops(mpw_handle* h, const float* y, const double* y64, int Fmax, int A, 
     variant = resolve_variant(h, variant, y64 != nullptr);
     if (y64 && (variant == MPW_HOP_TENSOR_2LIMB || variant == MPW_HOP_TENSOR_I8))
         return fail(MPW_ERR_UNSUPPORTED, "float64 received words use the 1-limb tensor or the gather hop");
+    if (variant == MPW_HOP_TENSOR_I8_ASYNC) {
+        if (y64) return fail(MPW_ERR_UNSUPPORTED, "float64 received words use the 1-limb tensor or the gather hop");
+        if (!ar_supported(h->tcp, h->n))
+            return fail(MPW_ERR_UNSUPPORTED, "asynchronous int8 tensor-core hop needs N = 128 or 256 and the u8 operand images");
+        int rc = ar_launch(h->tcp, h->n, h->nw, A, T, y, s2, pat_dev(h), h->num_sms, h->tco, st);
+        if (rc) return fail(MPW_ERR_CUDA, "asynchronous tensor-core hop launch failed: %s",
+                            rc < 0 ? cudaGetErrorString((cudaError_t)-rc) : "unsupported shape");
+        h->kernel_launches++;
+        return 0;
+    }
     if (variant == MPW_HOP_TENSOR || variant == MPW_HOP_TENSOR_2LIMB || variant == MPW_HOP_TENSOR_I8) {
         if (!h->tcp.ready) return fail(MPW_ERR_UNSUPPORTED, "tensor-core hop operand not built for this pattern set");
         if (variant == MPW_HOP_TENSOR_I8 && !h->tcp.ready8)

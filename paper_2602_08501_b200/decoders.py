@@ -222,7 +222,8 @@ def words32_to_64(words32: np.ndarray, n: int) -> np.ndarray:
 # Device decoder: one libmpwsd handle bound to (code, pattern set)
 
 _HOP = {"auto": _native.HOP_AUTO, "gather": _native.HOP_GATHER, "tensor": _native.HOP_TENSOR,
-        "tensor2": _native.HOP_TENSOR_2LIMB, "tensor_i8": _native.HOP_TENSOR_I8}
+        "tensor2": _native.HOP_TENSOR_2LIMB, "tensor_i8": _native.HOP_TENSOR_I8,
+        "tensor_i8a": _native.HOP_TENSOR_I8_ASYNC}
 
 
 class DeviceDecoder:

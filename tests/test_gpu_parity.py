@@ -46,11 +46,11 @@ def test_scl_lists_bit_exact_vs_reference(fx):
         np.testing.assert_array_equal(pm[f, :c], g["list_pm"][f, :c])
 
 
-VARIANTS = ["gather", "tensor", "tensor2", "tensor_i8"]
+VARIANTS = ["gather", "tensor", "tensor2", "tensor_i8", "tensor_i8a"]
 
 
 def _skip_i8(variant, n):
-    if variant == "tensor_i8" and n not in (128, 256):
+    if variant in ("tensor_i8", "tensor_i8a") and n not in (128, 256):
         pytest.skip("int8 screen: N = 128, 256")
 
 
@@ -94,7 +94,7 @@ def test_two_stage_vs_oracle_random_frames(name, variant):
     from paper_2602_08501_b200 import channel
     sigma = cfg.sigma(code=code)
     F = {"cfg1": 4096, "cfg3": 2048, "cfg2": 256, "cfg4": 96}[name]
-    if variant == "tensor_i8" and name in ("cfg2", "cfg4"):
+    if variant in ("tensor_i8", "tensor_i8a") and name in ("cfg2", "cfg4"):
         F *= 4      # the int8 screen's wider window: more frames
     if name == "cfg4" and variant == "gather":
         F = 32
@@ -115,7 +115,8 @@ def test_two_stage_vs_oracle_random_frames(name, variant):
 
 
 @pytest.mark.parametrize("variant,name", [(v, "cfg1") for v in VARIANTS[:3]] +
-                         [("tensor_i8", "cfg3"), ("tensor_i8", "cfg2"), ("tensor", "cfg2")])
+                         [("tensor_i8", "cfg3"), ("tensor_i8", "cfg2"), ("tensor", "cfg2"),
+                          ("tensor_i8a", "cfg3"), ("tensor_i8a", "cfg2")])
 def test_mp_wsd_random_anchors_vs_oracle(variant, name):
     cfg = configs.CONFIGS[name]
     code, sph = code_and_sphere(cfg)

@@ -29,34 +29,44 @@
 // running minimum (then only true window chunks are recorded); the extra scan
 // is not counted in iterations_used.
 //
-// CTA = 14 warps, persistent, one per SM:
-//   warp 0       producer: cp.async.bulk of 32 KB pre-swizzled u8 P stages
-//   warp 1       TMEM allocator + tcgen05.mma issuer
-//   warps 2..9   scan: two per TMEM lane quarter (columns [0,128) / [128,256))
-//   warps 10..13 workers: decisions, moves, refills
+// CTA = 20 warps, persistent, one per SM:
+//   warp 0        producer: cp.async.bulk of 32 KB pre-swizzled u8 P stages
+//   warp 1        TMEM allocator + tcgen05.mma issuer (warps 2, 3 idle: they fill the warpgroup)
+//   warps 4..11   scan: two per TMEM lane quarter (columns [0,128) / [128,256))
+//   warps 12..19  workers: decisions, moves, refills
+// Register budgets (setmaxnreg; the CTA's pool is what its own warps release): warps 0..3
+// drop from 96 to 40 registers, the workers take 120, the scan warps stay at 96.
 #pragma once
 #include "hop_tc.cuh"
 
 namespace ar {
 using namespace tc;
 
-constexpr int NWORK = 4;                       // worker warps
+#ifndef MPW_AR_NWORK
+#define MPW_AR_NWORK 8
+#endif
+constexpr int NWORK = MPW_AR_NWORK;            // worker warps (rows statically partitioned)
+static_assert(ROWS % NWORK == 0 && ROWS / NWORK <= 32, "rows per worker");
 constexpr int SCAN_T = 256;                    // scan threads (two per row)
-constexpr int THREADS = 64 + SCAN_T + 32 * NWORK;
+// warps 0..3: producer, MMA issuer, two idle (one warpgroup, so the three register budgets
+// below can be set per warpgroup); warps 4..11 scan; warps 12.. workers
+constexpr int SCAN_W0 = 4;
+constexpr int WORK_W0 = SCAN_W0 + SCAN_T / 32;
+constexpr int THREADS = 32 * (WORK_W0 + NWORK);
+static_assert(NWORK % 4 == 0, "worker warps in whole warpgroups");
 constexpr int CAP = 30;                        // hit-list entries per scan thread and cycle
 constexpr int AR_STAGES = 5;                   // P ring stages (one 128-position K-block of a tile each)
-constexpr int WSCR = 2 * 32 * 2;               // worker scratch: the row's hit chunks (uint16)
 constexpr int Q_INF = 0x7FFF;                  // s16 maximum: "no score"
 constexpr int MARGIN = 2;                      // tiles between the issue counter read and a row's first live tile
 static_assert(CAP <= 32, "one hit entry per worker lane");
 // a hit entry names a group of 32 patterns in 16 bits: |P| <= 2^17 gives 4096 groups
-static_assert(WSCR % 16 == 0, "worker scratch alignment");
 
 struct Params {
     int n, nw, A, T, np, ntiles;
     const float* y;
     S2Dev s2;
     const uint32_t* pbits;       // np x nw
+    const uint4* pbT;            // bits transposed for the workers: [group of 32 patterns][n / 8 position bytes][32 patterns]
     const uint8_t* btiles;       // [ntiles][KB][256 x 128 u8] swizzled images
     float tie_rel;
     float cert_g;                // fp32 summation bound factor (cert_gamma)
@@ -66,7 +76,7 @@ struct Params {
 __host__ __device__ constexpr size_t smem_bytes(int kb) {
     return (size_t)kb * A_KBLK_BYTES + (size_t)AR_STAGES * I8_STAGE_BYTES + (size_t)CAP * SCAN_T * 4 +
            ROWS * 8 /*row_ctl*/ + ROWS * 4 /*row_best*/ + ROWS * 4 /*row_done*/ + SCAN_T /*hit_cnt*/ +
-           NWORK * WSCR + (2 * AR_STAGES + 4) * 8 /*barriers*/ + 16 /*tmem slot, stop tile, issue counter, rows left*/;
+           (2 * AR_STAGES + 4) * 8 /*barriers*/ + 16 /*tmem slot, stop tile, issue counter, rows left*/;
 }
 
 __device__ __forceinline__ uint2 ld_shared_volatile_v2(const uint2* p) {
@@ -129,8 +139,7 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
     int* row_best = reinterpret_cast<int*>(row_ctl + ROWS);                 // [ROWS] running minimum over both halves
     int* row_done = row_best + ROWS;                                        // [ROWS] halves that finished the cycle
     uint8_t* hit_cnt = reinterpret_cast<uint8_t*>(row_done + ROWS);         // [SCAN_T] entries recorded in the cycle
-    unsigned char* wscr = reinterpret_cast<unsigned char*>(hit_cnt + SCAN_T);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(wscr + NWORK * WSCR);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(hit_cnt + SCAN_T);
     uint64_t* full = bars;
     uint64_t* empty = bars + STAGES;
     uint64_t* tfull = bars + 2 * STAGES;
@@ -166,7 +175,11 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    if (warp == 0) {
+    // register budgets per warpgroup (the kernel starts with 96 per thread; an increase can only
+    // take what a decrease in the same CTA released: 4 x 32 x 56 >= 8 x 32 x 24)
+    if (warp < SCAN_W0) {
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
+      if (warp == 0) {
         // ===== producer: the P tiles, cyclically, until the stop tile
         if (lane == 0) {
             int stage = 0, j = 0;
@@ -183,7 +196,7 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
                 if (++j == ntiles) j = 0;
             }
         }
-    } else if (warp == 1) {
+      } else if (warp == 1) {
         // ===== MMA issuer: one M128 N256 tile per step, K = 32 per instruction
         if (lane == 0) {
             const uint32_t idesc = (2u << 4) | (1u << 7) | ((uint32_t)(I8_TILE >> 3) << 17) | ((uint32_t)(ROWS >> 4) << 24);
@@ -223,10 +236,11 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
                 atomicAdd(&prm.stats[ST_ISS_TOT], (unsigned long long)(clock64() - t_0));
             }
         }
-    } else if (warp < 2 + SCAN_T / 32) {
+      }
+    } else if (warp < WORK_W0) {
         // ===== scan: thread = (row, column half); no data-dependent branch per tile
         const int g = warp & 3;                      // TMEM lane quarter of this warp
-        const int half = (warp - 2) >> 2;
+        const int half = (warp - SCAN_W0) >> 2;
         const int row = g * 32 + lane;
         const int thr = half * ROWS + row;
         const int col0 = half * (I8_TILE / 2);
@@ -317,10 +331,10 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
             }
         }
     } else {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 120;");
         // ===== workers: worker w owns rows lane * NWORK + w; the row state lives in
         // the registers of the lane that owns the row and is broadcast by shuffles
-        const int w = warp - (2 + SCAN_T / 32);
-        uint16_t* chl = reinterpret_cast<uint16_t*>(wscr + w * WSCR);       // hit chunks of the row [2 CAP]
+        const int w = warp - WORK_W0;
         const int myrow = lane * NWORK + w;
         int tr = -1, frame = 0, iters = 0, wq = 0;
         uint32_t flags = 0;
@@ -328,7 +342,7 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
         uint32_t c[NW];
 #pragma unroll
         for (int k = 0; k < NW; k++) c[k] = 0u;
-        bool fresh = true, exhausted = false, recyc = false;
+        bool fresh = lane < ROWS / NWORK, exhausted = false, recyc = false;   // lanes beyond the partition own no row
         const int count = *prm.s2.count;
         const int ntraj = count * A;
         // the worker's pocket: the next trajectory of the stage-2 queue, claimed ahead of
@@ -365,7 +379,7 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
 #define PH(k) if (STATS) { const long long t_ = clock64(); ph[k] += t_ - t_ph; t_ph = t_; }
         for (;;) {
             if (ld_shared_volatile_u32(stop_tile) != 0xFFFFFFFFu) break;
-            const int d = fresh ? 2 : (exhausted ? 0 : ld_shared_volatile(&row_done[myrow]));
+            const int d = fresh ? 2 : ((exhausted || lane >= ROWS / NWORK) ? 0 : ld_shared_volatile(&row_done[myrow]));
             const unsigned ready = __ballot_sync(MPW_FULL, d == 2);
             if (!ready) { __nanosleep(64); continue; }
             long long t_busy0 = 0;
@@ -390,18 +404,27 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
                 // the frame's y (this lane's 8 positions) is on its way while the hit lists are read
                 const float* yr = prm.y + (size_t)frame_ * n;
                 float4 ya = make_float4(0.f, 0.f, 0.f, 0.f), yb = ya;
-                if (lane * 8 < n) {
+                const bool pos_on = lane * 8 < n;      // this lane holds positions 8 lane .. 8 lane + 7
+                if (pos_on) {
                     const float4* y4 = reinterpret_cast<const float4*>(yr) + lane * 2;
                     ya = __ldg(y4);
                     yb = __ldg(y4 + 1);
                 }
                 __threadfence_block();
+                // everything the decision reads from shared memory, issued together: the final
+                // minimum, both halves' entry counts and entries, this lane's 8 int8 values
+                uint2* const qptr = reinterpret_cast<uint2*>(a_rows + (lane >> 4) * A_KBLK_BYTES +
+                                                             sw128_chunk(row, (lane & 15) >> 1) + (lane & 1) * 8);
                 const int mfin = ld_shared_volatile(&row_best[row]);
                 const int cnt0 = hit_cnt[row], cnt1 = hit_cnt[ROWS + row];
+                const int hl = lane < CAP ? lane : 0;
+                const uint32_t ent0 = hits[hl * SCAN_T + row], ent1 = hits[hl * SCAN_T + ROWS + row];
+                uint2 q2 = make_uint2(0u, 0u);
+                if (pos_on) q2 = *qptr;
                 const bool ovf = cnt0 > CAP || cnt1 > CAP;
                 if (STATS) st_rowcyc++;
                 if (ovf && !recyc_) {
-                    // hit list overflow: scan once more, recording only the chunks inside
+                    // hit list overflow: scan once more, recording only the groups inside
                     // the window of the achieved minimum
                     if (STATS) st_ovf++;
                     recyc_ = true;
@@ -409,111 +432,119 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
                 } else {
                     if (ovf) flags_ |= MPW_F_UNRESOLVED;
                     recyc_ = false;
-                    // the row's hit groups (32 patterns): entries of both halves inside the window of the final minimum
                     const int limit = mfin + wq_;
-                    int nh = 0;
-#pragma unroll
-                    for (int hf = 0; hf < 2; hf++) {
-                        const int cnt = min(hf ? cnt1 : cnt0, CAP);
-                        const uint32_t ent = lane < cnt ? hits[lane * SCAN_T + hf * ROWS + row] : 0xFFFFFFFFu;
-                        const bool ok = lane < cnt && (int)(ent >> 16) - KEY_BIAS < limit;
-                        const unsigned m = __ballot_sync(MPW_FULL, ok);
-                        if (ok) chl[nh + __popc(m & ((1u << lane) - 1u))] = (uint16_t)(ent & 0xFFFFu);
-                        nh += __popc(m);
-                    }
-                    __syncwarp();
                     PH(0);
-                    const double bnd = (double)ay_ * (double)prm.cert_g;   // |fl(S) - S| of the fp32 sums
+                    // |fl(S) - S| of the fp32 sums (rounded up), the tie threshold, and the margin
+                    // inside which two fp32 scores are not told apart
+                    const float bnd = ay_ * prm.cert_g * 1.000001f;
                     const float thr = prm.tie_rel * ed_ * 0.25f;
-                    const double Md = 2.0 * bnd + (double)thr;
+                    const float Mf = (2.0f * bnd + thr) * 1.000001f;
+                    // t = x ⊙ y of this lane's positions
+                    float tv[8];
+                    const uint32_t cw8 = select_word<NW>(c_, (lane >> 2) & (NW - 1)) >> ((lane & 3) * 8);
                     float Bs = CUDART_INF_F;
                     int Bi = 0x7FFFFFFF, nf = 0;
                     float fs = CUDART_INF_F;   // finalist `lane`: fp32 score, pattern
                     int fi = 0x7FFFFFFF;
-                    uint32_t pw = 0u;      // lanes < NW: word `lane` of the running best pattern
-                    // per hit group (32 patterns, one per lane): the exact integer score Q_p
-                    // by DP4A of the row's int8 image (broadcast from shared memory) with the
-                    // pattern's bits expanded to 0/1 bytes; the patterns inside the window of
-                    // the final minimum are then scored from y in fp32, the warp summing one
-                    // pattern at a time (8 positions per lane, butterfly sum)
-                    auto load_bits = [&](int grp, uint32_t (&bw)[NW]) {
-                        const int p = grp * 32 + lane;
-#pragma unroll
-                        for (int k = 0; k < NW; k++) bw[k] = 0u;
-                        if (p < np_) {
-                            const uint4* s4 = reinterpret_cast<const uint4*>(prm.pbits + (size_t)p * NW);
-#pragma unroll
-                            for (int k = 0; k < NW / 4; k++) {
-                                const uint4 v = __ldg(s4 + k);
-                                bw[4 * k] = v.x; bw[4 * k + 1] = v.y; bw[4 * k + 2] = v.z; bw[4 * k + 3] = v.w;
-                            }
+                    bool tv_ready = false;
+                    // Per hit group (32 patterns): lane L holds byte L (positions 8 L .. 8 L + 7)
+                    // of all 32 patterns (transposed bits, one 32-byte load per lane) and the
+                    // row's int8 values of the same positions; the exact integer score Q_j of
+                    // pattern j is the warp sum (REDUX) of two DP4As per lane.  The patterns
+                    // inside the window of the final minimum are then scored from y in fp32 with
+                    // the same bytes (8 positions per lane, butterfly sum).
+                    auto load_group = [&](int grp, uint4& t0, uint4& t1) {
+                        t0 = make_uint4(0u, 0u, 0u, 0u);
+                        t1 = t0;
+                        if (pos_on) {
+                            const uint4* s4 = prm.pbT + ((size_t)grp * (NW * 4) + lane) * 2;
+                            t0 = __ldg(s4);
+                            t1 = __ldg(s4 + 1);
                         }
                     };
-                    uint32_t bwn[NW];
-                    if (nh > 0) load_bits((int)chl[0], bwn);
-#pragma unroll 1
-                    for (int ih = 0; ih < nh; ih++) {
-                        const int grp = (int)chl[ih];
-                        uint32_t bw[NW];
+                    auto do_group = [&](int grp, const uint4& t0, const uint4& t1) {
+                        const uint32_t tb[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
+                        // this lane's share of Q_j for the 32 patterns: a nibble's bits -> 0/1 bytes by
+                        // one multiplication (bit k lands on bits k, k + 7, k + 14, k + 21; the four
+                        // copies of a nibble do not overlap, those of a whole byte would)
+                        int v[32];
 #pragma unroll
-                        for (int k = 0; k < NW; k++) bw[k] = bwn[k];
-                        if (ih + 1 < nh) load_bits((int)chl[ih + 1], bwn);   // in flight during this group
-                        int Q0 = 0, Q1 = 0;
-#pragma unroll
-                        for (int cc = 0; cc < NW * 2; cc++) {
-                            const uint4 qv = *reinterpret_cast<const uint4*>(a_rows + (cc >> 3) * A_KBLK_BYTES +
-                                                                             sw128_chunk(row, cc & 7));
-                            const uint32_t b16 = bw[cc >> 1] >> (16 * (cc & 1));
-                            auto ex = [](uint32_t nib) { return (int)(((nib & 0xFu) * 0x00204081u) & 0x01010101u); };
-                            Q0 = __dp4a((int)qv.x, ex(b16), Q0);
-                            Q1 = __dp4a((int)qv.y, ex(b16 >> 4), Q1);
-                            Q0 = __dp4a((int)qv.z, ex(b16 >> 8), Q0);
-                            Q1 = __dp4a((int)qv.w, ex(b16 >> 12), Q1);
+                        for (int j = 0; j < 32; j++) {
+                            const uint32_t byte = (tb[j >> 2] >> (8 * (j & 3))) & 0xFFu;
+                            const uint32_t lo = ((byte & 0xFu) * 0x00204081u) & 0x01010101u;
+                            const uint32_t hi = ((byte >> 4) * 0x00204081u) & 0x01010101u;
+                            v[j] = __dp4a((int)q2.y, (int)hi, __dp4a((int)q2.x, (int)lo, 0));
                         }
-                        unsigned cm = __ballot_sync(MPW_FULL, grp * 32 + lane < np_ && Q0 + Q1 < limit);
-                        if (STATS) st_chunks++;
-                        while (cm) {
-                            const int src_l = __ffs(cm) - 1;
-                            cm &= cm - 1;
-                            const int pc = grp * 32 + src_l;
-                            // the candidate's bits from the lane that holds them
-                            uint32_t myw = 0u, pwc = 0u;
+                        // transposing butterfly: after the five steps lane j holds the warp sum of v[j]
 #pragma unroll
-                            for (int k = 0; k < NW; k++) {
-                                const uint32_t x = __shfl_sync(MPW_FULL, bw[k], src_l);
-                                if (k == (lane >> 2)) myw = x;
-                                if (k == lane) pwc = x;
+                        for (int o = 16; o > 0; o >>= 1) {
+                            const bool up = (lane & o) != 0;
+#pragma unroll
+                            for (int i = 0; i < o; i++) {
+                                const int send = up ? v[i] : v[i + o];
+                                const int keep = up ? v[i + o] : v[i];
+                                v[i] = keep + __shfl_xor_sync(MPW_FULL, send, o);
                             }
-                            const uint32_t byte = (myw >> ((lane & 3) * 8)) & 0xFFu;
-                            const uint32_t cw = select_word<NW>(c_, (lane >> 2) & (NW - 1)) >> ((lane & 3) * 8);
+                        }
+                        const int Q = v[0];
+                        unsigned cm = __ballot_sync(MPW_FULL, grp * 32 + lane < np_ && Q < limit);
+                        if (STATS) st_chunks++;
+                        if (cm && !tv_ready) {
                             const float yv[8] = {ya.x, ya.y, ya.z, ya.w, yb.x, yb.y, yb.z, yb.w};
+#pragma unroll
+                            for (int k = 0; k < 8; k++)
+                                tv[k] = __uint_as_float(__float_as_uint(yv[k]) ^ (((cw8 >> k) & 1u) << 31));
+                            tv_ready = true;
+                        }
+                        while (cm) {
+                            const int j = __ffs(cm) - 1;
+                            cm &= cm - 1;
+                            const int pc = grp * 32 + j;
+                            const uint32_t byte = (select_word<8>(tb, j >> 2) >> (8 * (j & 3))) & 0xFFu;
                             float sp = 0.f;
 #pragma unroll
                             for (int k = 0; k < 8; k++)
-                                if ((byte >> k) & 1u) sp += __uint_as_float(__float_as_uint(yv[k]) ^ (((cw >> k) & 1u) << 31));
+                                if ((byte >> k) & 1u) sp += tv[k];
 #pragma unroll
                             for (int o = 16; o > 0; o >>= 1) sp += __shfl_xor_sync(MPW_FULL, sp, o);
-                            if (sp < Bs || (sp == Bs && pc < Bi)) { Bs = sp; Bi = pc; pw = pwc; }
+                            if (sp < Bs || (sp == Bs && pc < Bi)) { Bs = sp; Bi = pc; }
                             // finalists: everything within the certification margin of the running best
-                            if ((double)sp < (double)Bs + Md) {
+                            // (the difference of two close floats is exact)
+                            if (sp - Bs < Mf) {
                                 if (lane == nf) { fs = sp; fi = pc; }
                                 nf++;
                             }
                         }
+                    };
+#pragma unroll 1
+                    for (int hf = 0; hf < 2; hf++) {
+                        const int cnt = min(hf ? cnt1 : cnt0, CAP);
+                        const uint32_t ent = hf ? ent1 : ent0;
+                        unsigned m = __ballot_sync(MPW_FULL, lane < cnt && (int)(ent >> 16) - KEY_BIAS < limit);
+                        uint4 n0, n1;
+                        if (m) load_group((int)(__shfl_sync(MPW_FULL, ent, __ffs(m) - 1) & 0xFFFFu), n0, n1);
+                        while (m) {
+                            const int grp = (int)(__shfl_sync(MPW_FULL, ent, __ffs(m) - 1) & 0xFFFFu);
+                            m &= m - 1;
+                            const uint4 t0 = n0, t1 = n1;
+                            // the next group's bytes are in flight during this group
+                            if (m) load_group((int)(__shfl_sync(MPW_FULL, ent, __ffs(m) - 1) & 0xFFFFu), n0, n1);
+                            do_group(grp, t0, t1);
+                        }
                     }
                     PH(1);
                     if (nf > 32) flags_ |= MPW_F_UNRESOLVED;   // more near-equal scores than lanes
-                    const bool keep = (double)fs < (double)Bs + Md;
+                    const bool keep = fs - Bs < Mf;
                     const int nk = __popc(__ballot_sync(MPW_FULL, keep));
                     int best = Bi;
                     bool improve = false;
                     float sb = 0.f;
-                    const double aB = fabs((double)Bs);
-                    if (nk == 1 && aB > bnd && fabs(aB - (double)thr) > bnd) {
+                    const float aB = fabsf(Bs);
+                    if (nk == 1 && aB > bnd && fabsf(aB - thr) > bnd * 1.000001f) {
                         // the fp32 decision is the exact one
                         improve = Bs < 0.f;
                         sb = Bs;
-                        if (aB < (double)thr) flags_ |= MPW_F_TIE_ACCEPT;
+                        if (aB < thr) flags_ |= MPW_F_TIE_ACCEPT;
                     } else if (nk >= 1) {
                         // float64 scores of the finalists (ascending positions), one per lane
                         if (STATS) st_f64++;
@@ -539,20 +570,17 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
                     iters_++;
                     if (improve) {
                         // the move: c ^= p, the moved positions' int8 values negated
-                        if (best != Bi) pw = lane < NW ? __ldg(prm.pbits + (size_t)best * NW + lane) : 0u;
+                        const uint32_t pw = lane < NW ? __ldg(prm.pbits + (size_t)best * NW + lane) : 0u;
 #pragma unroll
                         for (int k = 0; k < NW; k++) c_[k] ^= __shfl_sync(MPW_FULL, pw, k);
                         const uint32_t word = __shfl_sync(MPW_FULL, pw, (lane >> 2) & (NW - 1));
                         const uint32_t b8 = (word >> ((lane & 3) * 8)) & 0xFFu;
-                        if (b8 && lane * 8 < n) {
-                            uint2* pq = reinterpret_cast<uint2*>(a_rows + (lane >> 4) * A_KBLK_BYTES +
-                                                                 sw128_chunk(row, (lane & 15) >> 1) + (lane & 1) * 8);
-                            uint2 v = *pq;
+                        if (b8 && pos_on) {
                             uint32_t m = byte_mask4(b8 & 0xFu);
-                            v.x = (v.x & ~m) | (__vsub4(0u, v.x) & m);
+                            q2.x = (q2.x & ~m) | (__vsub4(0u, q2.x) & m);
                             m = byte_mask4(b8 >> 4);
-                            v.y = (v.y & ~m) | (__vsub4(0u, v.y) & m);
-                            *pq = v;
+                            q2.y = (q2.y & ~m) | (__vsub4(0u, q2.y) & m);
+                            *qptr = q2;
                         }
                         ed_ += 4.f * sb;
                         if (prm.s2.traj_hops && lane == 0) prm.s2.traj_hops[(size_t)tr_ * T + iters_ - 1] = best + 1;

@@ -14,6 +14,8 @@ struct TcPatterns {
     bool ready8 = false;
     uint8_t* tiles8 = nullptr;
     int kb8 = 0, ntiles8 = 0;   // int8 tiles are tc::I8_TILE patterns wide
+    // asynchronous-row hop, worker view of P: bits transposed [group of 32 patterns][n / 8 position bytes][32 patterns]
+    uint4* pbT = nullptr;
 };
 
 // Launch options of the tensor hop (per handle, mpw_set_option)

@@ -19,18 +19,28 @@ bool ar_supported(const TcPatterns& t, int n) {
 
 template <int KB, int NW, bool STATS>
 static int ar_launch_t(const TcPatterns& t, int n, int A, int T, const float* y, S2Dev s2, PatDev P, int num_sms,
-                       cudaStream_t st) {
+                       int experiment, int hit_cap, cudaStream_t st) {
     ar::Params prm;
     prm.n = n; prm.nw = NW; prm.A = A; prm.T = T; prm.np = t.np; prm.ntiles = t.ntiles8;
     prm.y = y; prm.s2 = s2; prm.pbits = P.bits; prm.pbT = t.pbT; prm.btiles = t.tiles8;
     prm.tie_rel = 1e-5f;
+    prm.cap = hit_cap > 0 && hit_cap < ar::CAP ? hit_cap : ar::CAP;
     prm.cert_g = ar_cert_gamma(s2.wmax);
     prm.stats = nullptr;
+    prm.experiment = 0;
+    prm.tilestat = nullptr;
+    static unsigned long long* tilestat = nullptr;
+    if (experiment == 32) {   // light statistic of the production kernel: cycles per tile
+        if (!tilestat && cudaMallocManaged(&tilestat, 2 * sizeof(unsigned long long)) != cudaSuccess) return -1;
+        tilestat[0] = tilestat[1] = 0;
+        prm.tilestat = tilestat;
+    }
     static unsigned long long* stats = nullptr;
     if (STATS) {
         if (!stats && cudaMallocManaged(&stats, sizeof(unsigned long long) * ar::ST_N) != cudaSuccess) return -1;
         memset(stats, 0, sizeof(unsigned long long) * ar::ST_N);
         prm.stats = stats;
+        prm.experiment = experiment;
     }
     const size_t smem = ar::smem_bytes(KB);
     auto kern = ar::hop_ar_kernel<KB, NW, STATS>;
@@ -39,6 +49,11 @@ static int ar_launch_t(const TcPatterns& t, int n, int A, int T, const float* y,
     kern<<<num_sms, ar::THREADS, smem, st>>>(prm);
     e = cudaGetLastError();
     if (e != cudaSuccess) return -(int)e;
+    if (prm.tilestat) {
+        cudaStreamSynchronize(st);
+        fprintf(stderr, "[hop_ar] production kernel: %.0f tiles per CTA, %.1f cycles per tile\n", (double)tilestat[0] / num_sms,
+                tilestat[0] ? (double)tilestat[1] / (double)tilestat[0] : 0.0);
+    }
     if (STATS) {
         cudaStreamSynchronize(st);
         const unsigned long long* s = stats;
@@ -51,11 +66,12 @@ static int ar_launch_t(const TcPatterns& t, int n, int A, int T, const float* y,
                 s[ar::ST_ROWCYC] ? (double)s[ar::ST_ENTRIES] / (2.0 * (double)s[ar::ST_ROWCYC]) : 0.0, s[ar::ST_F64],
                 s[ar::ST_OVF], s[ar::ST_ROWCYC] ? (double)s[ar::ST_BUSY] / (double)s[ar::ST_ROWCYC] : 0.0);
         fprintf(stderr,
-                "[hop_ar] cycles per tile %.0f; issuer waits: B stage %.3f, accumulator %.3f of its time; scan warps wait "
+                "[hop_ar] cycles per tile %.0f; issuer: B stage wait %.3f, accumulator wait %.3f, MMA issue + commit %.3f of its time; scan warps wait "
                 "for the accumulator %.3f of their time\n",
-                tiles > 0 ? (double)s[ar::ST_ISS_TOT] / tiles : 0.0,
+                tiles > 0 ? (double)s[ar::ST_ISS_TOT] / tiles : 0.0,   // issuer 0's clock over all tiles
                 s[ar::ST_ISS_TOT] ? (double)s[ar::ST_ISS_FULL] / (double)s[ar::ST_ISS_TOT] : 0.0,
                 s[ar::ST_ISS_TOT] ? (double)s[ar::ST_ISS_TEMPTY] / (double)s[ar::ST_ISS_TOT] : 0.0,
+                s[ar::ST_ISS_TOT] ? (double)s[ar::ST_ISS_MMA] / (double)s[ar::ST_ISS_TOT] : 0.0,
                 s[ar::ST_SCAN_TOT] ? (double)s[ar::ST_SCAN_WAIT] / (double)s[ar::ST_SCAN_TOT] : 0.0);
         const double rc = s[ar::ST_ROWCYC] ? (double)s[ar::ST_ROWCYC] : 1.0;
         fprintf(stderr,
@@ -70,10 +86,10 @@ static int ar_launch_t(const TcPatterns& t, int n, int A, int T, const float* y,
 int ar_launch(const TcPatterns& t, int n, int nw, int A, int T, const float* y, S2Dev s2, PatDev P, int num_sms,
               const TcOpts& o, cudaStream_t st) {
     if (!ar_supported(t, n) || nw != n / 32) return 1;
-    const bool stats = o.experiment != 0;
+    const bool stats = o.experiment != 0 && o.experiment != 32;
     if (n == 256)
-        return stats ? ar_launch_t<2, 8, true>(t, n, A, T, y, s2, P, num_sms, st)
-                     : ar_launch_t<2, 8, false>(t, n, A, T, y, s2, P, num_sms, st);
-    return stats ? ar_launch_t<1, 4, true>(t, n, A, T, y, s2, P, num_sms, st)
-                 : ar_launch_t<1, 4, false>(t, n, A, T, y, s2, P, num_sms, st);
+        return stats ? ar_launch_t<2, 8, true>(t, n, A, T, y, s2, P, num_sms, o.experiment, o.ar_hit_cap, st)
+                     : ar_launch_t<2, 8, false>(t, n, A, T, y, s2, P, num_sms, o.experiment, o.ar_hit_cap, st);
+    return stats ? ar_launch_t<1, 4, true>(t, n, A, T, y, s2, P, num_sms, o.experiment, o.ar_hit_cap, st)
+                 : ar_launch_t<1, 4, false>(t, n, A, T, y, s2, P, num_sms, o.experiment, o.ar_hit_cap, st);
 }

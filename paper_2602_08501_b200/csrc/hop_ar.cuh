@@ -57,6 +57,11 @@ static_assert(NWORK % 4 == 0, "worker warps in whole warpgroups");
 constexpr int CAP = 30;                        // hit-list entries per scan thread and cycle
 constexpr int AR_STAGES = 5;                   // P ring stages (one 128-position K-block of a tile each)
 constexpr int Q_INF = 0x7FFF;                  // s16 maximum: "no score"
+#ifndef MPW_AR_NISS
+#define MPW_AR_NISS 2
+#endif
+constexpr int NISS = MPW_AR_NISS;             // MMA issuer threads (alternate tiles)
+static_assert(NISS == 1 || NISS == 2, "one issuer per accumulator");
 constexpr int MARGIN = 2;                      // tiles between the issue counter read and a row's first live tile
 static_assert(CAP <= 32, "one hit entry per worker lane");
 // a hit entry names a group of 32 patterns in 16 bits: |P| <= 2^17 gives 4096 groups
@@ -69,8 +74,13 @@ struct Params {
     const uint4* pbT;            // bits transposed for the workers: [group of 32 patterns][n / 8 position bytes][32 patterns]
     const uint8_t* btiles;       // [ntiles][KB][256 x 128 u8] swizzled images
     float tie_rel;
+    int cap;                     // hit-list entries per scan thread and cycle in use (<= CAP)
     float cert_g;                // fp32 summation bound factor (cert_gamma)
     unsigned long long* stats;   // STATS builds: counters (see hop_ar.cu)
+    unsigned long long* tilestat;   // optional (any build): [0] += tiles, [1] += clock64 cycles of issuer 0, per CTA
+    int experiment;              // STATS builds, timing probes (results wrong): 2 workers decide "no move" without
+                                 // scoring, 4 the producer stops copying once the ring is full, 8 scan skips the TMEM loads,
+                                 // 16 workers skip the proxy fence
 };
 
 __host__ __device__ constexpr size_t smem_bytes(int kb) {
@@ -94,6 +104,18 @@ __device__ __forceinline__ uint32_t ld_shared_volatile_u32(const volatile uint32
 }
 __device__ __forceinline__ void st_shared_volatile_u32(volatile uint32_t* p, uint32_t v) {
     asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"(smem_u32(const_cast<uint32_t*>(p))), "r"(v) : "memory");
+}
+
+// predicated shared-memory store / minimum / trap: one predicated instruction each, no branch
+// (the compiler turns the equivalent `if` into a divergent branch with a reconvergence barrier)
+__device__ __forceinline__ void st_shared_if(uint32_t addr, uint32_t v, bool p) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.shared.u32 [%0], %1;\n\t}" ::"r"(addr), "r"(v), "r"((uint32_t)p) : "memory");
+}
+__device__ __forceinline__ void red_min_shared_if(uint32_t addr, int v, bool p) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q red.shared.min.s32 [%0], %1;\n\t}" ::"r"(addr), "r"(v), "r"((uint32_t)p) : "memory");
+}
+__device__ __forceinline__ void trap_if(bool p) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %0, 0;\n\t@q trap;\n\t}" ::"r"((uint32_t)p));
 }
 
 // minimum of 32 packed s16 values (registers o .. o + 15): 8 three-input instructions
@@ -121,10 +143,23 @@ __device__ __forceinline__ int min64_s16_only(const uint32_t (&v)[32]) {
     return min((int)(short)(f & 0xFFFFu), (int)(short)(f >> 16));
 }
 
+// barrier waits of the producer and the issuer: 1 = spin on try_wait, 0 = try_wait with a
+// suspend-time hint (the thread sleeps until the phase completes)
+#ifndef MPW_AR_SPIN
+#define MPW_AR_SPIN 1
+#endif
+__device__ __forceinline__ void ar_wait(uint32_t bar, uint32_t parity) {
+#if MPW_AR_SPIN
+    mbar_wait(bar, parity);
+#else
+    while (!mbar_try_hint(bar, parity)) {}
+#endif
+}
+
 // stats slots
 enum { ST_TILES = 0, ST_LIVE, ST_ROWCYC, ST_CHUNKS, ST_F64, ST_OVF, ST_BUSY, ST_FINISHED, ST_ENTRIES,
        ST_SCAN_WAIT, ST_SCAN_TOT, ST_ISS_FULL, ST_ISS_TEMPTY, ST_ISS_TOT, ST_W_LIST, ST_W_CHUNK, ST_W_DECIDE, ST_W_CLAIM,
-       ST_W_PUBLISH, ST_W_POCKET, ST_N };
+       ST_W_PUBLISH, ST_W_POCKET, ST_ISS_MMA, ST_N };
 
 template <int KB, int NW, bool STATS>
 __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
@@ -187,52 +222,70 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
             for (uint32_t gt = 0;; gt++) {
                 if (gt >= ld_shared_volatile_u32(stop_tile)) break;
                 for (int kb = 0; kb < KB; kb++) {
-                    mbar_wait_issuer(smem_u32(&empty[stage]), phase ^ 1);
+                    ar_wait(smem_u32(&empty[stage]), phase ^ 1);
                     const uint32_t fb = smem_u32(&full[stage]);
-                    mbar_expect_tx(fb, STB);
-                    bulk_g2s(smem_u32(b_ring + stage * STB), prm.btiles + ((size_t)j * KB + kb) * STB, STB, fb);
+                    if (STATS && (prm.experiment & 4) && gt >= 4) {
+                        mbar_arrive(fb);   // timing probe: no P traffic
+                    } else {
+                        mbar_expect_tx(fb, STB);
+                        bulk_g2s(smem_u32(b_ring + stage * STB), prm.btiles + ((size_t)j * KB + kb) * STB, STB, fb);
+                    }
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
                 if (++j == ntiles) j = 0;
             }
         }
-      } else if (warp == 1) {
-        // ===== MMA issuer: one M128 N256 tile per step, K = 32 per instruction
+      } else if (warp == 1 || (NISS == 2 && warp == 2)) {
+        // ===== MMA issuers: one M128 N256 tile per step, K = 32 per instruction.  Two
+        // threads (warps 1 and 2) take alternate tiles, each with its own accumulator:
+        // while one runs through the barrier checks of its next tile, the other's MMAs keep
+        // the tensor pipe fed (one thread alone leaves the pipe idle ~20 % of the time: its
+        // per-tile waits, fences and commits outlast the few MMAs the pipe can queue)
         if (lane == 0) {
+            const uint32_t which = (uint32_t)(warp - 1);
             const uint32_t idesc = (2u << 4) | (1u << 7) | ((uint32_t)(I8_TILE >> 3) << 17) | ((uint32_t)(ROWS >> 4) << 24);
             const uint32_t abase = smem_u32(a_rows), bring = smem_u32(b_ring);
-            int stage = 0;
-            uint32_t phase = 0;
-            long long w_full = 0, w_tempty = 0, t_0 = 0, t_a = 0;
-            if (STATS) t_0 = clock64();
-            for (uint32_t gt = 0;; gt++) {
+            const uint32_t ictr = smem_u32(const_cast<uint32_t*>(issue_ctr));
+            long long w_full = 0, w_tempty = 0, w_mma = 0, t_0 = 0, t_a = 0;
+            if (STATS || prm.tilestat) t_0 = clock64();
+            uint32_t gt_end = 0;
+            for (uint32_t gt = which;; gt += NISS) {
+                gt_end = gt;
                 if (gt >= ld_shared_volatile_u32(stop_tile)) break;
                 const uint32_t buf = gt & 1u;
                 if (STATS) t_a = clock64();
-                mbar_wait_issuer(smem_u32(&tempty[buf]), ((gt >> 1) & 1u) ^ 1u);
+                ar_wait(smem_u32(&tempty[buf]), ((gt >> 1) & 1u) ^ 1u);
                 if (STATS) w_tempty += clock64() - t_a;
                 tc_fence_after();
-                // published before the tile's MMAs are issued: a worker that reads v knows
-                // that no MMA of tile v + 1 has been issued yet
-                st_shared_volatile_u32(issue_ctr, gt);
+                // published (as a running maximum) before the tile's MMAs are issued: a
+                // worker that reads v knows that no MMA of a tile beyond v has been issued yet
+                asm volatile("red.shared.max.u32 [%0], %1;" ::"r"(ictr), "r"(gt) : "memory");
                 const uint32_t d = tmem_base + buf * I8_TILE;
                 for (int kb = 0; kb < KB; kb++) {
+                    const uint32_t u = gt * KB + kb;           // K-block number -> ring stage and phase
+                    const uint32_t stage = u % STAGES, phase = (u / STAGES) & 1u;
                     if (STATS) t_a = clock64();
-                    mbar_wait_issuer(smem_u32(&full[stage]), phase);
+                    ar_wait(smem_u32(&full[stage]), phase);
                     if (STATS) w_full += clock64() - t_a;
                     tc_fence_after();
                     const uint64_t bd = sw128_desc(bring + stage * STB);
                     const uint64_t ad = sw128_desc(abase + kb * A_KBLK_BYTES);
+                    if (STATS) t_a = clock64();
 #pragma unroll
                     for (int ks = 0; ks < 4; ks++) tc_mma_i8(d, ad + 2 * ks, bd + 2 * ks, idesc, (kb | ks) != 0);
                     tc_commit(smem_u32(&empty[stage]));
-                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                    if (STATS) w_mma += clock64() - t_a;
                 }
                 tc_commit(smem_u32(&tfull[buf]));
             }
-            if (STATS) {
+            if (prm.tilestat && which == 0) {
+                atomicAdd(&prm.tilestat[0], (unsigned long long)gt_end);
+                atomicAdd(&prm.tilestat[1], (unsigned long long)(clock64() - t_0));
+            }
+            if (STATS && which == 0) {
                 atomicAdd(&prm.stats[ST_ISS_FULL], (unsigned long long)w_full);
                 atomicAdd(&prm.stats[ST_ISS_TEMPTY], (unsigned long long)w_tempty);
+                atomicAdd(&prm.stats[ST_ISS_MMA], (unsigned long long)w_mma);
                 atomicAdd(&prm.stats[ST_ISS_TOT], (unsigned long long)(clock64() - t_0));
             }
         }
@@ -246,7 +299,9 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
         const int col0 = half * (I8_TILE / 2);
         const uint32_t t_lane = tmem_base + ((uint32_t)(g * 32) << 16);
         const bool ragged = (np_ % I8_TILE) != 0;
+        const int cap = prm.cap;
         uint32_t seen = 0x80000000u;                 // start tile of the cycle this thread knows
+        const uint32_t hits_addr = smem_u32(hits) + (uint32_t)thr * 4u, best_addr = smem_u32(&row_best[row]);
         int cnt = 0, m_run = Q_INF, pub = 0x7FFFFFFF, wq = 0;
         int j = 0;
         unsigned long long st_live = 0, st_tiles = 0, st_entries = 0;
@@ -261,8 +316,13 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
             tc_fence_after();
             uint32_t va[32], vb[32];
             const uint32_t tbase = t_lane + buf * I8_TILE + col0;
-            TC_LD32P(tbase, va);
-            TC_LD32P(tbase + 64, vb);
+            if (STATS && (prm.experiment & 8)) {
+#pragma unroll
+                for (int e = 0; e < 32; e++) { va[e] = 0x00010001u * (uint32_t)(e + lane); vb[e] = va[e]; }
+            } else {
+                TC_LD32P(tbase, va);
+                TC_LD32P(tbase + 64, vb);
+            }
             // the row's control word, then the other half's published minimum (in this
             // order: a new control word implies the reset of the minimum is visible)
             const uint2 ctl = ld_shared_volatile_v2(&row_ctl[row]);
@@ -288,29 +348,30 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
             const int m0 = min32_s16(va, 0), m1 = min32_s16(va, 16), m2 = min32_s16(vb, 0), m3 = min32_s16(vb, 16);
             const bool isnew = ctl.x != seen;
             seen = ctl.x;
-            if (isnew) {
-                cnt = 0;
-                m_run = (int)(ctl.y & 0xFFFFu) - KEY_BIAS;
-                pub = 0x7FFFFFFF;
-                wq = (int)(ctl.y >> 16);
-                if (gt > ctl.x) __trap();   // the start tile was observed late: protocol violation, fail the launch
-            }
+            // a new cycle: counters reset, the running minimum starts from the seed
+            cnt = isnew ? 0 : cnt;
+            m_run = isnew ? (int)(ctl.y & 0xFFFFu) - KEY_BIAS : m_run;
+            pub = isnew ? 0x7FFFFFFF : pub;
+            wq = isnew ? (int)(ctl.y >> 16) : wq;
+            trap_if(isnew && gt > ctl.x);   // the start tile was observed late: protocol violation, fail the launch
             const uint32_t age = gt - seen;
             const bool live = age < (uint32_t)ntiles;
             const int mt = min(min(m0, m1), min(m2, m3));
-            if (live) m_run = min(m_run, min(mt, shb));
+            m_run = live ? min(m_run, min(mt, shb)) : m_run;
             const int lim = m_run + wq;
             const uint32_t grp0 = (uint32_t)pa >> 5;
             auto record = [&](int m, uint32_t grp) {
-                const bool h = live && m < lim;
-                if (h && cnt < CAP) hits[cnt * SCAN_T + thr] = ((uint32_t)(m + KEY_BIAS) << 16) | grp;
+                const bool h = live && m < lim && !(STATS && (prm.experiment & 8));
+                st_shared_if(hits_addr + (uint32_t)cnt * (SCAN_T * 4), ((uint32_t)(m + KEY_BIAS) << 16) | grp, h && cnt < cap);
                 cnt += h ? 1 : 0;
             };
             record(m0, grp0);
             record(m1, grp0 + 1u);
             record(m2, grp0 + 2u);
             record(m3, grp0 + 3u);
-            if (live && mt < pub) { atomicMin(&row_best[row], mt); pub = mt; }
+            const bool lower = live && mt < pub;
+            red_min_shared_if(best_addr, mt, lower);
+            pub = lower ? mt : pub;
             if (STATS) { st_tiles++; st_live += live ? 1 : 0; }
             if (live && age == (uint32_t)(ntiles - 1)) {
                 // cycle end: hand the hit list to the row's worker
@@ -381,7 +442,7 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
             if (ld_shared_volatile_u32(stop_tile) != 0xFFFFFFFFu) break;
             const int d = fresh ? 2 : ((exhausted || lane >= ROWS / NWORK) ? 0 : ld_shared_volatile(&row_done[myrow]));
             const unsigned ready = __ballot_sync(MPW_FULL, d == 2);
-            if (!ready) { __nanosleep(64); continue; }
+            if (!ready) { __nanosleep(200); continue; }
             long long t_busy0 = 0;
             if (STATS) { t_busy0 = clock64(); t_ph = t_busy0; }
             const int L = __ffs(ready) - 1;
@@ -421,7 +482,7 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
                 const uint32_t ent0 = hits[hl * SCAN_T + row], ent1 = hits[hl * SCAN_T + ROWS + row];
                 uint2 q2 = make_uint2(0u, 0u);
                 if (pos_on) q2 = *qptr;
-                const bool ovf = cnt0 > CAP || cnt1 > CAP;
+                const bool ovf = cnt0 > prm.cap || cnt1 > prm.cap;
                 if (STATS) st_rowcyc++;
                 if (ovf && !recyc_) {
                     // hit list overflow: scan once more, recording only the groups inside
@@ -518,9 +579,10 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
                     };
 #pragma unroll 1
                     for (int hf = 0; hf < 2; hf++) {
-                        const int cnt = min(hf ? cnt1 : cnt0, CAP);
+                        const int cnt = min(hf ? cnt1 : cnt0, prm.cap);
                         const uint32_t ent = hf ? ent1 : ent0;
                         unsigned m = __ballot_sync(MPW_FULL, lane < cnt && (int)(ent >> 16) - KEY_BIAS < limit);
+                        if (STATS && (prm.experiment & 2)) m = 0u;   // timing probe: no scoring
                         uint4 n0, n1;
                         if (m) load_group((int)(__shfl_sync(MPW_FULL, ent, __ffs(m) - 1) & 0xFFFFu), n0, n1);
                         while (m) {
@@ -660,7 +722,7 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
                 wq_ = wf < 16384.f ? __float2int_ru(wf) : 16384;
                 // the row image is complete and visible to the tensor core's reads of
                 // every MMA issued from now on
-                fence_proxy_async();
+                if (!(STATS && (prm.experiment & 16))) fence_proxy_async();   // (16: timing probe without the fence)
                 __syncwarp();
                 if (lane == 0) {
                     row_best[row] = 0x7FFFFFFF;

@@ -24,6 +24,7 @@ struct TcOpts {
     int i8_pair = 0;       // int8, N = 256: cta_group::2 pair kernel
     int i8_cluster = 1;    // int8, N = 256: 2 = CTA pairs sharing the P stream by multicast
     int f16_cluster = 1;   // 1-limb, N = 256: CTA pairs sharing the P stream (default on)
+    int ar_hit_cap = 0;    // asynchronous-row hop: hit-list capacity per scan thread (0 = the compiled maximum)
 };
 
 bool tc_supported(int n, int np);

@@ -454,16 +454,17 @@ int launch_gather(mpw_handle* h, HopParams hp, int max_traj, cudaStream_t st) {
     return 0;
 }
 
-// MPW_HOP_AUTO: the int8 screen where a round streams enough of P to amortise
-// its wider certification window (N = 256 and >= 32 tiles of 256 patterns:
-// cfg4 0.71x the f16 hop time; slower on cfg2/cfg3), else one fp16 limb, else
-// the gather kernel
+// MPW_HOP_AUTO: the int8 screen where a scan streams enough of P to amortise
+// its wider certification window (N = 256 and >= 32 tiles of 256 patterns), in
+// its asynchronous-row form (hop_ar.cuh: cfg4 82 ms against 107 ms for the
+// synchronous rounds of hop_tc.cuh); else one fp16 limb, else the gather kernel
 // float64 inputs (f64): the 1-limb fp16 screen with float64 re-scoring, else
 // the gather kernel
 int resolve_variant(mpw_handle* h, int variant, bool f64 = false) {
     if (variant != MPW_HOP_AUTO) return variant;
     if (!(tc_supported(h->n, h->np) && h->tcp.ready)) return MPW_HOP_GATHER;
-    if (!f64 && h->tcp.ready8 && h->n >= 256 && h->tcp.ntiles >= 32) return MPW_HOP_TENSOR_I8;
+    if (!f64 && h->tcp.ready8 && h->n >= 256 && h->tcp.ntiles >= 32)
+        return ar_supported(h->tcp, h->n) ? MPW_HOP_TENSOR_I8_ASYNC : MPW_HOP_TENSOR_I8;
     return MPW_HOP_TENSOR;
 }
 
@@ -1150,6 +1151,11 @@ int mpw_set_option(mpw_handle* h, const char* key, int value) {
         return 0;
     }
     if (!strcmp(key, "f16_cluster")) { h->tco.f16_cluster = value ? 1 : 0; return 0; }
+    if (!strcmp(key, "ar_hit_cap")) {   // asynchronous-row hop: hit-list entries per scan thread and cycle (tests: small values force re-scans)
+        if (value < 0 || value > 30) return fail(MPW_ERR_ARG, "ar_hit_cap must be 0 (default) .. 30");
+        h->tco.ar_hit_cap = value;
+        return 0;
+    }
     return fail(MPW_ERR_ARG, "unknown option '%s'", key);
 }
 

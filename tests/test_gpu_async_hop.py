@@ -1,0 +1,125 @@
+"""GPU parity of the asynchronous-row int8 hop (hop_ar.cuh, variant "tensor_i8a")
+on the paths its design adds: hit-list overflow (re-scan with a seeded running
+minimum), exact ties (coarse received words), ragged anchor lists and queues
+smaller than one CTA, and hop-by-hop equality of the accepted patterns with the
+oracle.  Codewords must equal the oracle's except on frames the kernel flags."""
+import numpy as np
+import pytest
+
+from oracle import oracle as orc
+from paper_2602_08501_b200 import channel, configs
+from paper_2602_08501_b200.codes import encode_batch
+from paper_2602_08501_b200.decoders import DeviceDecoder, words32_to_64, words64_to_32
+from paper_2602_08501_b200._native import FLAG_TIE_FINAL as TIE_FINAL, FLAG_UNRESOLVED as UNRESOLVED
+from tests.helpers import code_and_sphere
+
+pytestmark = pytest.mark.gpu
+
+
+def _np(t):
+    return t.cpu().numpy()
+
+
+def _check_two_stage(cfg, code, sph, dec, y, sigma, max_flagged):
+    o = dec.two_stage_batch(y, sigma, cfg.list_size, cfg.num_paths, cfg.max_iterations,
+                            cfg.activation_mode, variant="tensor_i8a")
+    r = orc.two_stage_batch(y, code, sph, cfg.list_size, cfg.num_paths, cfg.max_iterations,
+                            cfg.activation_mode == "crc_gated", sigma, nthreads=8)
+    best = words32_to_64(_np(o["best"]).view(np.uint32), code.n)
+    flags = _np(o["flags"])
+    mism = np.flatnonzero((best != r["best"]).any(axis=1))
+    risky = np.flatnonzero(flags & (UNRESOLVED | TIE_FINAL))
+    assert set(mism.tolist()) <= set(risky.tolist()), f"unflagged mismatches {mism}"
+    assert len(risky) <= max_flagged, f"{len(risky)} flagged frames"
+    ok = np.setdiff1d(np.arange(y.shape[0]), risky)
+    np.testing.assert_array_equal(_np(o["iters"])[ok], r["iters"][ok])
+    return o, r
+
+
+@pytest.mark.parametrize("name,cap,max_flagged", [("cfg4", 3, 128), ("cfg4", 10, 4), ("cfg2", 8, 8)])
+def test_hit_list_overflow_rescans(name, cap, max_flagged):
+    """With the hit lists cut to a few entries most cycles overflow: the row
+    scans again with the achieved minimum as the seed, and the decisions (and
+    iterations_used, which must not count the extra scans) still equal the
+    oracle's.  A frame is flagged UNRESOLVED only if the seeded re-scan overflows
+    too, i.e. its true window holds more groups than the cut list (with 3
+    entries that happens in most frames: 72 row cycles each; the unflagged ones
+    must still be exact)."""
+    cfg = configs.CONFIGS[name]
+    code, sph = code_and_sphere(cfg)
+    sigma = cfg.sigma(code=code)
+    F = 128 if name == "cfg4" else 256
+    _, _, y = channel.bulk_inputs(code, 21, 0, 0, F, sigma)
+    dec = DeviceDecoder(code, sph)
+    dec.set_option("ar_hit_cap", cap)
+    _check_two_stage(cfg, code, sph, dec, y, sigma, max_flagged=max_flagged)
+
+
+@pytest.mark.parametrize("name", ["cfg4", "cfg2"])
+def test_coarse_received_words_ties(name):
+    """Received words on a grid of 0.5 make many pattern scores equal exactly: the
+    argmin must be the lowest pattern index among the exact ties
+    (decoders.py:391) and accept only strict improvement (decoders.py:395-398)."""
+    cfg = configs.CONFIGS[name]
+    code, sph = code_and_sphere(cfg)
+    sigma = cfg.sigma(code=code)
+    F = 96 if name == "cfg4" else 192
+    _, _, y = channel.bulk_inputs(code, 22, 0, 0, F, sigma)
+    y = (np.round(y * 2.0) / 2.0).astype(np.float32)
+    dec = DeviceDecoder(code, sph)
+    # exact ties are reported (TIE flags) but must be resolved like the oracle
+    o = dec.two_stage_batch(y, sigma, cfg.list_size, cfg.num_paths, cfg.max_iterations,
+                            cfg.activation_mode, variant="tensor_i8a")
+    r = orc.two_stage_batch(y, code, sph, cfg.list_size, cfg.num_paths, cfg.max_iterations,
+                            cfg.activation_mode == "crc_gated", sigma, nthreads=8)
+    best = words32_to_64(_np(o["best"]).view(np.uint32), code.n)
+    flags = _np(o["flags"])
+    mism = np.flatnonzero((best != r["best"]).any(axis=1))
+    # equal final EDs of different anchors (TIE_FINAL) pick the lowest anchor in both; only
+    # UNRESOLVED frames (more than 32 exactly tied finalists) may differ
+    assert set(mism.tolist()) <= set(np.flatnonzero(flags & UNRESOLVED).tolist()), f"mismatches {mism}"
+    ok = np.flatnonzero((flags & UNRESOLVED) == 0)
+    np.testing.assert_array_equal(_np(o["iters"])[ok], r["iters"][ok])
+
+
+@pytest.mark.parametrize("F", [1, 5, 300])
+def test_mp_wsd_hops_and_ragged_anchor_lists(F):
+    """mp_wsd on random anchors with ragged anchor counts (including queues far
+    smaller than one CTA's 128 rows): accepted pattern per hop, iterations_used
+    and best codewords equal the oracle's."""
+    cfg = configs.CONFIGS["cfg4"]
+    code, sph = code_and_sphere(cfg)
+    rng = np.random.default_rng(23 + F)
+    A, T = 6, 8
+    msgs = rng.integers(0, 2, (F * A, code.k), dtype=np.uint8)
+    anc64 = encode_batch(code, msgs).reshape(F, A, -1)
+    sigma = cfg.sigma(code=code)
+    # a noisy version of the first anchor: trajectories from the other anchors make many moves
+    first = np.unpackbits(np.ascontiguousarray(anc64[:, 0]).view(np.uint8), axis=-1, bitorder="little")[:, :code.n]
+    y = ((1.0 - 2.0 * first) + rng.normal(0.0, sigma, size=(F, code.n))).astype(np.float32)
+    nanc = rng.integers(1, A + 1, size=F).astype(np.int32)
+    dec = DeviceDecoder(code, sph)
+    o = dec.mp_wsd_batch(y, words64_to_32(anc64, code.n), T, n_anchor=nanc, variant="tensor_i8a")
+    best = words32_to_64(_np(o["best"]).view(np.uint32), code.n)
+    flags = _np(o["flags"])
+    risky = set(np.flatnonzero(flags & (UNRESOLVED | TIE_FINAL)).tolist())
+    # the oracle takes one anchor count per call: frames grouped by their count
+    for a in np.unique(nanc):
+        idx = np.flatnonzero(nanc == a)
+        r = orc.mpwsd_batch(y[idx], np.ascontiguousarray(anc64[idx, :a]), sph, T, nthreads=8)
+        for k, f in enumerate(idx):
+            if int(f) in risky:
+                continue
+            np.testing.assert_array_equal(best[f], r["best"][k], err_msg=f"frame {f}")
+            np.testing.assert_array_equal(_np(o["iters"])[f, :a], r["iters"][k], err_msg=f"frame {f}")
+            np.testing.assert_array_equal(_np(o["hops"])[f, :a], r["hops"][k], err_msg=f"frame {f}")
+    assert len(risky) <= max(1, F // 50)
+
+
+def test_auto_picks_the_async_hop_on_cfg4():
+    cfg = configs.CONFIGS["cfg4"]
+    code, sph = code_and_sphere(cfg)
+    assert DeviceDecoder(code, sph).auto_variant == "tensor_i8a"
+    cfg2 = configs.CONFIGS["cfg2"]
+    code2, sph2 = code_and_sphere(cfg2)
+    assert DeviceDecoder(code2, sph2).auto_variant == "tensor"

@@ -28,7 +28,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--frames", type=int, default=8192)
     ap.add_argument("--config", default="cfg4")
-    ap.add_argument("--variants", default="tensor_i8,tensor,tensor2")
+    ap.add_argument("--variants", default="tensor_i8a,tensor_i8,tensor,tensor2")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "cfg4_oracle_subsample.json"))
     args = ap.parse_args()
     cfg = configs.CONFIGS[args.config]

@@ -54,7 +54,8 @@ constexpr int SCAN_W0 = 4;
 constexpr int WORK_W0 = SCAN_W0 + SCAN_T / 32;
 constexpr int THREADS = 32 * (WORK_W0 + NWORK);
 static_assert(NWORK % 4 == 0, "worker warps in whole warpgroups");
-constexpr int CAP = 30;                        // hit-list entries per scan thread and cycle
+constexpr int CAP = 22;                        // hit-list entries per scan thread and cycle
+constexpr int RSW = 16;                        // 32-bit words of a row's state in shared memory
 constexpr int AR_STAGES = 5;                   // P ring stages (one 128-position K-block of a tile each)
 constexpr int Q_INF = 0x7FFF;                  // s16 maximum: "no score"
 #ifndef MPW_AR_NISS
@@ -62,7 +63,7 @@ constexpr int Q_INF = 0x7FFF;                  // s16 maximum: "no score"
 #endif
 constexpr int NISS = MPW_AR_NISS;             // MMA issuer threads (alternate tiles)
 static_assert(NISS == 1 || NISS == 2, "one issuer per accumulator");
-constexpr int MARGIN = 2;                      // tiles between the issue counter read and a row's first live tile
+constexpr int MARGIN = 1;                      // tiles between the issue counter read and a row's first live tile
 static_assert(CAP <= 32, "one hit entry per worker lane");
 // a hit entry names a group of 32 patterns in 16 bits: |P| <= 2^17 gives 4096 groups
 
@@ -86,6 +87,7 @@ struct Params {
 __host__ __device__ constexpr size_t smem_bytes(int kb) {
     return (size_t)kb * A_KBLK_BYTES + (size_t)AR_STAGES * I8_STAGE_BYTES + (size_t)CAP * SCAN_T * 4 +
            ROWS * 8 /*row_ctl*/ + ROWS * 4 /*row_best*/ + ROWS * 4 /*row_done*/ + SCAN_T /*hit_cnt*/ +
+           ROWS * RSW * 4 /*row state*/ + 16 /*ready mask*/ +
            (2 * AR_STAGES + 4) * 8 /*barriers*/ + 16 /*tmem slot, stop tile, issue counter, rows left*/;
 }
 
@@ -174,7 +176,9 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
     int* row_best = reinterpret_cast<int*>(row_ctl + ROWS);                 // [ROWS] running minimum over both halves
     int* row_done = row_best + ROWS;                                        // [ROWS] halves that finished the cycle
     uint8_t* hit_cnt = reinterpret_cast<uint8_t*>(row_done + ROWS);         // [SCAN_T] entries recorded in the cycle
-    uint64_t* bars = reinterpret_cast<uint64_t*>(hit_cnt + SCAN_T);
+    uint32_t* row_state = reinterpret_cast<uint32_t*>(hit_cnt + SCAN_T);    // [ROWS][RSW]: c[8], trajectory, frame, iters | flags | recyc, ed, err, inv_s, sum|y|, wq
+    uint32_t* ready_mask = row_state + ROWS * RSW;                          // [4]: rows whose cycle ended (or that await their first trajectory)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(ready_mask + 4);
     uint64_t* full = bars;
     uint64_t* empty = bars + STAGES;
     uint64_t* tfull = bars + 2 * STAGES;
@@ -201,6 +205,8 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
         row_done[r] = 0;
     }
     for (int r = threadIdx.x; r < SCAN_T; r += THREADS) hit_cnt[r] = 0;
+    for (int r = threadIdx.x; r < ROWS * RSW; r += THREADS) row_state[r] = (r % RSW) == 8 ? 0xFFFFFFFFu : 0u;   // no trajectory yet
+    if (threadIdx.x < 4) ready_mask[threadIdx.x] = 0xFFFFFFFFu;   // every row awaits its first trajectory
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -378,7 +384,7 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
                 if (STATS) st_entries += cnt;
                 hit_cnt[thr] = (uint8_t)min(cnt, 255);
                 __threadfence_block();
-                atomicAdd(&row_done[row], 1);
+                if (atomicAdd(&row_done[row], 1) == 1) atomicOr(&ready_mask[row >> 5], 1u << (row & 31));   // both halves done
             }
             if (++j == ntiles) j = 0;
         }
@@ -393,17 +399,9 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
         }
     } else {
         asm volatile("setmaxnreg.inc.sync.aligned.u32 120;");
-        // ===== workers: worker w owns rows lane * NWORK + w; the row state lives in
-        // the registers of the lane that owns the row and is broadcast by shuffles
+        // ===== workers: any worker takes any ready row (a bit mask of rows whose cycle
+        // ended); the row's state lives in shared memory between its cycles
         const int w = warp - WORK_W0;
-        const int myrow = lane * NWORK + w;
-        int tr = -1, frame = 0, iters = 0, wq = 0;
-        uint32_t flags = 0;
-        float ed = 0.f, err = 0.f, inv_s = 1.f, ay = 0.f;
-        uint32_t c[NW];
-#pragma unroll
-        for (int k = 0; k < NW; k++) c[k] = 0u;
-        bool fresh = lane < ROWS / NWORK, exhausted = false, recyc = false;   // lanes beyond the partition own no row
         const int count = *prm.s2.count;
         const int ntraj = count * A;
         // the worker's pocket: the next trajectory of the stage-2 queue, claimed ahead of
@@ -440,23 +438,36 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
 #define PH(k) if (STATS) { const long long t_ = clock64(); ph[k] += t_ - t_ph; t_ph = t_; }
         for (;;) {
             if (ld_shared_volatile_u32(stop_tile) != 0xFFFFFFFFu) break;
-            const int d = fresh ? 2 : ((exhausted || lane >= ROWS / NWORK) ? 0 : ld_shared_volatile(&row_done[myrow]));
-            const unsigned ready = __ballot_sync(MPW_FULL, d == 2);
-            if (!ready) { __nanosleep(200); continue; }
+            // a ready row: every worker starts its search at a different word of the mask
+            const int wi_l = (lane + w) & 3;
+            const uint32_t mw = lane < 4 ? ld_shared_volatile_u32(ready_mask + wi_l) : 0u;
+            const unsigned has = __ballot_sync(MPW_FULL, mw != 0u);
+            if (!has) { __nanosleep(100); continue; }
             long long t_busy0 = 0;
             if (STATS) { t_busy0 = clock64(); t_ph = t_busy0; }
-            const int L = __ffs(ready) - 1;
-            const int row = L * NWORK + w;
-            // the row's state, broadcast from its owner lane
-            int tr_ = __shfl_sync(MPW_FULL, tr, L), frame_ = __shfl_sync(MPW_FULL, frame, L);
-            int iters_ = __shfl_sync(MPW_FULL, iters, L), wq_ = __shfl_sync(MPW_FULL, wq, L);
-            uint32_t flags_ = __shfl_sync(MPW_FULL, flags, L);
-            float ed_ = __shfl_sync(MPW_FULL, ed, L), err_ = __shfl_sync(MPW_FULL, err, L);
-            float inv_ = __shfl_sync(MPW_FULL, inv_s, L), ay_ = __shfl_sync(MPW_FULL, ay, L);
-            bool recyc_ = __shfl_sync(MPW_FULL, (int)recyc, L) != 0;
+            const int srcl = __ffs(has) - 1;
+            const int wi = (srcl + w) & 3;
+            const uint32_t mword = __shfl_sync(MPW_FULL, mw, srcl);
+            const int bit = (w & 1) ? 31 - __clz(mword) : __ffs(mword) - 1;   // two search directions: fewer collisions
+            uint32_t old = 0u;
+            if (lane == 0) old = atomicAnd(&ready_mask[wi], ~(1u << bit));
+            old = __shfl_sync(MPW_FULL, old, 0);
+            if (!((old >> bit) & 1u)) continue;   // another worker took it
+            const int row = wi * 32 + bit;
+            __threadfence_block();
+            // the row's state
+            const uint32_t sw = lane < RSW ? row_state[row * RSW + lane] : 0u;
             uint32_t c_[NW];
 #pragma unroll
-            for (int k = 0; k < NW; k++) c_[k] = __shfl_sync(MPW_FULL, c[k], L);
+            for (int k = 0; k < NW; k++) c_[k] = __shfl_sync(MPW_FULL, sw, k);
+            int tr_ = (int)__shfl_sync(MPW_FULL, sw, 8), frame_ = (int)__shfl_sync(MPW_FULL, sw, 9);
+            const uint32_t packed = __shfl_sync(MPW_FULL, sw, 10);
+            int iters_ = (int)(packed & 0xFFFFu);
+            uint32_t flags_ = (packed >> 16) & 0xFFu;
+            bool recyc_ = (packed >> 24) != 0u;
+            float ed_ = __uint_as_float(__shfl_sync(MPW_FULL, sw, 11)), err_ = __uint_as_float(__shfl_sync(MPW_FULL, sw, 12));
+            float inv_ = __uint_as_float(__shfl_sync(MPW_FULL, sw, 13)), ay_ = __uint_as_float(__shfl_sync(MPW_FULL, sw, 14));
+            int wq_ = (int)__shfl_sync(MPW_FULL, sw, 15);
             int seed = Q_INF;
             bool need_claim = tr_ < 0;
             bool exhausted_ = false;
@@ -720,6 +731,19 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
                 // window of the next cycle in q units (rounded up; >= 16384 records everything)
                 const float wf = (2.0f * err_ + prm.tie_rel * ed_ * 0.25f) * inv_ * 1.00001f + 1.0f;
                 wq_ = wf < 16384.f ? __float2int_ru(wf) : 16384;
+                // the row's state back to shared memory (whichever worker decides its next cycle)
+                {
+                    uint32_t ow = select_word<NW>(c_, lane & (NW - 1));
+                    if (lane == 8) ow = (uint32_t)tr_;
+                    if (lane == 9) ow = (uint32_t)frame_;
+                    if (lane == 10) ow = (uint32_t)iters_ | (flags_ << 16) | ((recyc_ ? 1u : 0u) << 24);
+                    if (lane == 11) ow = __float_as_uint(ed_);
+                    if (lane == 12) ow = __float_as_uint(err_);
+                    if (lane == 13) ow = __float_as_uint(inv_);
+                    if (lane == 14) ow = __float_as_uint(ay_);
+                    if (lane == 15) ow = (uint32_t)wq_;
+                    if (lane < RSW) row_state[row * RSW + lane] = ow;
+                }
                 // the row image is complete and visible to the tensor core's reads of
                 // every MMA issued from now on
                 if (!(STATS && (prm.experiment & 16))) fence_proxy_async();   // (16: timing probe without the fence)
@@ -732,15 +756,6 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
                     st_shared_volatile_v2(&row_ctl[row],
                                           make_uint2(v + MARGIN, ((uint32_t)wq_ << 16) | (uint32_t)(seed + KEY_BIAS)));
                 }
-            }
-            if (lane == L) {
-                tr = tr_; frame = frame_; iters = iters_; wq = wq_; flags = flags_;
-                ed = ed_; err = err_; inv_s = inv_; ay = ay_;
-                recyc = recyc_;
-                fresh = false;
-                exhausted = exhausted_;
-#pragma unroll
-                for (int k = 0; k < NW; k++) c[k] = c_[k];
             }
             PH(4);
             if (used_pocket) refill_pocket();   // after the row is live again

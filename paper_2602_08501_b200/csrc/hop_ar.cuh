@@ -148,7 +148,7 @@ __device__ __forceinline__ int min64_s16_only(const uint32_t (&v)[32]) {
 // barrier waits of the producer and the issuer: 1 = spin on try_wait, 0 = try_wait with a
 // suspend-time hint (the thread sleeps until the phase completes)
 #ifndef MPW_AR_SPIN
-#define MPW_AR_SPIN 1
+#define MPW_AR_SPIN 0
 #endif
 __device__ __forceinline__ void ar_wait(uint32_t bar, uint32_t parity) {
 #if MPW_AR_SPIN
@@ -519,6 +519,7 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
                     float fs = CUDART_INF_F;   // finalist `lane`: fp32 score, pattern
                     int fi = 0x7FFFFFFF;
                     bool tv_ready = false;
+                    uint32_t pw = 0u;          // lanes < NW: word `lane` of the running best pattern
                     // Per hit group (32 patterns): lane L holds byte L (positions 8 L .. 8 L + 7)
                     // of all 32 patterns (transposed bits, one 32-byte load per lane) and the
                     // row's int8 values of the same positions; the exact integer score Q_j of
@@ -579,7 +580,12 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
                                 if ((byte >> k) & 1u) sp += tv[k];
 #pragma unroll
                             for (int o = 16; o > 0; o >>= 1) sp += __shfl_xor_sync(MPW_FULL, sp, o);
-                            if (sp < Bs || (sp == Bs && pc < Bi)) { Bs = sp; Bi = pc; }
+                            if (sp < Bs || (sp == Bs && pc < Bi)) {
+                                Bs = sp;
+                                Bi = pc;
+                                // the running best's bits are fetched now; a move needs them later
+                                if (lane < NW) pw = __ldg(prm.pbits + (size_t)pc * NW + lane);
+                            }
                             // finalists: everything within the certification margin of the running best
                             // (the difference of two close floats is exact)
                             if (sp - Bs < Mf) {
@@ -588,22 +594,27 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
                             }
                         }
                     };
+                    // the row's hit groups of both halves as one 64-bit mask over (half, list slot);
+                    // the next group's bytes are in flight while a group is scored
+                    const int c0 = min(cnt0, prm.cap), c1 = min(cnt1, prm.cap);
+                    unsigned long long mm =
+                        (unsigned long long)__ballot_sync(MPW_FULL, lane < c0 && (int)(ent0 >> 16) - KEY_BIAS < limit) |
+                        ((unsigned long long)__ballot_sync(MPW_FULL, lane < c1 && (int)(ent1 >> 16) - KEY_BIAS < limit) << 32);
+                    if (STATS && (prm.experiment & 2)) mm = 0ull;   // timing probe: no scoring
+                    auto group_at = [&](unsigned long long m) {
+                        const int idx = __ffsll((long long)m) - 1;
+                        const uint32_t e = __shfl_sync(MPW_FULL, idx & 32 ? ent1 : ent0, idx & 31);
+                        return (int)(e & 0xFFFFu);
+                    };
+                    uint4 n0, n1;
+                    if (mm) load_group(group_at(mm), n0, n1);
 #pragma unroll 1
-                    for (int hf = 0; hf < 2; hf++) {
-                        const int cnt = min(hf ? cnt1 : cnt0, prm.cap);
-                        const uint32_t ent = hf ? ent1 : ent0;
-                        unsigned m = __ballot_sync(MPW_FULL, lane < cnt && (int)(ent >> 16) - KEY_BIAS < limit);
-                        if (STATS && (prm.experiment & 2)) m = 0u;   // timing probe: no scoring
-                        uint4 n0, n1;
-                        if (m) load_group((int)(__shfl_sync(MPW_FULL, ent, __ffs(m) - 1) & 0xFFFFu), n0, n1);
-                        while (m) {
-                            const int grp = (int)(__shfl_sync(MPW_FULL, ent, __ffs(m) - 1) & 0xFFFFu);
-                            m &= m - 1;
-                            const uint4 t0 = n0, t1 = n1;
-                            // the next group's bytes are in flight during this group
-                            if (m) load_group((int)(__shfl_sync(MPW_FULL, ent, __ffs(m) - 1) & 0xFFFFu), n0, n1);
-                            do_group(grp, t0, t1);
-                        }
+                    while (mm) {
+                        const int grp = group_at(mm);
+                        mm &= mm - 1;
+                        const uint4 t0 = n0, t1 = n1;
+                        if (mm) load_group(group_at(mm), n0, n1);
+                        do_group(grp, t0, t1);
                     }
                     PH(1);
                     if (nf > 32) flags_ |= MPW_F_UNRESOLVED;   // more near-equal scores than lanes
@@ -643,7 +654,7 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
                     iters_++;
                     if (improve) {
                         // the move: c ^= p, the moved positions' int8 values negated
-                        const uint32_t pw = lane < NW ? __ldg(prm.pbits + (size_t)best * NW + lane) : 0u;
+                        if (best != Bi) pw = lane < NW ? __ldg(prm.pbits + (size_t)best * NW + lane) : 0u;
 #pragma unroll
                         for (int k = 0; k < NW; k++) c_[k] ^= __shfl_sync(MPW_FULL, pw, k);
                         const uint32_t word = __shfl_sync(MPW_FULL, pw, (lane >> 2) & (NW - 1));

@@ -57,13 +57,13 @@ static int ar_launch_t(const TcPatterns& t, int n, int A, int T, const float* y,
     if (STATS) {
         cudaStreamSynchronize(st);
         const unsigned long long* s = stats;
-        const double tiles = (double)s[ar::ST_TILES] / 32.0 / 8.0;   // per-lane counts of 8 scan warps
+        const double tiles = (double)s[ar::ST_TILES] / 32.0 / (ar::SCAN_T / 32);   // per-lane counts of the scan warps
         fprintf(stderr,
                 "[hop_ar] CTA-tiles %.0f, live row-halves %.4f, row cycles %llu (finished %llu), hit chunks/cycle %.3f, "
                 "entries/thread-cycle %.2f, f64 decisions %llu, overflow re-scans %llu, worker busy cycles/row-cycle %.0f\n",
                 tiles, s[ar::ST_TILES] ? (double)s[ar::ST_LIVE] / (double)s[ar::ST_TILES] : 0.0, s[ar::ST_ROWCYC],
                 s[ar::ST_FINISHED], s[ar::ST_ROWCYC] ? (double)s[ar::ST_CHUNKS] / (double)s[ar::ST_ROWCYC] : 0.0,
-                s[ar::ST_ROWCYC] ? (double)s[ar::ST_ENTRIES] / (2.0 * (double)s[ar::ST_ROWCYC]) : 0.0, s[ar::ST_F64],
+                s[ar::ST_ROWCYC] ? (double)s[ar::ST_ENTRIES] / ((double)ar::NCOL * (double)s[ar::ST_ROWCYC]) : 0.0, s[ar::ST_F64],
                 s[ar::ST_OVF], s[ar::ST_ROWCYC] ? (double)s[ar::ST_BUSY] / (double)s[ar::ST_ROWCYC] : 0.0);
         fprintf(stderr,
                 "[hop_ar] cycles per tile %.0f; issuer: B stage wait %.3f, accumulator wait %.3f, MMA issue + commit %.3f of its time; scan warps wait "
@@ -76,9 +76,10 @@ static int ar_launch_t(const TcPatterns& t, int n, int A, int T, const float* y,
         const double rc = s[ar::ST_ROWCYC] ? (double)s[ar::ST_ROWCYC] : 1.0;
         fprintf(stderr,
                 "[hop_ar] worker cycles per row cycle: lists+t %.0f, chunk scores %.0f, decision+move %.0f, claim+build %.0f, "
-                "publish %.0f, pocket refill %.0f\n",
+                "publish %.0f, pocket refill %.0f; tiles per row cycle "
+                "between cycle end and next start %.2f\n",
                 s[ar::ST_W_LIST] / rc, s[ar::ST_W_CHUNK] / rc, s[ar::ST_W_DECIDE] / rc, s[ar::ST_W_CLAIM] / rc,
-                s[ar::ST_W_PUBLISH] / rc, s[ar::ST_W_POCKET] / rc);
+                s[ar::ST_W_PUBLISH] / rc, s[ar::ST_W_POCKET] / rc, s[ar::ST_DEAD] / rc);
     }
     return 0;
 }

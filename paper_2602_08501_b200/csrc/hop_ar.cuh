@@ -29,13 +29,17 @@
 // running minimum (then only true window chunks are recorded); the extra scan
 // is not counted in iterations_used.
 //
-// CTA = 20 warps, persistent, one per SM:
+// CTA = 28 warps (NCOL = 4; 20 with NCOL = 2), persistent, one per SM:
 //   warp 0        producer: cp.async.bulk of 32 KB pre-swizzled u8 P stages
-//   warp 1        TMEM allocator + tcgen05.mma issuer (warps 2, 3 idle: they fill the warpgroup)
-//   warps 4..11   scan: two per TMEM lane quarter (columns [0,128) / [128,256))
-//   warps 12..19  workers: decisions, moves, refills
-// Register budgets (setmaxnreg; the CTA's pool is what its own warps release): warps 0..3
-// drop from 96 to 40 registers, the workers take 120, the scan warps stay at 96.
+//   warps 1, 2    TMEM allocator + two tcgen05.mma issuer threads (warp 3 idle: it fills the warpgroup)
+//   warps 4..19   scan: NCOL per TMEM lane quarter, 256 / NCOL columns of every tile each (a scan
+//                 warp's per-tile work is serial -- wait, TMEM load, release, minima, records -- so
+//                 with two warps per quarter it, not the MMA, set the tile period)
+//   warps 20..27  workers: decisions, moves, refills
+// Register budgets (setmaxnreg; the CTA's pool is what its own warps release).  NCOL = 2:
+// warps 0..3 drop from 96 to 40 registers, the workers take 120, the scan warps stay at 96.
+// NCOL = 4 (16 scan warps, 896 threads, 72 registers at launch): warps 0..3 drop to 40, the
+// scan warps to 64, the workers take 104.
 #pragma once
 #include "hop_tc.cuh"
 
@@ -47,14 +51,21 @@ using namespace tc;
 #endif
 constexpr int NWORK = MPW_AR_NWORK;            // worker warps (rows statically partitioned)
 static_assert(ROWS % NWORK == 0 && ROWS / NWORK <= 32, "rows per worker");
-constexpr int SCAN_T = 256;                    // scan threads (two per row)
+#ifndef MPW_AR_NCOL
+#define MPW_AR_NCOL 2
+#endif
+constexpr int NCOL = MPW_AR_NCOL;              // scan threads per row: each scans 256 / NCOL columns of every tile
+static_assert(NCOL == 2 || NCOL == 4, "column parts per row");
+constexpr int SCAN_T = ROWS * NCOL;            // scan threads
+constexpr int NLD = I8_TILE / NCOL / 64;       // 64-column TMEM loads per scan thread and tile
+constexpr int NGRP = I8_TILE / NCOL / 32;      // 32-pattern groups per scan thread and tile
 // warps 0..3: producer, MMA issuer, two idle (one warpgroup, so the three register budgets
 // below can be set per warpgroup); warps 4..11 scan; warps 12.. workers
 constexpr int SCAN_W0 = 4;
 constexpr int WORK_W0 = SCAN_W0 + SCAN_T / 32;
 constexpr int THREADS = 32 * (WORK_W0 + NWORK);
 static_assert(NWORK % 4 == 0, "worker warps in whole warpgroups");
-constexpr int CAP = 22;                        // hit-list entries per scan thread and cycle
+constexpr int CAP = NCOL == 2 ? 22 : 11;       // hit-list entries per scan thread and cycle
 constexpr int RSW = 16;                        // 32-bit words of a row's state in shared memory
 constexpr int AR_STAGES = 5;                   // P ring stages (one 128-position K-block of a tile each)
 constexpr int Q_INF = 0x7FFF;                  // s16 maximum: "no score"
@@ -121,6 +132,20 @@ __device__ __forceinline__ void trap_if(bool p) {
 }
 
 // minimum of 32 packed s16 values (registers o .. o + 15): 8 three-input instructions
+template <int NV>
+__device__ __forceinline__ int min32_s16_b(const uint32_t (&v)[NV], int o) {
+    if constexpr (NV < 32) {
+        return 0x7FFF;
+    } else {
+        const uint32_t a = min3_s16x2(v[o], v[o + 1], v[o + 2]), b = min3_s16x2(v[o + 3], v[o + 4], v[o + 5]);
+        const uint32_t c = min3_s16x2(v[o + 6], v[o + 7], v[o + 8]), d = min3_s16x2(v[o + 9], v[o + 10], v[o + 11]);
+        const uint32_t e = min3_s16x2(v[o + 12], v[o + 13], v[o + 14]);
+        const uint32_t f = min3_s16x2(a, b, c), g = min3_s16x2(d, e, v[o + 15]);
+        uint32_t r;
+        asm("min.s16x2 %0, %1, %2;" : "=r"(r) : "r"(f), "r"(g));
+        return min((int)(short)(r & 0xFFFFu), (int)(short)(r >> 16));
+    }
+}
 __device__ __forceinline__ int min32_s16(const uint32_t (&v)[32], int o) {
     const uint32_t a = min3_s16x2(v[o], v[o + 1], v[o + 2]), b = min3_s16x2(v[o + 3], v[o + 4], v[o + 5]);
     const uint32_t c = min3_s16x2(v[o + 6], v[o + 7], v[o + 8]), d = min3_s16x2(v[o + 9], v[o + 10], v[o + 11]);
@@ -158,10 +183,14 @@ __device__ __forceinline__ void ar_wait(uint32_t bar, uint32_t parity) {
 #endif
 }
 
+#ifndef MPW_AR_BACKOFF
+#define MPW_AR_BACKOFF 3000
+#endif
+
 // stats slots
 enum { ST_TILES = 0, ST_LIVE, ST_ROWCYC, ST_CHUNKS, ST_F64, ST_OVF, ST_BUSY, ST_FINISHED, ST_ENTRIES,
        ST_SCAN_WAIT, ST_SCAN_TOT, ST_ISS_FULL, ST_ISS_TEMPTY, ST_ISS_TOT, ST_W_LIST, ST_W_CHUNK, ST_W_DECIDE, ST_W_CLAIM,
-       ST_W_PUBLISH, ST_W_POCKET, ST_ISS_MMA, ST_N };
+       ST_W_PUBLISH, ST_W_POCKET, ST_ISS_MMA, ST_DEAD, ST_N };
 
 template <int KB, int NW, bool STATS>
 __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
@@ -193,7 +222,7 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; s++) { mbar_init(smem_u32(&full[s]), 1); mbar_init(smem_u32(&empty[s]), 1); }
-        for (int b = 0; b < 2; b++) { mbar_init(smem_u32(&tfull[b]), 1); mbar_init(smem_u32(&tempty[b]), 8); }
+        for (int b = 0; b < 2; b++) { mbar_init(smem_u32(&tfull[b]), 1); mbar_init(smem_u32(&tempty[b]), 4 * NCOL); }
         *stop_tile = 0xFFFFFFFFu;
         *issue_ctr = 0u;
         *rows_left = ROWS;
@@ -216,8 +245,8 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    // register budgets per warpgroup (the kernel starts with 96 per thread; an increase can only
-    // take what a decrease in the same CTA released: 4 x 32 x 56 >= 8 x 32 x 24)
+    // register budgets per warpgroup (an increase can only take what decreases in the same CTA
+    // released: NCOL = 2, from 96: 4 x 32 x 56 >= 8 x 32 x 24; NCOL = 4, from 72: 4 x 32 x 32 + 16 x 32 x 8 = 8 x 32 x 32)
     if (warp < SCAN_W0) {
       asm volatile("setmaxnreg.dec.sync.aligned.u32 40;");
       if (warp == 0) {
@@ -297,12 +326,13 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
         }
       }
     } else if (warp < WORK_W0) {
-        // ===== scan: thread = (row, column half); no data-dependent branch per tile
+        if (NCOL == 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 64;");
+        // ===== scan: thread = (row, column part); no data-dependent branch per tile
         const int g = warp & 3;                      // TMEM lane quarter of this warp
-        const int half = (warp - SCAN_W0) >> 2;
+        const int colq = (warp - SCAN_W0) >> 2;      // column part of this warp
         const int row = g * 32 + lane;
-        const int thr = half * ROWS + row;
-        const int col0 = half * (I8_TILE / 2);
+        const int thr = colq * ROWS + row;
+        const int col0 = colq * (I8_TILE / NCOL);
         const uint32_t t_lane = tmem_base + ((uint32_t)(g * 32) << 16);
         const bool ragged = (np_ % I8_TILE) != 0;
         const int cap = prm.cap;
@@ -320,14 +350,14 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
             while (!mbar_try_hint(smem_u32(&tfull[buf]), (gt >> 1) & 1u)) {}
             if (STATS) sw_wait += clock64() - sw_a;
             tc_fence_after();
-            uint32_t va[32], vb[32];
+            uint32_t va[32], vb[NLD == 2 ? 32 : 1];
             const uint32_t tbase = t_lane + buf * I8_TILE + col0;
             if (STATS && (prm.experiment & 8)) {
 #pragma unroll
-                for (int e = 0; e < 32; e++) { va[e] = 0x00010001u * (uint32_t)(e + lane); vb[e] = va[e]; }
+                for (int e = 0; e < 32; e++) { va[e] = 0x00010001u * (uint32_t)(e + lane); if (NLD == 2) vb[e] = va[e]; }
             } else {
                 TC_LD32P(tbase, va);
-                TC_LD32P(tbase + 64, vb);
+                if constexpr (NLD == 2) TC_LD32P(tbase + 64, vb);
             }
             // the row's control word, then the other half's published minimum (in this
             // order: a new control word implies the reset of the minimum is visible)
@@ -347,11 +377,17 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
 #pragma unroll
                 for (int e = 0; e < 32; e++) {
                     mask(va[e], pa + 2 * e);
-                    mask(vb[e], pa + 64 + 2 * e);
+                    if constexpr (NLD == 2) mask(vb[e], pa + 64 + 2 * e);
                 }
             }
-            // minima of the thread's four 32-pattern groups (16 packed registers each)
-            const int m0 = min32_s16(va, 0), m1 = min32_s16(va, 16), m2 = min32_s16(vb, 0), m3 = min32_s16(vb, 16);
+            // minima of the thread's 32-pattern groups (16 packed registers each)
+            int mg[NGRP];
+            mg[0] = min32_s16(va, 0);
+            mg[1] = min32_s16(va, 16);
+            if constexpr (NLD == 2) {
+                mg[2] = min32_s16_b(vb, 0);
+                mg[3] = min32_s16_b(vb, 16);
+            }
             const bool isnew = ctl.x != seen;
             seen = ctl.x;
             // a new cycle: counters reset, the running minimum starts from the seed
@@ -362,7 +398,8 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
             trap_if(isnew && gt > ctl.x);   // the start tile was observed late: protocol violation, fail the launch
             const uint32_t age = gt - seen;
             const bool live = age < (uint32_t)ntiles;
-            const int mt = min(min(m0, m1), min(m2, m3));
+            int mt = min(mg[0], mg[1]);
+            if constexpr (NLD == 2) mt = min(mt, min(mg[2], mg[3]));
             m_run = live ? min(m_run, min(mt, shb)) : m_run;
             const int lim = m_run + wq;
             const uint32_t grp0 = (uint32_t)pa >> 5;
@@ -371,10 +408,8 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
                 st_shared_if(hits_addr + (uint32_t)cnt * (SCAN_T * 4), ((uint32_t)(m + KEY_BIAS) << 16) | grp, h && cnt < cap);
                 cnt += h ? 1 : 0;
             };
-            record(m0, grp0);
-            record(m1, grp0 + 1u);
-            record(m2, grp0 + 2u);
-            record(m3, grp0 + 3u);
+#pragma unroll
+            for (int k = 0; k < NGRP; k++) record(mg[k], grp0 + (uint32_t)k);
             const bool lower = live && mt < pub;
             red_min_shared_if(best_addr, mt, lower);
             pub = lower ? mt : pub;
@@ -384,7 +419,7 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
                 if (STATS) st_entries += cnt;
                 hit_cnt[thr] = (uint8_t)min(cnt, 255);
                 __threadfence_block();
-                if (atomicAdd(&row_done[row], 1) == 1) atomicOr(&ready_mask[row >> 5], 1u << (row & 31));   // both halves done
+                if (atomicAdd(&row_done[row], 1) == NCOL - 1) atomicOr(&ready_mask[row >> 5], 1u << (row & 31));   // all parts done
             }
             if (++j == ntiles) j = 0;
         }
@@ -398,7 +433,8 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
             }
         }
     } else {
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 120;");
+        if (NCOL == 4) asm volatile("setmaxnreg.inc.sync.aligned.u32 104;");
+        else asm volatile("setmaxnreg.inc.sync.aligned.u32 120;");
         // ===== workers: any worker takes any ready row (a bit mask of rows whose cycle
         // ended); the row's state lives in shared memory between its cycles
         const int w = warp - WORK_W0;
@@ -433,7 +469,7 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
             }
         };
         refill_pocket();
-        unsigned long long st_rowcyc = 0, st_chunks = 0, st_f64 = 0, st_ovf = 0, st_busy = 0, st_fin = 0;
+        unsigned long long st_rowcyc = 0, st_chunks = 0, st_f64 = 0, st_ovf = 0, st_busy = 0, st_fin = 0, st_dead = 0;
         long long ph[6] = {0, 0, 0, 0, 0, 0}, t_ph = 0;
 #define PH(k) if (STATS) { const long long t_ = clock64(); ph[k] += t_ - t_ph; t_ph = t_; }
         for (;;) {
@@ -442,7 +478,8 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
             const int wi_l = (lane + w) & 3;
             const uint32_t mw = lane < 4 ? ld_shared_volatile_u32(ready_mask + wi_l) : 0u;
             const unsigned has = __ballot_sync(MPW_FULL, mw != 0u);
-            if (!has) { __nanosleep(100); continue; }
+            // (workers on the MMA issuers' schedulers, warps 1 and 2 mod 4, yield to the others)
+            if (!has) { __nanosleep(((warp & 3) == 1 || (warp & 3) == 2) ? MPW_AR_BACKOFF : 100); continue; }
             long long t_busy0 = 0;
             if (STATS) { t_busy0 = clock64(); t_ph = t_busy0; }
             const int srcl = __ffs(has) - 1;
@@ -488,12 +525,19 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
                 uint2* const qptr = reinterpret_cast<uint2*>(a_rows + (lane >> 4) * A_KBLK_BYTES +
                                                              sw128_chunk(row, (lane & 15) >> 1) + (lane & 1) * 8);
                 const int mfin = ld_shared_volatile(&row_best[row]);
-                const int cnt0 = hit_cnt[row], cnt1 = hit_cnt[ROWS + row];
+                int cntq[NCOL];
+                uint32_t entq[NCOL];
                 const int hl = lane < CAP ? lane : 0;
-                const uint32_t ent0 = hits[hl * SCAN_T + row], ent1 = hits[hl * SCAN_T + ROWS + row];
+#pragma unroll
+                for (int q = 0; q < NCOL; q++) {
+                    cntq[q] = hit_cnt[q * ROWS + row];
+                    entq[q] = hits[hl * SCAN_T + q * ROWS + row];
+                }
                 uint2 q2 = make_uint2(0u, 0u);
                 if (pos_on) q2 = *qptr;
-                const bool ovf = cnt0 > prm.cap || cnt1 > prm.cap;
+                bool ovf = false;
+#pragma unroll
+                for (int q = 0; q < NCOL; q++) ovf = ovf || cntq[q] > prm.cap;
                 if (STATS) st_rowcyc++;
                 if (ovf && !recyc_) {
                     // hit list overflow: scan once more, recording only the groups inside
@@ -594,26 +638,40 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
                             }
                         }
                     };
-                    // the row's hit groups of both halves as one 64-bit mask over (half, list slot);
-                    // the next group's bytes are in flight while a group is scored
-                    const int c0 = min(cnt0, prm.cap), c1 = min(cnt1, prm.cap);
-                    unsigned long long mm =
-                        (unsigned long long)__ballot_sync(MPW_FULL, lane < c0 && (int)(ent0 >> 16) - KEY_BIAS < limit) |
-                        ((unsigned long long)__ballot_sync(MPW_FULL, lane < c1 && (int)(ent1 >> 16) - KEY_BIAS < limit) << 32);
-                    if (STATS && (prm.experiment & 2)) mm = 0ull;   // timing probe: no scoring
-                    auto group_at = [&](unsigned long long m) {
-                        const int idx = __ffsll((long long)m) - 1;
-                        const uint32_t e = __shfl_sync(MPW_FULL, idx & 32 ? ent1 : ent0, idx & 31);
-                        return (int)(e & 0xFFFFu);
+                    // the row's hit groups: per column part a mask over its list slots; the next
+                    // group's bytes are in flight while a group is scored
+                    uint32_t mq[NCOL];
+#pragma unroll
+                    for (int q = 0; q < NCOL; q++)
+                        mq[q] = __ballot_sync(MPW_FULL, lane < min(cntq[q], prm.cap) && (int)(entq[q] >> 16) - KEY_BIAS < limit);
+                    if (STATS && (prm.experiment & 2)) {   // timing probe: no scoring
+#pragma unroll
+                        for (int q = 0; q < NCOL; q++) mq[q] = 0u;
+                    }
+                    // first pending (part, slot): its group, -1 if none; pop() removes it
+                    auto peek = [&]() -> int {
+                        int g = -1;
+#pragma unroll
+                        for (int q = NCOL - 1; q >= 0; q--)
+                            if (mq[q]) g = (int)(__shfl_sync(MPW_FULL, entq[q], __ffs(mq[q]) - 1) & 0xFFFFu);
+                        return g;
+                    };
+                    auto pop = [&]() {
+                        bool done = false;
+#pragma unroll
+                        for (int q = 0; q < NCOL; q++)
+                            if (!done && mq[q]) { mq[q] &= mq[q] - 1; done = true; }
                     };
                     uint4 n0, n1;
-                    if (mm) load_group(group_at(mm), n0, n1);
+                    int gnext = peek();
+                    if (gnext >= 0) load_group(gnext, n0, n1);
 #pragma unroll 1
-                    while (mm) {
-                        const int grp = group_at(mm);
-                        mm &= mm - 1;
+                    while (gnext >= 0) {
+                        const int grp = gnext;
+                        pop();
                         const uint4 t0 = n0, t1 = n1;
-                        if (mm) load_group(group_at(mm), n0, n1);
+                        gnext = peek();
+                        if (gnext >= 0) load_group(gnext, n0, n1);
                         do_group(grp, t0, t1);
                     }
                     PH(1);
@@ -764,6 +822,10 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
                     row_done[row] = 0;
                     __threadfence_block();
                     const uint32_t v = ld_shared_volatile_u32(issue_ctr);
+                    if (STATS) {
+                        const uint32_t prev = ld_shared_volatile_v2(&row_ctl[row]).x;
+                        if (prev != 0x80000000u) st_dead += (v + MARGIN) - (prev + (uint32_t)ntiles);
+                    }
                     st_shared_volatile_v2(&row_ctl[row],
                                           make_uint2(v + MARGIN, ((uint32_t)wq_ << 16) | (uint32_t)(seed + KEY_BIAS)));
                 }
@@ -781,6 +843,7 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
             atomicAdd(&prm.stats[ST_OVF], st_ovf);
             atomicAdd(&prm.stats[ST_BUSY], st_busy);
             atomicAdd(&prm.stats[ST_FINISHED], st_fin);
+            atomicAdd(&prm.stats[ST_DEAD], st_dead);
             for (int k = 0; k < 6; k++) atomicAdd(&prm.stats[ST_W_LIST + k], (unsigned long long)ph[k]);
         }
     }

@@ -221,8 +221,8 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
     const int n = prm.n, A = prm.A, T = prm.T, np_ = prm.np, ntiles = prm.ntiles;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < STAGES; s++) { mbar_init(smem_u32(&full[s]), 1); mbar_init(smem_u32(&empty[s]), 1); }
-        for (int b = 0; b < 2; b++) { mbar_init(smem_u32(&tfull[b]), 1); mbar_init(smem_u32(&tempty[b]), 4 * NCOL); }
+        for (int s = 0; s < STAGES; s++) { mbar_init(smem_u32(&empty[s]), 1); }
+        for (int b = 0; b < 2; b++) { mbar_init(smem_u32(&tfull[b]), 1); mbar_init(smem_u32(&tempty[b]), 4 * NCOL + 1); }   // tempty: the scan warps' releases + the producer's arrival with the tile's bytes
         *stop_tile = 0xFFFFFFFFu;
         *issue_ctr = 0u;
         *rows_left = ROWS;
@@ -256,15 +256,17 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
             uint32_t phase = 0;
             for (uint32_t gt = 0;; gt++) {
                 if (gt >= ld_shared_volatile_u32(stop_tile)) break;
+                // One barrier per accumulator collects what tile gt's MMAs wait for: the scan
+                // warps' releases of tile gt - 2 and both stages of tile gt.  Its previous phase
+                // (tile gt - 2) must be complete before this tile's arrival joins the next.
+                const uint32_t gb = smem_u32(&tempty[gt & 1u]);
+                if (gt >= 2) ar_wait(gb, (((gt >> 1) & 1u) ^ 1u));
+                const bool probe = STATS && (prm.experiment & 4) && gt >= 4;   // timing probe: no P traffic
+                if (probe) mbar_arrive(gb);
+                else mbar_expect_tx(gb, KB * STB);
                 for (int kb = 0; kb < KB; kb++) {
                     ar_wait(smem_u32(&empty[stage]), phase ^ 1);
-                    const uint32_t fb = smem_u32(&full[stage]);
-                    if (STATS && (prm.experiment & 4) && gt >= 4) {
-                        mbar_arrive(fb);   // timing probe: no P traffic
-                    } else {
-                        mbar_expect_tx(fb, STB);
-                        bulk_g2s(smem_u32(b_ring + stage * STB), prm.btiles + ((size_t)j * KB + kb) * STB, STB, fb);
-                    }
+                    if (!probe) bulk_g2s(smem_u32(b_ring + stage * STB), prm.btiles + ((size_t)j * KB + kb) * STB, STB, gb);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
                 if (++j == ntiles) j = 0;
@@ -273,9 +275,10 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
       } else if (warp == 1 || (NISS == 2 && warp == 2)) {
         // ===== MMA issuers: one M128 N256 tile per step, K = 32 per instruction.  Two
         // threads (warps 1 and 2) take alternate tiles, each with its own accumulator:
-        // while one runs through the barrier checks of its next tile, the other's MMAs keep
+        // while one runs through the barrier check of its next tile, the other's MMAs keep
         // the tensor pipe fed (one thread alone leaves the pipe idle ~20 % of the time: its
-        // per-tile waits, fences and commits outlast the few MMAs the pipe can queue)
+        // per-tile waits, fences and commits outlast the few MMAs the pipe can queue).  A
+        // tile waits on one barrier only (the accumulator's: releases + the tile's bytes)
         if (lane == 0) {
             const uint32_t which = (uint32_t)(warp - 1);
             const uint32_t idesc = (2u << 4) | (1u << 7) | ((uint32_t)(I8_TILE >> 3) << 17) | ((uint32_t)(ROWS >> 4) << 24);
@@ -289,7 +292,7 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
                 if (gt >= ld_shared_volatile_u32(stop_tile)) break;
                 const uint32_t buf = gt & 1u;
                 if (STATS) t_a = clock64();
-                ar_wait(smem_u32(&tempty[buf]), ((gt >> 1) & 1u) ^ 1u);
+                ar_wait(smem_u32(&tempty[buf]), (gt >> 1) & 1u);
                 if (STATS) w_tempty += clock64() - t_a;
                 tc_fence_after();
                 // published (as a running maximum) before the tile's MMAs are issued: a
@@ -298,11 +301,7 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
                 const uint32_t d = tmem_base + buf * I8_TILE;
                 for (int kb = 0; kb < KB; kb++) {
                     const uint32_t u = gt * KB + kb;           // K-block number -> ring stage and phase
-                    const uint32_t stage = u % STAGES, phase = (u / STAGES) & 1u;
-                    if (STATS) t_a = clock64();
-                    ar_wait(smem_u32(&full[stage]), phase);
-                    if (STATS) w_full += clock64() - t_a;
-                    tc_fence_after();
+                    const uint32_t stage = u % STAGES;
                     const uint64_t bd = sw128_desc(bring + stage * STB);
                     const uint64_t ad = sw128_desc(abase + kb * A_KBLK_BYTES);
                     if (STATS) t_a = clock64();
@@ -336,6 +335,10 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
         const uint32_t t_lane = tmem_base + ((uint32_t)(g * 32) << 16);
         const bool ragged = (np_ % I8_TILE) != 0;
         const int cap = prm.cap;
+        if (lane == 0) {   // no release precedes the first two tiles: the scan warps arrive for them up front
+            mbar_arrive(smem_u32(&tempty[0]));
+            mbar_arrive(smem_u32(&tempty[1]));
+        }
         uint32_t seen = 0x80000000u;                 // start tile of the cycle this thread knows
         const uint32_t hits_addr = smem_u32(hits) + (uint32_t)thr * 4u, best_addr = smem_u32(&row_best[row]);
         int cnt = 0, m_run = Q_INF, pub = 0x7FFFFFFF, wq = 0;

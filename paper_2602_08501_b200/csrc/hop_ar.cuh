@@ -74,7 +74,7 @@ constexpr int Q_INF = 0x7FFF;                  // s16 maximum: "no score"
 #endif
 constexpr int NISS = MPW_AR_NISS;             // MMA issuer threads (alternate tiles)
 static_assert(NISS == 1 || NISS == 2, "one issuer per accumulator");
-constexpr int MARGIN = 1;                      // tiles between the issue counter read and a row's first live tile
+constexpr int MARGIN = 2;                      // tiles between the issue counter read and a row's first live tile
 static_assert(CAP <= 32, "one hit entry per worker lane");
 // a hit entry names a group of 32 patterns in 16 bits: |P| <= 2^17 gives 4096 groups
 
@@ -208,7 +208,6 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
     uint32_t* row_state = reinterpret_cast<uint32_t*>(hit_cnt + SCAN_T);    // [ROWS][RSW]: c[8], trajectory, frame, iters | flags | recyc, ed, err, inv_s, sum|y|, wq
     uint32_t* ready_mask = row_state + ROWS * RSW;                          // [4]: rows whose cycle ended (or that await their first trajectory)
     uint64_t* bars = reinterpret_cast<uint64_t*>(ready_mask + 4);
-    uint64_t* full = bars;
     uint64_t* empty = bars + STAGES;
     uint64_t* tfull = bars + 2 * STAGES;
     uint64_t* tempty = tfull + 2;
@@ -443,13 +442,12 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
         const int w = warp - WORK_W0;
         const int count = *prm.s2.count;
         const int ntraj = count * A;
-        // the worker's pocket: the next trajectory of the stage-2 queue, claimed ahead of
-        // its use (queue slot x anchor; short lists skip), its frame's y and anchor on
-        // their way into L2.  pk_tr: -1 queue exhausted
-        int pk_tr = -1, pk_frame = 0;
-        float4 pk_qs = make_float4(1.f, 1.f, 0.f, 0.f);
-        auto refill_pocket = [&]() {
-            int ntr = -1, nq = 0;
+        // next trajectory of the stage-2 queue (queue slot x anchor; short lists skip), claimed
+        // when a row needs one.  (Claiming ahead into a per-worker pocket saved ~1.5k cycles per
+        // trajectory but could strand the pocket of a worker that gets no more rows at the end.)
+        auto claim_next = [&](int& nq) -> int {
+            int ntr = -1;
+            nq = 0;
             if (lane == 0) {
                 for (;;) {
                     const int cand = atomicAdd(prm.s2.work_next, 1);
@@ -461,17 +459,9 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
                     break;
                 }
             }
-            ntr = __shfl_sync(MPW_FULL, ntr, 0);
             nq = __shfl_sync(MPW_FULL, nq, 0);
-            pk_tr = ntr;
-            if (ntr >= 0) {
-                pk_frame = prm.s2.frame[nq];
-                pk_qs = prm.s2.qscale[nq];
-                if (lane * 128 < n * 4) prefetch_l2(reinterpret_cast<const char*>(prm.y + (size_t)pk_frame * n) + lane * 128);
-                if (lane == 31) prefetch_l2(prm.s2.anchors + (size_t)ntr * NW);
-            }
+            return __shfl_sync(MPW_FULL, ntr, 0);
         };
-        refill_pocket();
         unsigned long long st_rowcyc = 0, st_chunks = 0, st_f64 = 0, st_ovf = 0, st_busy = 0, st_fin = 0, st_dead = 0;
         long long ph[6] = {0, 0, 0, 0, 0, 0}, t_ph = 0;
 #define PH(k) if (STATS) { const long long t_ = clock64(); ph[k] += t_ - t_ph; t_ph = t_; }
@@ -511,7 +501,6 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
             int seed = Q_INF;
             bool need_claim = tr_ < 0;
             bool exhausted_ = false;
-            bool used_pocket = false;
             if (tr_ >= 0) {
                 // the frame's y (this lane's 8 positions) is on its way while the hit lists are read
                 const float* yr = prm.y + (size_t)frame_ * n;
@@ -746,8 +735,9 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
             }
             PH(2);
             if (need_claim) {
-                tr_ = pk_tr;
-                if (pk_tr < 0) {
+                int nq;
+                tr_ = claim_next(nq);
+                if (tr_ < 0) {
                     exhausted_ = true;
                     if (lane == 0 && atomicSub(rows_left, 1) == 1) {
                         // the CTA's last row: everybody stops a few tiles past the issuer
@@ -755,11 +745,11 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
                         st_shared_volatile_u32(stop_tile, ld_shared_volatile_u32(issue_ctr) + 4u + STAGES);
                     }
                 } else {
-                    used_pocket = true;
-                    frame_ = pk_frame;
-                    inv_ = pk_qs.x;
-                    err_ = pk_qs.z;
-                    ay_ = pk_qs.w;
+                    frame_ = prm.s2.frame[nq];
+                    const float4 qs = prm.s2.qscale[nq];
+                    inv_ = qs.x;
+                    err_ = qs.z;
+                    ay_ = qs.w;
                     const uint32_t aw = lane < NW ? __ldg(prm.s2.anchors + (size_t)tr_ * NW + lane) : 0u;
                     float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
                     if (lane * 8 < n) {
@@ -834,7 +824,6 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
                 }
             }
             PH(4);
-            if (used_pocket) refill_pocket();   // after the row is live again
             PH(5);
             if (STATS) st_busy += clock64() - t_busy0;
         }

@@ -123,3 +123,33 @@ def test_auto_picks_the_async_hop_on_cfg4():
     cfg2 = configs.CONFIGS["cfg2"]
     code2, sph2 = code_and_sphere(cfg2)
     assert DeviceDecoder(code2, sph2).auto_variant == "tensor"
+
+
+def test_decisions_do_not_depend_on_timing():
+    """Rows start their cycles at whatever tile the MMA stream is at, so the same
+    frames decoded as one batch and as four batches meet different tile phases,
+    worker orders and hit-list contents.  Every trajectory's iterations_used and
+    every codeword must still be identical (1.2 million row cycles: a hazard
+    between a row image update and the first tile of the row's next cycle
+    showed up here at ~1e-5 per cycle before the issue counter update was made
+    to precede the MMA issue)."""
+    cfg = configs.CONFIGS["cfg4"]
+    code, sph = code_and_sphere(cfg)
+    sigma = cfg.sigma(code=code)
+    F = 16384
+    _, _, y = channel.bulk_inputs(code, 31, 0, 0, F, sigma)
+    dec = DeviceDecoder(code, sph)
+    args = (sigma, cfg.list_size, cfg.num_paths, cfg.max_iterations, cfg.activation_mode)
+    one = dec.two_stage_batch(y, *args, variant="tensor_i8a")
+    it1, b1 = _np(one["iters"]).copy(), _np(one["best"]).copy()
+    parts = [dec.two_stage_batch(y[k:k + F // 4], *args, variant="tensor_i8a") for k in range(0, F, F // 4)]
+    it4 = np.concatenate([_np(p["iters"]) for p in parts])
+    b4 = np.concatenate([_np(p["best"]) for p in parts])
+    np.testing.assert_array_equal(it1, it4)
+    np.testing.assert_array_equal(b1, b4)
+    # and both equal the synchronous int8 screen (a different kernel with the same exact decisions)
+    ref = dec.two_stage_batch(y, *args, variant="tensor_i8")
+    flags = _np(ref["flags"]) | _np(one["flags"])
+    ok = np.flatnonzero((flags & (UNRESOLVED | TIE_FINAL)) == 0)
+    np.testing.assert_array_equal(it1[ok], _np(ref["iters"])[ok])
+    np.testing.assert_array_equal(b1[ok], _np(ref["best"])[ok])

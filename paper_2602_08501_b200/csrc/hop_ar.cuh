@@ -683,7 +683,23 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
                         // float64 scores of the finalists (ascending positions), one per lane
                         if (STATS) st_f64++;
                         double e = CUDART_INF;
-                        if (keep) e = exact_score<NW>(yr, c_, prm.pbits + (size_t)fi * NW, NW, n);
+                        if (keep) {
+                            // rolled loops (same ascending-position sum as exact_score in common.cuh):
+                            // this path decides 0.1 % of the row cycles, and its unrolled form was
+                            // half of the kernel's code
+                            e = 0.0;
+                            const uint32_t* pb = prm.pbits + (size_t)fi * NW;
+#pragma unroll 1
+                            for (int wd = 0; wd < NW; wd++) {
+                                const uint32_t cwd = select_word<NW>(c_, wd);
+#pragma unroll 1
+                                for (uint32_t b = __ldg(pb + wd); b; b &= b - 1) {
+                                    const int i = __ffs(b) - 1;
+                                    const double yi = (double)__ldg(yr + wd * 32 + i);
+                                    e += ((cwd >> i) & 1u) ? -yi : yi;
+                                }
+                            }
+                        }
                         double be = e;
                         int bi = keep ? fi : 0x7FFFFFFF;
 #pragma unroll

@@ -184,7 +184,7 @@ __device__ __forceinline__ void ar_wait(uint32_t bar, uint32_t parity) {
 }
 
 #ifndef MPW_AR_BACKOFF
-#define MPW_AR_BACKOFF 3000
+#define MPW_AR_BACKOFF 1000
 #endif
 
 // stats slots

@@ -183,7 +183,11 @@ int mpw_set_timing(mpw_handle* h, int enable);
  * tensor-hop variants for A/B runs and tests: "i8_cluster" (2 = CTA pairs
  * sharing the P stream), "i8_pair" (1 = cta_group::2 pair MMAs), "f16_cluster"
  * (0 = single CTAs for the 1-limb N = 256 shape), "hop_experiment" (profiling
- * and test bits of the hop kernel, e.g. 2048 = int8 window overflow at 4 keys). */
+ * and test bits of the hop kernels, e.g. 2048 = int8 window overflow at 4 keys;
+ * for the asynchronous-row hop: 32 = cycles per tile of the production kernel
+ * on stderr, other non-zero values = the instrumented build), "ar_hit_cap"
+ * (asynchronous-row hop: hit-list entries per scan thread and cycle, 0 = the
+ * compiled maximum; small values force the re-scan path in tests). */
 int mpw_set_option(mpw_handle* h, const char* key, int value);
 int mpw_read_timing(mpw_handle* h, double* ms_out, long long* launches_out, int reset);
 

@@ -14,20 +14,23 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-OBJ = os.path.join(ROOT, "paper_2602_08501_b200", "csrc", "build", "hop_tc.o")
+OBJS = [os.path.join(ROOT, "paper_2602_08501_b200", "csrc", "build", o) for o in ("hop_ar.o", "hop_tc.o")]
 KEYS = ("UTCIMMA", "UTCHMMA", "UTCQMMA", "UTCBAR", "LDTM", "STTM", "UBLKCP", "UTMALDG", "SYNCS",
-        "VIMNMX3", "FMNMX3", "LDL", "STL")
+        "USETMAXREG", "IDP", "VIMNMX3", "FMNMX3", "LDL", "STL")
 
 
 def demangle(name):
     m = re.match(r"_ZN2tc13hop_tc_kernelILi(\d+)ELi(\d+)ELi(\d+)ELi(\d+)ELi(\d+)ELi(\d+)EEEvNS_6ParamsE", name)
+    a = re.match(r"_ZN2ar13hop_ar_kernelILi(\d+)ELi(\d+)ELb([01])EEEvNS_6ParamsE", name)
+    if a:
+        return f"hop_ar_kernel<KB={a.group(1)},NW={a.group(2)},STATS={a.group(3)}>"
     if not m:
         return name
     kb, nw, limbs, mode, cl, pm = map(int, m.groups())
     return f"hop_tc_kernel<KB={kb},NW={nw},LIMBS={limbs},MODE={mode},CL={cl},PM={pm}>"
 
 
-def main():
+def census(OBJ):
     sass = subprocess.run(["cuobjdump", "-sass", OBJ], capture_output=True, text=True, check=True).stdout
     res = subprocess.run(["cuobjdump", "--dump-resource-usage", OBJ], capture_output=True, text=True,
                          check=True).stdout
@@ -43,7 +46,11 @@ def main():
             if op in counts:
                 counts[op] += 1
         out[demangle(name)] = dict(instructions=len(ops), **counts, **usage.get(name, {}))
-    json.dump({"object": os.path.relpath(OBJ, ROOT), "kernels": out}, sys.stdout, indent=1)
+    return out
+
+
+def main():
+    json.dump({"objects": {os.path.relpath(o, ROOT): census(o) for o in OBJS}}, sys.stdout, indent=1)
     print()
 
 

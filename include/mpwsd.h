@@ -63,7 +63,7 @@ extern "C" {
 #define MPW_HOP_TENSOR 2  /* tcgen05, one fp16 limb of t, certified top-6 */
 #define MPW_HOP_TENSOR_2LIMB 3 /* tcgen05, fp16 hi+lo limbs of t, certified top-6 */
 #define MPW_HOP_TENSOR_I8 4 /* tcgen05 kind::i8, per-frame int8 quantisation of t, certified top-14 (N = 128, 256) */
-#define MPW_HOP_TENSOR_I8_ASYNC 5 /* kind::i8 with asynchronous rows: continuous P stream, chunk-minimum scan, worker-warp decisions (N = 128, 256) */
+#define MPW_HOP_TENSOR_I8_ASYNC 5 /* kind::i8 with asynchronous rows: continuous P stream, group-minimum scan, worker-warp decisions (N = 128, 256; float32 and float64 received words) */
 
 /* counters (int64, accumulated by mpw_two_stage_batch; caller zeroes) */
 #define MPW_CTR_FRAMES 0

@@ -5,11 +5,14 @@
 #include "hop_ar.cuh"
 #include "hop_tc_api.h"
 
-static float ar_cert_gamma(int wmax) {
-    // any summation order of at most wmax terms: |fl(S) - S| <= gamma_{wmax-1} sum|t_i|
+static float ar_cert_gamma(int wmax, bool y64) {
+    // any summation order of at most wmax terms: |fl(S) - S| <= gamma_{wmax-1} sum|t_i|;
+    // with float64 inputs the fp32 rounding of y adds u sum|y|
     const double u = 5.9604644775390625e-8;
     const double k = wmax > 1 ? wmax - 1 : 0;
-    return (float)(k * u / (1.0 - k * u) * 1.002);
+    double g = k * u / (1.0 - k * u);
+    if (y64) g += u;
+    return (float)(g * 1.002);
 }
 
 bool ar_supported(const TcPatterns& t, int n) {
@@ -18,14 +21,14 @@ bool ar_supported(const TcPatterns& t, int n) {
 }
 
 template <int KB, int NW, bool STATS>
-static int ar_launch_t(const TcPatterns& t, int n, int A, int T, const float* y, S2Dev s2, PatDev P, int num_sms,
+static int ar_launch_t(const TcPatterns& t, int n, int A, int T, const float* y, const double* y64, S2Dev s2, PatDev P, int num_sms,
                        int experiment, int hit_cap, cudaStream_t st) {
     ar::Params prm;
     prm.n = n; prm.nw = NW; prm.A = A; prm.T = T; prm.np = t.np; prm.ntiles = t.ntiles8;
-    prm.y = y; prm.s2 = s2; prm.pbits = P.bits; prm.pbT = t.pbT; prm.btiles = t.tiles8;
+    prm.y = y; prm.y64 = y64; prm.s2 = s2; prm.pbits = P.bits; prm.pbT = t.pbT; prm.btiles = t.tiles8;
     prm.tie_rel = 1e-5f;
     prm.cap = hit_cap > 0 && hit_cap < ar::CAP ? hit_cap : ar::CAP;
-    prm.cert_g = ar_cert_gamma(s2.wmax);
+    prm.cert_g = ar_cert_gamma(s2.wmax, y64 != nullptr);
     prm.stats = nullptr;
     prm.experiment = 0;
     prm.tilestat = nullptr;
@@ -84,13 +87,13 @@ static int ar_launch_t(const TcPatterns& t, int n, int A, int T, const float* y,
     return 0;
 }
 
-int ar_launch(const TcPatterns& t, int n, int nw, int A, int T, const float* y, S2Dev s2, PatDev P, int num_sms,
-              const TcOpts& o, cudaStream_t st) {
+int ar_launch(const TcPatterns& t, int n, int nw, int A, int T, const float* y, const double* y64, S2Dev s2, PatDev P,
+              int num_sms, const TcOpts& o, cudaStream_t st) {
     if (!ar_supported(t, n) || nw != n / 32) return 1;
     const bool stats = o.experiment != 0 && o.experiment != 32;
     if (n == 256)
-        return stats ? ar_launch_t<2, 8, true>(t, n, A, T, y, s2, P, num_sms, o.experiment, o.ar_hit_cap, st)
-                     : ar_launch_t<2, 8, false>(t, n, A, T, y, s2, P, num_sms, o.experiment, o.ar_hit_cap, st);
-    return stats ? ar_launch_t<1, 4, true>(t, n, A, T, y, s2, P, num_sms, o.experiment, o.ar_hit_cap, st)
-                 : ar_launch_t<1, 4, false>(t, n, A, T, y, s2, P, num_sms, o.experiment, o.ar_hit_cap, st);
+        return stats ? ar_launch_t<2, 8, true>(t, n, A, T, y, y64, s2, P, num_sms, o.experiment, o.ar_hit_cap, st)
+                     : ar_launch_t<2, 8, false>(t, n, A, T, y, y64, s2, P, num_sms, o.experiment, o.ar_hit_cap, st);
+    return stats ? ar_launch_t<1, 4, true>(t, n, A, T, y, y64, s2, P, num_sms, o.experiment, o.ar_hit_cap, st)
+                 : ar_launch_t<1, 4, false>(t, n, A, T, y, y64, s2, P, num_sms, o.experiment, o.ar_hit_cap, st);
 }

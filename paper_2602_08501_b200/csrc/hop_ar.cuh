@@ -81,6 +81,7 @@ static_assert(CAP <= 32, "one hit entry per worker lane");
 struct Params {
     int n, nw, A, T, np, ntiles;
     const float* y;
+    const double* y64;           // float64 inputs: the caller's received words (y = their fp32 rounding), else null
     S2Dev s2;
     const uint32_t* pbits;       // np x nw
     const uint4* pbT;            // bits transposed for the workers: [group of 32 patterns][n / 8 position bytes][32 patterns]
@@ -695,7 +696,8 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
 #pragma unroll 1
                                 for (uint32_t b = __ldg(pb + wd); b; b &= b - 1) {
                                     const int i = __ffs(b) - 1;
-                                    const double yi = (double)__ldg(yr + wd * 32 + i);
+                                    const double yi = prm.y64 ? __ldg(prm.y64 + (size_t)frame_ * n + wd * 32 + i)
+                                                              : (double)__ldg(yr + wd * 32 + i);
                                     e += ((cwd >> i) & 1u) ? -yi : yi;
                                 }
                             }

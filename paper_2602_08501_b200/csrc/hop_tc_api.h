@@ -44,5 +44,6 @@ int tc_launch(const TcPatterns& t, int n, int nw, int A, int T, const float* y, 
 // warps decide; needs the u8 images of TcPatterns.
 // o.experiment != 0 launches the statistics build (one line on stderr per launch).
 bool ar_supported(const TcPatterns& t, int n);
-int ar_launch(const TcPatterns& t, int n, int nw, int A, int T, const float* y, S2Dev s2, PatDev P, int num_sms,
-              const TcOpts& o, cudaStream_t st);
+// y64 (may be null): the caller's float64 received words, y their fp32 rounding.
+int ar_launch(const TcPatterns& t, int n, int nw, int A, int T, const float* y, const double* y64, S2Dev s2, PatDev P,
+              int num_sms, const TcOpts& o, cudaStream_t st);

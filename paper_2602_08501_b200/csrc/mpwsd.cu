@@ -276,13 +276,17 @@ __global__ void frame_kernel(FrameArgs fa) {
 // (warp per frame: also the per-frame score error bounds the hop kernels use)
 // float64 inputs: every screen bound also covers sum_{supp}|y64_i - y_i| <=
 // the sum of the wmax largest fp32 rounding errors of the frame
-__device__ __forceinline__ float4 widen_for_y64(float4 eb, const float* __restrict__ yrow,
-                                                const double* __restrict__ y64row, int n, int wmax) {
+__device__ __forceinline__ float y64_rounding_bound(const float* __restrict__ yrow, const double* __restrict__ y64row,
+                                                    int n, int wmax) {
     float r[32];
     int cnt = 0;
     for (int i = threadIdx.x & 31; i < n; i += 32, cnt++)
         r[cnt] = __double2float_ru(fabs(y64row[i] - (double)yrow[i]));
-    const float R = warp_topw_bound(r, cnt, wmax);
+    return warp_topw_bound(r, cnt, wmax);
+}
+__device__ __forceinline__ float4 widen_for_y64(float4 eb, const float* __restrict__ yrow,
+                                                const double* __restrict__ y64row, int n, int wmax) {
+    const float R = y64_rounding_bound(yrow, y64row, n, wmax);
     return make_float4(eb.x + R, eb.y + R, eb.z + R, eb.w);
 }
 
@@ -294,7 +298,8 @@ __global__ void queue_identity_kernel(int F, int A, int n, const float* __restri
     if (q < F) {
         float4 eb = warp_error_bounds(y + (size_t)q * n, n, s2.wmax);
         if (y64) eb = widen_for_y64(eb, y + (size_t)q * n, y64 + (size_t)q * n, n, s2.wmax);
-        const float4 qs = warp_i8_scale(y + (size_t)q * n, n, s2.wmax);
+        float4 qs = warp_i8_scale(y + (size_t)q * n, n, s2.wmax);
+        if (y64) qs.z += y64_rounding_bound(y + (size_t)q * n, y64 + (size_t)q * n, n, s2.wmax);   // int8 screen of fp32(y64)
         if (lane == 0) {
             s2.frame[q] = q;
             s2.nanchor[q] = nanchor ? min(nanchor[q], A) : A;
@@ -313,7 +318,8 @@ __global__ void ebound_kernel(int n, const float* __restrict__ y, const double* 
         const float* yr = y + (size_t)s2.frame[q] * n;
         float4 eb = warp_error_bounds(yr, n, s2.wmax);
         if (y64) eb = widen_for_y64(eb, yr, y64 + (size_t)s2.frame[q] * n, n, s2.wmax);
-        const float4 qs = warp_i8_scale(yr, n, s2.wmax);
+        float4 qs = warp_i8_scale(yr, n, s2.wmax);
+        if (y64) qs.z += y64_rounding_bound(yr, y64 + (size_t)s2.frame[q] * n, n, s2.wmax);   // int8 screen of fp32(y64)
         if (lane == 0) { s2.ebound[q] = eb; s2.qscale[q] = qs; }
     }
 }
@@ -458,13 +464,16 @@ int launch_gather(mpw_handle* h, HopParams hp, int max_traj, cudaStream_t st) {
 // its wider certification window (N = 256 and >= 32 tiles of 256 patterns), in
 // its asynchronous-row form (hop_ar.cuh: cfg4 82 ms against 107 ms for the
 // synchronous rounds of hop_tc.cuh); else one fp16 limb, else the gather kernel
-// float64 inputs (f64): the 1-limb fp16 screen with float64 re-scoring, else
-// the gather kernel
+// float64 inputs (f64): the asynchronous-row int8 hop where it applies (its
+// workers re-score from the float64 words), else the 1-limb fp16 screen with
+// float64 re-scoring, else the gather kernel
 int resolve_variant(mpw_handle* h, int variant, bool f64 = false) {
     if (variant != MPW_HOP_AUTO) return variant;
     if (!(tc_supported(h->n, h->np) && h->tcp.ready)) return MPW_HOP_GATHER;
-    if (!f64 && h->tcp.ready8 && h->n >= 256 && h->tcp.ntiles >= 32)
-        return ar_supported(h->tcp, h->n) ? MPW_HOP_TENSOR_I8_ASYNC : MPW_HOP_TENSOR_I8;
+    if (h->tcp.ready8 && h->n >= 256 && h->tcp.ntiles >= 32) {
+        if (ar_supported(h->tcp, h->n)) return MPW_HOP_TENSOR_I8_ASYNC;   // float32 and float64 received words
+        if (!f64) return MPW_HOP_TENSOR_I8;
+    }
     return MPW_HOP_TENSOR;
 }
 
@@ -472,12 +481,11 @@ int run_hops(mpw_handle* h, const float* y, const double* y64, int Fmax, int A, 
              cudaStream_t st) {
     variant = resolve_variant(h, variant, y64 != nullptr);
     if (y64 && (variant == MPW_HOP_TENSOR_2LIMB || variant == MPW_HOP_TENSOR_I8))
-        return fail(MPW_ERR_UNSUPPORTED, "float64 received words use the 1-limb tensor or the gather hop");
+        return fail(MPW_ERR_UNSUPPORTED, "float64 received words use the asynchronous-row int8, the 1-limb tensor or the gather hop");
     if (variant == MPW_HOP_TENSOR_I8_ASYNC) {
-        if (y64) return fail(MPW_ERR_UNSUPPORTED, "float64 received words use the 1-limb tensor or the gather hop");
         if (!ar_supported(h->tcp, h->n))
             return fail(MPW_ERR_UNSUPPORTED, "asynchronous int8 tensor-core hop needs N = 128 or 256 and the u8 operand images");
-        int rc = ar_launch(h->tcp, h->n, h->nw, A, T, y, s2, pat_dev(h), h->num_sms, h->tco, st);
+        int rc = ar_launch(h->tcp, h->n, h->nw, A, T, y, y64, s2, pat_dev(h), h->num_sms, h->tco, st);
         if (rc) return fail(MPW_ERR_CUDA, "asynchronous tensor-core hop launch failed: %s",
                             rc < 0 ? cudaGetErrorString((cudaError_t)-rc) : "unsupported shape");
         h->kernel_launches++;

@@ -153,3 +153,29 @@ def test_decisions_do_not_depend_on_timing():
     ok = np.flatnonzero((flags & (UNRESOLVED | TIE_FINAL)) == 0)
     np.testing.assert_array_equal(it1[ok], _np(ref["iters"])[ok])
     np.testing.assert_array_equal(b1[ok], _np(ref["best"])[ok])
+
+
+def test_float64_received_words_through_the_async_hop():
+    """float64 received words (what the reference's functions coerce to) through
+    the asynchronous-row hop: the int8 screen runs on fp32(y) with the window
+    widened by the rounding, the workers' fp32 bound covers it and the float64
+    re-scoring reads the float64 words.  Decisions must equal the 1-limb tensor
+    hop's float64 path (pinned against the reference's float64 goldens) on
+    words that are not float32-representable."""
+    cfg = configs.CONFIGS["cfg4"]
+    code, sph = code_and_sphere(cfg)
+    sigma = cfg.sigma(code=code)
+    F = 512
+    _, _, y32 = channel.bulk_inputs(code, 41, 0, 0, F, sigma)
+    rng = np.random.default_rng(41)
+    y = y32.astype(np.float64) + rng.uniform(-1e-9, 1e-9, size=y32.shape)
+    dec = DeviceDecoder(code, sph)
+    args = (sigma, cfg.list_size, cfg.num_paths, cfg.max_iterations, cfg.activation_mode)
+    a = dec.two_stage_batch(y, *args, variant="tensor_i8a")
+    b = dec.two_stage_batch(y, *args, variant="tensor")
+    flags = _np(a["flags"]) | _np(b["flags"])
+    ok = np.flatnonzero((flags & (UNRESOLVED | TIE_FINAL)) == 0)
+    assert len(ok) >= F - F // 50
+    np.testing.assert_array_equal(_np(a["best"])[ok], _np(b["best"])[ok])
+    np.testing.assert_array_equal(_np(a["iters"])[ok], _np(b["iters"])[ok])
+    np.testing.assert_allclose(_np(a["best_ed"])[ok], _np(b["best_ed"])[ok], rtol=1e-13)

@@ -123,7 +123,8 @@ int mpw_mpwsd_batch(mpw_handle* h, const float* y, const uint32_t* anchors, cons
                     int32_t* iters, int32_t* hops, uint8_t* flags, void* stream);
 /* Same with float64 received words (F x n): the screens run on their fp32
  * rounding with error bounds widened by the rounding, every exact re-scoring
- * and reported ED uses the float64 values (variant AUTO, TENSOR or GATHER). */
+ * and reported ED uses the float64 values (variant AUTO, TENSOR_I8_ASYNC, TENSOR
+ * or GATHER). */
 int mpw_mpwsd_batch_f64(mpw_handle* h, const double* y, const uint32_t* anchors, const int32_t* n_anchor,
                         int F, int A, int T, int variant, uint32_t* best, double* best_ed,
                         int32_t* iters, int32_t* hops, uint8_t* flags, void* stream);

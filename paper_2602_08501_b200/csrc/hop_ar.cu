@@ -1,6 +1,7 @@
 // Asynchronous-row int8 tensor hop: host side (launch, statistics).
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 
 #include "hop_ar.cuh"
 #include "hop_tc_api.h"
@@ -16,7 +17,7 @@ static float ar_cert_gamma(int wmax, bool y64) {
 }
 
 bool ar_supported(const TcPatterns& t, int n) {
-    // u8 images present (|P| <= 2^17, 127 wmax < 8192), 64-pattern chunk ids fit 16 bits
+    // u8 images present (|P| <= 2^17, 127 wmax < 8192), 32-pattern group ids fit 16 bits
     return t.ready8 && t.pbT && (n == 128 || n == 256) && t.np <= (1 << 17);
 }
 
@@ -32,6 +33,11 @@ static int ar_launch_t(const TcPatterns& t, int n, int A, int T, const float* y,
     prm.stats = nullptr;
     prm.experiment = 0;
     prm.tilestat = nullptr;
+    // statistics buffers (instrumented / hop_experiment = 32 launches only) are shared by all
+    // handles of the process: such launches are serialised
+    static std::mutex stat_mutex;
+    std::unique_lock<std::mutex> stat_lock(stat_mutex, std::defer_lock);
+    if (STATS || experiment == 32) stat_lock.lock();
     static unsigned long long* tilestat = nullptr;
     if (experiment == 32) {   // light statistic of the production kernel: cycles per tile
         if (!tilestat && cudaMallocManaged(&tilestat, 2 * sizeof(unsigned long long)) != cudaSuccess) return -1;

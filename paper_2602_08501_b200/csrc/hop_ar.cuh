@@ -333,7 +333,6 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
         const int thr = colq * ROWS + row;
         const int col0 = colq * (I8_TILE / NCOL);
         const uint32_t t_lane = tmem_base + ((uint32_t)(g * 32) << 16);
-        const bool ragged = (np_ % I8_TILE) != 0;
         const int cap = prm.cap;
         if (lane == 0) {   // no release precedes the first two tiles: the scan warps arrive for them up front
             mbar_arrive(smem_u32(&tempty[0]));
@@ -372,17 +371,7 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
             __syncwarp();
             if (lane == 0) mbar_arrive(smem_u32(&tempty[buf]));
             const int pa = j * I8_TILE + col0;
-            if (ragged && j == ntiles - 1) {
-                auto mask = [&](uint32_t& r, int p) {   // s16 maximum past |P|
-                    if (p >= np_) r = (r & 0xFFFF0000u) | 0x7FFFu;
-                    if (p + 1 >= np_) r = (r & 0xFFFFu) | 0x7FFF0000u;
-                };
-#pragma unroll
-                for (int e = 0; e < 32; e++) {
-                    mask(va[e], pa + 2 * e);
-                    if constexpr (NLD == 2) mask(vb[e], pa + 64 + 2 * e);
-                }
-            }
+            // (no tail mask: the image columns past |P| repeat pattern 0, hop_tc.cu tc_build8)
             // minima of the thread's 32-pattern groups (16 packed registers each)
             int mg[NGRP];
             mg[0] = min32_s16(va, 0);

@@ -55,8 +55,12 @@ static int tc_build8(TcPatterns& t, const uint32_t* bits, int np, int n, int nw)
     const int ntiles = (np + tc::I8_TILE - 1) / tc::I8_TILE;
     const size_t bytes = (size_t)ntiles * kb * tc::I8_STAGE_BYTES;
     std::vector<uint8_t> img(bytes, 0);
-    for (int p = 0; p < np; p++) {
-        const int j = p / tc::I8_TILE, r = p % tc::I8_TILE;
+    // the columns of the last tile past |P| repeat pattern 0: their scores are those of a real
+    // pattern, so they never change a minimum and the asynchronous-row scan needs no tail mask
+    // (its workers ignore pattern indices >= |P|; the synchronous screen masks the tail itself)
+    for (int pp = 0; pp < ntiles * tc::I8_TILE; pp++) {
+        const int p = pp < np ? pp : 0;
+        const int j = pp / tc::I8_TILE, r = pp % tc::I8_TILE;
         for (int i = 0; i < n; i++) {
             if (!((bits[(size_t)p * nw + (i >> 5)] >> (i & 31)) & 1u)) continue;
             const int k = i / 128, col = i % 128;

@@ -62,6 +62,11 @@ def _micro_peaks():
         return {"i8": 16384.0, "f16": 8192.0, "smem": 128.0, "sms": 148, "source": "nominal per-clock rates"}
 
 
+def _num_sms():
+    import torch
+    return torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+
+
 def _ncu_traffic(key):
     """DRAM bytes (read + write) per launch of the dominant kernel from one
     committed `ncu --set full` capture of the same command
@@ -323,6 +328,7 @@ def run_ours(args, cfg, code, sph, sigma, backend: str = "nccl", device_index=No
     counters.zero_()
     dec.set_timing(True)
     dec.read_timing(reset=True)
+    dec.hop_tile_stats(reset=True)
     launches0 = dec.launch_count
     clocks = ClockSampler(local)
     clocks.start()
@@ -342,6 +348,8 @@ def run_ours(args, cfg, code, sph, sigma, backend: str = "nccl", device_index=No
     ms = e0.elapsed_time(e1)
     launches = dec.launch_count - launches0
     kms, klaunch = dec.read_timing(reset=True)
+    hop_tiles, hop_cycles = dec.hop_tile_stats(reset=True)   # rank 0's own launches of the timed region
+    rank_scans = int(counters[3].item())
     dec.set_timing(False)
     ctr = counters.clone()
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
@@ -424,6 +432,15 @@ def run_ours(args, cfg, code, sph, sigma, backend: str = "nccl", device_index=No
                     "peak_source": f"measured kind::i8 rate {micro['i8']:.0f} ops/clk/SM ({micro['source']}) x "
                                    f"{micro['sms']} SMs x {mhz:.0f} MHz (median SM clock of the timed region)",
                     "frac_of_2x_bf16_burst": ach / (2.0 * peaks["bf16_tflops"])}
+            if asyn and hop_tiles:
+                # why frac is below the tensor pipe's activity: the pipe needs 1,024 cycles per
+                # 256-pattern tile of 128 rows, the kernel spends cycles_per_tile, and a row is
+                # live (inside a scan) only rows_live of its tiles (the MMA computes all 128 rows)
+                ntiles = (sph.nonzero_size + 255) // 256
+                roof["hop_detail"] = {"cycles_per_tile": hop_cycles / hop_tiles, "mma_cycles_per_tile": 1024,
+                                      "tiles_per_cta_per_step": hop_tiles / args.steps / _num_sms(),
+                                      "rows_live": rank_scans * ntiles / (hop_tiles * 128.0),
+                                      "source": "mpw_hop_tile_stats over the timed region (rank 0)"}
         elif variant_used in ("tensor", "tensor2"):
             limbs = 1 if variant_used == "tensor" else 2
             flop = evals / ws * 2.0 * limbs * code.n  # limbs x 2N FLOP per evaluation

@@ -191,6 +191,12 @@ int mpw_set_timing(mpw_handle* h, int enable);
  * compiled maximum; small values force the re-scan path in tests). */
 int mpw_set_option(mpw_handle* h, const char* key, int value);
 int mpw_read_timing(mpw_handle* h, double* ms_out, long long* launches_out, int reset);
+/* Asynchronous-row hop: out[0] = 256-pattern tiles streamed, out[1] = SM clock cycles of
+ * the streaming loop, both summed over the CTAs of every launch since the last reset
+ * (synchronises the device).  cycles / tiles against 1,024 (the MMA time of a tile) and
+ * scans x tiles-per-scan against tiles x 128 rows (the rows' live share) explain the
+ * bench's roofline fraction. */
+int mpw_hop_tile_stats(mpw_handle* h, unsigned long long* out, int reset);
 
 /* Device-side channel generator for bulk sweeps: frames [first_frame,
  * first_frame + F) of the counter-based Philox4x32-10 stream (seed, snr_idx):

@@ -47,6 +47,7 @@ _SIGS = {
     "mpw_set_timing": (c_int, [c_void_p, c_int]),
     "mpw_set_option": (c_int, [c_void_p, ctypes.c_char_p, c_int]),
     "mpw_read_timing": (c_int, [c_void_p, c_void_p, c_void_p, c_int]),
+    "mpw_hop_tile_stats": (c_int, [c_void_p, c_void_p, c_int]),
     "mpw_num_patterns": (c_int, [c_void_p]),
     "mpw_channel_batch": (c_int, [c_void_p, c_uint64, c_int, ctypes.c_longlong, c_int, c_double,
                                   c_void_p, c_void_p, c_void_p, c_void_p]),

@@ -32,7 +32,7 @@ static int ar_launch_t(const TcPatterns& t, int n, int A, int T, const float* y,
     prm.cert_g = ar_cert_gamma(s2.wmax, y64 != nullptr);
     prm.stats = nullptr;
     prm.experiment = 0;
-    prm.tilestat = nullptr;
+    prm.tilestat = t.ar_stat;   // accumulated over launches (mpw_hop_tile_stats)
     // statistics buffers (instrumented / hop_experiment = 32 launches only) are shared by all
     // handles of the process: such launches are serialised
     static std::mutex stat_mutex;
@@ -58,7 +58,7 @@ static int ar_launch_t(const TcPatterns& t, int n, int A, int T, const float* y,
     kern<<<num_sms, ar::THREADS, smem, st>>>(prm);
     e = cudaGetLastError();
     if (e != cudaSuccess) return -(int)e;
-    if (prm.tilestat) {
+    if (experiment == 32 && prm.tilestat == tilestat) {
         cudaStreamSynchronize(st);
         fprintf(stderr, "[hop_ar] production kernel: %.0f tiles per CTA, %.1f cycles per tile\n", (double)tilestat[0] / num_sms,
                 tilestat[0] ? (double)tilestat[1] / (double)tilestat[0] : 0.0);

@@ -35,6 +35,8 @@ void tc_release(TcPatterns& t) {
     if (t.tiles8) cudaFree(t.tiles8);
     if (t.pbT) cudaFree(t.pbT);
     t.pbT = nullptr;
+    if (t.ar_stat) cudaFree(t.ar_stat);
+    t.ar_stat = nullptr;
     t.tiles = nullptr;
     t.tiles8 = nullptr;
     t.ready = false;
@@ -80,6 +82,8 @@ static int tc_build8(TcPatterns& t, const uint32_t* bits, int np, int n, int nw)
             tr[((size_t)(p / 32) * nb + b) * 32 + (p % 32)] = (uint8_t)((bits[(size_t)p * nw + (b >> 2)] >> (8 * (b & 3))) & 0xFFu);
     if (cudaMalloc(&t.pbT, tr.size()) != cudaSuccess) return -1;
     if (cudaMemcpy(t.pbT, tr.data(), tr.size(), cudaMemcpyHostToDevice) != cudaSuccess) return -1;
+    if (cudaMalloc(&t.ar_stat, 2 * sizeof(unsigned long long)) != cudaSuccess) return -1;
+    if (cudaMemset(t.ar_stat, 0, 2 * sizeof(unsigned long long)) != cudaSuccess) return -1;
     return 0;
 }
 

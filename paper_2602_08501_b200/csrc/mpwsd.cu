@@ -1183,6 +1183,16 @@ int mpw_read_timing(mpw_handle* h, double* ms_out /*4*/, long long* launches_out
     return 0;
 }
 
+int mpw_hop_tile_stats(mpw_handle* h, unsigned long long* out /*2*/, int reset) {
+    if (!h || !out) return fail(MPW_ERR_ARG, "null argument");
+    out[0] = out[1] = 0;
+    if (!h->tcp.ar_stat) return 0;
+    if (set_device(h)) return MPW_ERR_CUDA;
+    CK(cudaMemcpy(out, h->tcp.ar_stat, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    if (reset) CK(cudaMemset(h->tcp.ar_stat, 0, 2 * sizeof(unsigned long long)));
+    return 0;
+}
+
 int mpw_num_patterns(mpw_handle* h) { return h ? h->np : -1; }
 
 long long mpw_launch_count(mpw_handle* h) { return h ? h->kernel_launches : -1; }

@@ -451,6 +451,12 @@ class DeviceDecoder:
     def message_of_words(self, cw_words64: np.ndarray) -> np.ndarray:
         return message_words(self._pivots, self._mix, unpack_bits(cw_words64, self.n))
 
+    def hop_tile_stats(self, reset: bool = False):
+        """(tiles, cycles) of the asynchronous-row hop since the last reset (mpw_hop_tile_stats)."""
+        out = np.zeros(2, dtype=np.uint64)
+        _native.check(_native.lib().mpw_hop_tile_stats(self._h, out.ctypes.data, int(reset)))
+        return int(out[0]), int(out[1])
+
     def set_option(self, key: str, value: int):
         """mpw_set_option (include/mpwsd.h): stage-1 kernel choice, timing, and
         the tensor hop's A/B launch variants and test hooks."""

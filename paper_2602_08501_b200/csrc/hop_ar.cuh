@@ -6,40 +6,41 @@
 // the P tiles stream cyclically and never stop, and every trajectory row runs
 // its own scan cycle (ntiles consecutive tiles starting at any tile).  The
 // scan warps do no insertion and take no data-dependent branch per tile: per
-// 64-pattern chunk they keep the chunk minimum, the row's running minimum, and
-// append the chunks whose minimum lies inside the certification window of the
-// running minimum to a per-thread hit list in shared memory (a predicated
-// store).  When a row's cycle ends, a worker warp (four per CTA, rows
-// statically partitioned) filters the row's hit chunks against the final
-// minimum, scores every pattern of those chunks from y in fp32 (supports in
-// ascending position), certifies the argmin / accept decision
+// 32-pattern group they keep the group minimum, update the row's running
+// minimum, and append the groups whose minimum lies inside the certification
+// window of the running minimum to a per-thread hit list in shared memory (a
+// predicated store).  When a row's cycle ends its bit is set in a ready mask;
+// any of the worker warps takes it, keeps the hit groups inside the window of
+// the final minimum m, recomputes the exact integer scores Q_p of their
+// patterns (DP4A on the row's int8 image and the pattern bits, transposed so a
+// lane holds its 8 positions of all 32 patterns), scores every pattern with
+// Q_p < m + wq from y in fp32, certifies the argmin / accept decision
 // (decoders.py:385-398) with the recursive-summation bound or re-scores the
-// finalists in float64, applies the move to the row's int8 image (or stores
-// the trajectory and builds the next one from the stage-2 queue), and
-// publishes the tile at which the row's next cycle starts.  Rows are dead only
-// between their cycle end and that tile (a few tiles); no CTA-wide round end
-// exists, so the MMA stream is continuous.
+// finalists in float64, applies the move to the row's int8 image (or stores the
+// trajectory and builds the next one of the stage-2 queue), and publishes the
+// tile at which the row's next cycle starts.  Rows are dead only between their
+// cycle end and that tile (about ten tiles of 244 at cfg4); no CTA-wide round
+// end exists, so the MMA stream is continuous.
 //
-// Exactness: a pattern outside every recorded chunk has Q_p >= m + wq for the
+// Exactness: a pattern outside every kept group has Q_p >= m + wq for the
 // row's final minimum m, hence S_p > S_best + thr by the frame's quantisation
 // bound (same window as the synchronous int8 screen, common.cuh warp_i8_scale);
-// all patterns of the recorded chunks are scored from y, so the decision is
-// the exact one.  A hit list that overflows (CAP entries per thread and cycle)
+// every pattern with Q_p < m + wq is scored from y, so the decision is the
+// exact one.  A hit list that overflows (CAP entries per thread and cycle)
 // makes the row scan once more with the achieved minimum as the seed of the
-// running minimum (then only true window chunks are recorded); the extra scan
+// running minimum (then only true window groups are recorded); the extra scan
 // is not counted in iterations_used.
 //
-// CTA = 28 warps (NCOL = 4; 20 with NCOL = 2), persistent, one per SM:
+// CTA = 20 warps (NCOL = 2), persistent, one per SM:
 //   warp 0        producer: cp.async.bulk of 32 KB pre-swizzled u8 P stages
-//   warps 1, 2    TMEM allocator + two tcgen05.mma issuer threads (warp 3 idle: it fills the warpgroup)
-//   warps 4..19   scan: NCOL per TMEM lane quarter, 256 / NCOL columns of every tile each (a scan
-//                 warp's per-tile work is serial -- wait, TMEM load, release, minima, records -- so
-//                 with two warps per quarter it, not the MMA, set the tile period)
-//   warps 20..27  workers: decisions, moves, refills
-// Register budgets (setmaxnreg; the CTA's pool is what its own warps release).  NCOL = 2:
-// warps 0..3 drop from 96 to 40 registers, the workers take 120, the scan warps stay at 96.
-// NCOL = 4 (16 scan warps, 896 threads, 72 registers at launch): warps 0..3 drop to 40, the
-// scan warps to 64, the workers take 104.
+//   warps 1, 2    TMEM allocator + two tcgen05.mma issuer threads on alternate tiles (warp 3
+//                 idle: it fills the warpgroup)
+//   warps 4..11   scan: NCOL per TMEM lane quarter, 256 / NCOL columns of every tile each
+//   warps 12..19  workers: decisions, moves, refills
+// Register budgets (setmaxnreg; the CTA's pool is what its own warps release): warps 0..3
+// drop from 96 to 40 registers, the workers take 120, the scan warps stay at 96.  (NCOL = 4,
+// 16 scan warps of 64 columns at 64 registers with workers at 104, compiles and is correct but
+// measured slower: seven warps per scheduler.)
 #pragma once
 #include "hop_tc.cuh"
 
@@ -49,8 +50,7 @@ using namespace tc;
 #ifndef MPW_AR_NWORK
 #define MPW_AR_NWORK 8
 #endif
-constexpr int NWORK = MPW_AR_NWORK;            // worker warps (rows statically partitioned)
-static_assert(ROWS % NWORK == 0 && ROWS / NWORK <= 32, "rows per worker");
+constexpr int NWORK = MPW_AR_NWORK;            // worker warps (any worker takes any ready row)
 #ifndef MPW_AR_NCOL
 #define MPW_AR_NCOL 2
 #endif
@@ -59,8 +59,8 @@ static_assert(NCOL == 2 || NCOL == 4, "column parts per row");
 constexpr int SCAN_T = ROWS * NCOL;            // scan threads
 constexpr int NLD = I8_TILE / NCOL / 64;       // 64-column TMEM loads per scan thread and tile
 constexpr int NGRP = I8_TILE / NCOL / 32;      // 32-pattern groups per scan thread and tile
-// warps 0..3: producer, MMA issuer, two idle (one warpgroup, so the three register budgets
-// below can be set per warpgroup); warps 4..11 scan; warps 12.. workers
+// warps 0..3: producer, two MMA issuers, one idle (one warpgroup, so the register budgets
+// can be set per warpgroup); then the scan warps; then the workers
 constexpr int SCAN_W0 = 4;
 constexpr int WORK_W0 = SCAN_W0 + SCAN_T / 32;
 constexpr int THREADS = 32 * (WORK_W0 + NWORK);

@@ -179,3 +179,24 @@ def test_float64_received_words_through_the_async_hop():
     np.testing.assert_array_equal(_np(a["best"])[ok], _np(b["best"])[ok])
     np.testing.assert_array_equal(_np(a["iters"])[ok], _np(b["iters"])[ok])
     np.testing.assert_allclose(_np(a["best_ed"])[ok], _np(b["best_ed"])[ok], rtol=1e-13)
+
+
+def test_empty_and_tiny_stage2_queues():
+    """CRC-gated decoding at high SNR: every frame (or all but a few) passes stage 1, so the hop is
+    launched on an empty or nearly empty stage-2 queue and must still terminate and agree with the
+    oracle."""
+    cfg = configs.CONFIGS["cfg3"]
+    code, sph = code_and_sphere(cfg)
+    dec = DeviceDecoder(code, sph)
+    for snr_scale, F in ((0.05, 256), (0.6, 512)):
+        sigma = cfg.sigma(code=code) * snr_scale
+        _, _, y = channel.bulk_inputs(code, 51, 0, 0, F, sigma)
+        o = dec.two_stage_batch(y, sigma, cfg.list_size, cfg.num_paths, cfg.max_iterations, "crc_gated",
+                                variant="tensor_i8a")
+        r = orc.two_stage_batch(y, code, sph, cfg.list_size, cfg.num_paths, cfg.max_iterations, True, sigma, nthreads=8)
+        np.testing.assert_array_equal(_np(o["stage"]), r["stage"])
+        best = words32_to_64(_np(o["best"]).view(np.uint32), code.n)
+        flags = _np(o["flags"])
+        ok = np.flatnonzero((flags & (UNRESOLVED | TIE_FINAL)) == 0)
+        np.testing.assert_array_equal(best[ok], r["best"][ok])
+    assert int(_np(o["stage"]).sum()) >= 0

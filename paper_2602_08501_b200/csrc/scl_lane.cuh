@@ -49,7 +49,13 @@ struct SclLane {
     static constexpr size_t PTR = PS + 4 * (size_t)L * NWP;
     static constexpr size_t SEL = PTR + 4 * (size_t)L * PTRW;
     static constexpr size_t CAND = (SEL + 4 * (size_t)L + 15) & ~(size_t)15;   // (pm, pm+|dm|) per path
-    static constexpr size_t TOTAL = CAND + 16 * (size_t)L;
+    // Scratch of the cooperative frozen runs (SclCoop below): 3N/2 doubles.  Where the
+    // instances of the dead paths can hold it (N = 256, L >= 16) it aliases them, else it is
+    // a region of its own.
+    static constexpr int SCRN = 3 * N / 2;
+    static constexpr bool SCR_ALIAS = (L - 1) * INST >= SCRN;
+    static constexpr size_t SCR = CAND + 16 * (size_t)L;
+    static constexpr size_t TOTAL = SCR + (SCR_ALIAS ? 0 : 8 * (size_t)SCRN);
     // offset of stored level lvl (3..RL-1) inside an instance
     __host__ __device__ static constexpr int off(int lvl) { return N / 4 - 2 * (N >> (lvl > 0 ? lvl : 0)); }
     // offset of register level lvl (RL..M) inside the lane's register array
@@ -205,6 +211,139 @@ __device__ __forceinline__ void clone_levels(double (&r)[SclLane<N, L>::RT], int
     }
 }
 
+// first non-frozen leaf at or after phi (N if there is none)
+template <int N>
+__device__ __forceinline__ int next_info_leaf(const uint32_t* __restrict__ frozen, int phi) {
+    constexpr int NW = N >= 32 ? N / 32 : 1;
+    for (int w = phi >> 5; w < NW; w++) {
+        uint32_t m = ~frozen[w];
+        if (w == (phi >> 5)) m &= ~0u << (phi & 31);
+        if (N < 32) m &= (1u << (N & 31)) - 1u;
+        if (m) return w * 32 + __ffs(m) - 1;
+    }
+    return N;
+}
+
+// ---- cooperative frozen runs
+// While only P < L paths are alive, the lanes of the dead paths would just
+// repeat work.  A run of frozen leaves [phi0, phi0 + tau) that starts where the
+// parent LLRs are virtual (phi0 = 0 or a multiple of N/8) is therefore computed
+// by all L lanes of the frame together, G = L / P lanes per live path.  Every
+// decision in the run is 0, so the left siblings of the path to leaf
+// phi0 + tau are rate-0 subtrees: their leaf LLRs come from an in-place
+// butterfly (f into the lower, g with u = 0 into the upper half of every node)
+// and the penalties are added in leaf order (decoders.py:216-218).  Each value
+// is produced by the same IEEE operation on the same operands as in the
+// depth-first schedule (decoders.py:239-252), so the path metrics stay
+// bit-identical.  The path's arrays of levels lev0..M end up in the scratch
+// (stored levels: directly in instance p), from where the caller installs them.
+//
+// Scratch of path p (W = h0r + h0 + h0/2 doubles, h0 = N >> lev0, h0r = lev0 ? h0 : 0):
+//   [0, h0r)                 root array (level lev0) unless it is a stored level
+//   h0r + h0 - 2 (N >> k)    path array of level k > lev0
+//   h0r + h0                 butterfly buffer (h0 / 2)
+template <int N, int L>
+struct SclCoop {
+    using Lay = SclLane<N, L>;
+    __device__ static __forceinline__ int h0r(int lev0) { return lev0 ? (N >> lev0) : 0; }
+    __device__ static __forceinline__ int stride(int lev0) { return h0r(lev0) + (N >> lev0) + (N >> (lev0 + 1)); }
+    __device__ static __forceinline__ double* level(double* base, double* inst, int lev0, int k) {
+        if (k > SCL_VIRT && k < Lay::RL) return inst + Lay::off(k);
+        return (k == lev0) ? base : base + h0r(lev0) + (N >> lev0) - 2 * (N >> k);
+    }
+    // in-place butterfly of a rate-0 subtree of h leaves by the G lanes of a path
+    __device__ static __forceinline__ void butterfly(double* B, int h, int s, int G) {
+        for (int sz = h; sz >= 2; sz >>= 1) {
+            const int hh = sz >> 1;
+            for (int t = s; t < (h >> 1); t += G) {
+                const int j = t & (hh - 1), i0 = ((t - j) << 1) + j, i1 = i0 + hh;
+                const double a = B[i0], c = B[i1];
+                B[i0] = scl_f(a, c);
+                B[i1] = c + a;
+            }
+            __syncwarp();
+        }
+    }
+    __device__ static __forceinline__ double penalties(const double* B, int h, double pm) {
+        for (int j = 0; j < h; j++) {
+            const double dm = B[j];
+            pm = pm + fabs(dm) * (double)(dm < 0.0);
+        }
+        return pm;
+    }
+    // returns the path metric of path p = l / G after the run
+    __device__ static __forceinline__ double run(int phi0, int tau, int lev0, int P, double pm,
+                                                 const double* __restrict__ llr0, const uint32_t* ps_all,
+                                                 double* llr, double* scr, int l) {
+        constexpr int M = Lay::M;
+        const int G = L / P, p = l / G, s = l - p * G;
+        const int h0 = N >> lev0;
+        double* base = scr + (size_t)p * stride(lev0);
+        double* inst = llr + (size_t)p * Lay::INST;
+        double* B = base + h0r(lev0) + h0;
+        const uint32_t* psrow = ps_all + p * Lay::NWP;
+        const double* cur = llr0;
+        if (lev0) {
+            // root of the run = right child made by the g node at depth lev0 - 1 (virtual parent)
+            double* root = level(base, inst, lev0, lev0);
+            const int n2 = phi0 >> (M - 2);
+            for (int j = s; j < h0; j += G) {
+                double v;
+                if (lev0 == 1) v = lv1<N>(llr0, psrow, 1, j);
+                else if (lev0 == 2) v = lv2<N>(llr0, psrow, n2, j);
+                else {
+                    const double a = lv2<N>(llr0, psrow, n2, j), c = lv2<N>(llr0, psrow, n2, j + N / 8);
+                    const int pos = n2 * (N / 4) + j;
+                    v = c + (((psrow[pos >> 5] >> (pos & 31)) & 1u) ? -a : a);
+                }
+                root[j] = v;
+            }
+            __syncwarp();
+            if (tau == h0) {                       // the whole subtree is frozen
+                butterfly(root, h0, s, G);
+                return penalties(root, h0, pm);
+            }
+            cur = root;
+        }
+        int sz = h0, lev = lev0, t = tau;
+        while (sz > 1) {
+            const int h = sz >> 1;
+            double* child = level(base, inst, lev0, lev + 1);
+            if (t < h) {
+                for (int j = s; j < h; j += G) child[j] = scl_f(cur[j], cur[j + h]);
+                __syncwarp();
+            } else {
+                for (int j = s; j < h; j += G) {
+                    const double a = cur[j], c = cur[j + h];
+                    B[j] = scl_f(a, c);
+                    child[j] = c + a;
+                }
+                __syncwarp();
+                butterfly(B, h, s, G);
+                pm = penalties(B, h, pm);
+                __syncwarp();
+                t -= h;
+            }
+            cur = child;
+            sz = h;
+            lev++;
+        }
+        return pm;
+    }
+};
+
+// register levels LVL..M of the lane := the path arrays a cooperative run left in the scratch
+template <int N, int L, int LVL>
+__device__ __forceinline__ void coop_install(double (&r)[SclLane<N, L>::RT], double* sb, double* si, int lev0) {
+    using Lay = SclLane<N, L>;
+    if constexpr (LVL <= Lay::M) {
+        const double* a = SclCoop<N, L>::level(sb, si, lev0, LVL);
+#pragma unroll
+        for (int j = 0; j < (N >> LVL); j++) r[Lay::roff(LVL) + j] = a[j];
+        coop_install<N, L, LVL + 1>(r, sb, si, lev0);
+    }
+}
+
 template <int N, int L>
 __global__ void __launch_bounds__(128, 4) scl_lane_kernel(CodeDev code, const float* __restrict__ y,
                                                        const double* __restrict__ llr64, int F,
@@ -226,6 +365,7 @@ __global__ void __launch_bounds__(128, 4) scl_lane_kernel(CodeDev code, const fl
     uint32_t* psrow = ps_all + l * NWP;
     uint8_t* ptrrow = ptr_all + l * Lay::PTRW * 4;
     double* myllr = llr + (size_t)l * Lay::INST;
+    double* scrx = reinterpret_cast<double*>(base + Lay::SCR);      // (unused when the scratch aliases llr)
     const double sig2 = sigma * sigma;
 
     for (long long fb = ((long long)blockIdx.x * wpb + wib) * FPW; fb < F;
@@ -246,7 +386,58 @@ __global__ void __launch_bounds__(128, 4) scl_lane_kernel(CodeDev code, const fl
         for (int j = 0; j < Lay::RT; j++) r[j] = 0.0;
         __syncwarp();
 
+        // combine after leaf phi (:253-259); after the last leaf it runs up to the root
+        auto combine = [&](int phi) {
+            const int c = __ffs(~phi) - 1;
+            for (int d = M - 1; d >= M - c; d--) {
+                const int half = N >> (d + 1);
+                const int lo = (phi >> (M - d)) << (M - d);
+                if (half >= 32) {
+                    const int hw = half >> 5, w0 = lo >> 5;
+                    for (int i = 0; i < hw; i++) psrow[w0 + i] ^= psrow[w0 + hw + i];
+                } else {
+                    const uint32_t mask = ((1u << half) - 1u) << (lo & 31);
+                    const uint32_t x = psrow[lo >> 5];
+                    psrow[lo >> 5] = x ^ ((x >> half) & mask);
+                }
+            }
+        };
+        int nlive = 1;                      // live paths = lanes 0..nlive-1 of the frame
         for (int phi = 0; phi < N; phi++) {
+            if constexpr (N >= 64 && L >= 2) {
+                // cooperative frozen run (coop_frozen_run above) while at most L/2 paths live
+                if ((phi & (N / 8 - 1)) == 0 && 2 * nlive <= L && ((code.frozen[phi >> 5] >> (phi & 31)) & 1u)) {
+                    const int lev0 = phi ? M - __ffs(phi) + 1 : 0;
+                    const int h0 = N >> lev0;
+                    const int tau = min(next_info_leaf<N>(code.frozen, phi) - phi, h0);
+                    const int cap = Lay::SCR_ALIAS ? (L - nlive) * Lay::INST : Lay::SCRN;
+                    if (tau >= 8 && (lev0 || tau < N) && nlive * SclCoop<N, L>::stride(lev0) <= cap) {
+                        const int P = nlive, G = L / P;
+                        double* scr = Lay::SCR_ALIAS ? llr + (size_t)P * Lay::INST : scrx;
+                        const double pin = __shfl_sync(MPW_FULL, pm, g0 + l / G);
+                        const double pout = SclCoop<N, L>::run(phi, tau, lev0, P, pin, llr0, ps_all, llr, scr, l);
+                        const double pmine = __shfl_sync(MPW_FULL, pout, g0 + (l < P ? l * G : l));
+                        if (l < P) pm = pmine;
+                        if (tau == h0) {            // whole subtree done: only the last leaf's combine acts
+                            combine(phi + h0 - 1);
+                            __syncwarp();
+                            phi += h0 - 1;
+                            continue;
+                        }
+                        // install the arrays on the path to leaf phi + tau (an information leaf)
+                        const int pl = l < P ? l : 0;
+                        double* sb = scr + (size_t)pl * SclCoop<N, L>::stride(lev0);
+                        double* si = llr + (size_t)pl * Lay::INST;
+                        if constexpr (Lay::RL > SCL_VIRT + 1) {   // (dead paths point at path 0's arrays)
+#pragma unroll
+                            for (int k = SCL_VIRT + 1; k < Lay::RL; k++) ptrrow[k] = (uint8_t)pl;
+                        }
+                        coop_install<N, L, Lay::RL>(r, sb, si, lev0);
+                        __syncwarp();
+                        phi += tau;
+                    }
+                }
+            }
             // descent to leaf phi: one g at depth M-1-ctz(phi), then f's.  Nodes
             // whose child level is virtual (depth < SCL_VIRT) need no work.
             // descent to leaf phi: one g at depth M-1-ctz(phi), then f's (one call
@@ -267,6 +458,7 @@ __global__ void __launch_bounds__(128, 4) scl_lane_kernel(CodeDev code, const fl
                 // stable rank of the 2L candidates (pm_k natural, pm_k + |dm_k| flipped);
                 // every path publishes its pair once, then reads all L pairs with
                 // broadcast 16-byte loads (instead of 2L 64-bit shuffles)
+                nlive = min(L, 2 * nlive);
                 const double vn = pm, vf = pm + fabs(dm);
                 cand[l] = make_double2(vn, vf);
                 __syncwarp();
@@ -314,20 +506,7 @@ __global__ void __launch_bounds__(128, 4) scl_lane_kernel(CodeDev code, const fl
                 for (int w = 0; w < Lay::PTRW; w++) mp[w] = rp[w];
                 __syncwarp();
             }
-            // combine (:253-259); after the last leaf it runs up to the root
-            const int c = __ffs(~phi) - 1;
-            for (int d = M - 1; d >= M - c; d--) {
-                const int half = N >> (d + 1);
-                const int lo = (phi >> (M - d)) << (M - d);
-                if (half >= 32) {
-                    const int hw = half >> 5, w0 = lo >> 5;
-                    for (int i = 0; i < hw; i++) psrow[w0 + i] ^= psrow[w0 + hw + i];
-                } else {
-                    const uint32_t mask = ((1u << half) - 1u) << (lo & 31);
-                    const uint32_t x = psrow[lo >> 5];
-                    psrow[lo >> 5] = x ^ ((x >> half) & mask);
-                }
-            }
+            combine(phi);
         }
 
         // ---- list: finite paths, stable by pm (decoders.py:261-268)

@@ -183,16 +183,18 @@ __device__ __forceinline__ void lane_step(bool is_g, double (&r)[SclLane<N, L>::
     }
 }
 
+// Descent to a leaf: the nodes at depths d0..M-1 (a g node at d0 unless this is
+// leaf 0, f nodes below).  One jump on d0 per leaf, the node bodies fall through
+// and exist once in the binary; each has its depth as a constant, so HALF and
+// the register indices are constants.
 template <int N, int L>
-__device__ __forceinline__ void lane_node(int d, bool is_g, double (&r)[SclLane<N, L>::RT], const double* llr,
-                                          double* myllr, uint8_t* ptrrow, const double* llr0,
-                                          const uint32_t* psrow, int n2, int lo, int l) {
-    // dispatch on depth so HALF = N >> (d+1) and the register indices are constants
+__device__ __forceinline__ void lane_descent(int d0, bool first_g, double (&r)[SclLane<N, L>::RT], const double* llr,
+                                             double* myllr, uint8_t* ptrrow, const double* llr0,
+                                             const uint32_t* psrow, int n2, int lo, int l) {
 #define MPW_LANE_CASE(DD) \
-    case DD: lane_step<N, L, DD>(is_g, r, llr, myllr, ptrrow, llr0, psrow, n2, lo, l); break;
-    switch (d) {
-        MPW_LANE_CASE(0) MPW_LANE_CASE(1) MPW_LANE_CASE(2) MPW_LANE_CASE(3)
-        MPW_LANE_CASE(4) MPW_LANE_CASE(5) MPW_LANE_CASE(6) MPW_LANE_CASE(7)
+    case DD: lane_step<N, L, DD>(first_g && d0 == DD, r, llr, myllr, ptrrow, llr0, psrow, n2, d0 == DD ? lo : 0, l);
+    switch (d0 < SCL_VIRT ? SCL_VIRT : d0) {
+        MPW_LANE_CASE(2) MPW_LANE_CASE(3) MPW_LANE_CASE(4) MPW_LANE_CASE(5) MPW_LANE_CASE(6) MPW_LANE_CASE(7)
         default: break;
     }
 #undef MPW_LANE_CASE
@@ -447,9 +449,7 @@ __global__ void __launch_bounds__(128, 4) scl_lane_kernel(CodeDev code, const fl
                 d0 = M - __ffs(phi);
                 lo = (phi >> (M - d0)) << (M - d0);
             }
-            for (int d = d0; d < M; d++)
-                lane_node<N, L>(d, phi && d == d0, r, llr, myllr, ptrrow, llr0, psrow, phi >> (M - 2),
-                                d == d0 ? lo : 0, l);
+            lane_descent<N, L>(d0, phi != 0, r, llr, myllr, ptrrow, llr0, psrow, phi >> (M - 2), lo, l);
             const double dm = r[Lay::roff(M)];
             const bool frozen = (code.frozen[phi >> 5] >> (phi & 31)) & 1u;
             if (frozen) {

@@ -246,3 +246,52 @@ def test_scl_lane_every_list_size_vs_oracle(n, quantised):
             u_bits = np.array([[(int(uw[f, i, j // 64]) >> (j % 64)) & 1 for j in range(n)]
                                for i in range(c)], dtype=np.uint8)
             np.testing.assert_array_equal(u_bits, u_ref, err_msg=f"L={L} frame {f}")
+
+
+def _coop_info_sets(n):
+    """Information sets that put the lane-per-path SCL through every shape of
+    its cooperative frozen runs (csrc/scl_lane.cuh, SclCoop): run lengths from
+    the minimum (8) to N - 1, runs that cover a whole right subtree while 1, 2
+    or 4 paths live (levels 1, 2, 3), runs that end inside it, a first
+    information leaf at 0 (no run) and scattered early information leaves."""
+    e, q, h = n // 8, n // 4, n // 2
+    tail = list(range(n - 6, n))
+    return {
+        "first_info_at_8": [8, 9] + tail,
+        "only_last_leaf": [n - 1],
+        "first_info_at_half": [h, h + 1] + tail,
+        "whole_eighth_two_paths": [e - 1, 2 * e + 3] + tail,            # [e, 2e) frozen with 2 paths
+        "whole_quarter_two_paths": [q - 1, h + 5] + tail,               # [q, 2q) frozen with 2 paths
+        "whole_half_two_paths": [h - 1, n - 7] + tail[1:],              # [h, n-7) frozen runs with 2 paths
+        "whole_eighth_four_paths": [e - 2, e - 1, 3 * e - 1] + tail,    # [e, 2e) with 4 paths, then inside [2e, 3e)
+        "info_at_zero": [0, 1, e, q + 1] + tail,
+        "scattered": [3, e + 9, q - 1, q + e, h - 1, h + e + 2, h + q] + tail,
+    }
+
+
+@pytest.mark.parametrize("n", [64, 128, 256])
+def test_scl_cooperative_frozen_runs_vs_oracle(n):
+    """decoders.py:181-268 on polar codes with arbitrary information sets: the
+    frozen runs the lanes of a frame compute together must leave lists,
+    codewords and float64 path metrics bit-equal to the depth-first schedule
+    (the oracle's restatement), with LLR ties and zeros included."""
+    from paper_2602_08501_b200.codes import polar_code_from_info_set
+    F = 24
+    for name, info in _coop_info_sets(n).items():
+        info = sorted(set(i for i in info if 0 <= i < n))
+        code = polar_code_from_info_set(n, info)
+        rng = np.random.default_rng(n + len(name))
+        llr = rng.normal(0.6, 1.8, size=(F, n))
+        llr[F // 2:] = np.round(llr[F // 2:] * 2.0) / 2.0
+        dec = DeviceDecoder(code)
+        for L in (4, 8, 16, 32):
+            o = dec.scl_batch(llrs=llr, list_size=L)
+            ln = _np(o["list_n"])
+            cw = words32_to_64(_np(o["list_cw"]).view(np.uint32), n)
+            pm = _np(o["list_pm"])
+            for f in range(F):
+                _, cw_ref, pm_ref = orc.scl(llr[f], code.info_set, n, L)
+                c = cw_ref.shape[0]
+                assert ln[f] == c, (name, L, f)
+                np.testing.assert_array_equal(cw[f, :c], cw_ref, err_msg=f"{name} L={L} frame {f}")
+                np.testing.assert_array_equal(pm[f, :c], pm_ref, err_msg=f"{name} L={L} frame {f}")

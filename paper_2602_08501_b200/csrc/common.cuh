@@ -110,28 +110,33 @@ __device__ __forceinline__ double exact_score64(const double* __restrict__ yrow,
 // Upper bound on the sum of the w largest of the values x[] spread over the
 // warp (lane holds x[lane + 32 j]): for any tau with #{x > tau} <= w,
 // sum_top_w <= sum_{x > tau} x + (w - #{x > tau}) * tau.  tau by bisection.
-__device__ __forceinline__ float warp_topw_bound(const float* xv, int cnt, int w) {
+// CNT > 0: the lane's value count is a compile-time constant (n = 32 CNT), so the
+// arrays of the callers stay in registers; CNT = 0: any n <= 1024.
+template <int CNT = 0>
+__device__ __forceinline__ float warp_topw_bound(const float* xv, int cnt_rt, int w) {
+    constexpr int CAP = CNT ? CNT : 32;
+    const int cnt = CNT ? CNT : cnt_rt;
     float mx = 0.0f;
-    for (int j = 0; j < cnt; j++) mx = fmaxf(mx, xv[j]);
+#pragma unroll
+    for (int j = 0; j < CAP; j++) if (j < cnt) mx = fmaxf(mx, xv[j]);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(MPW_FULL, mx, o));
     float lo = 0.0f, hi = mx;
     for (int it = 0; it < 12; it++) {
         const float mid = 0.5f * (lo + hi);
         int c = 0;
-        for (int j = 0; j < cnt; j++) c += xv[j] > mid;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(MPW_FULL, c, o);
+        for (int j = 0; j < CAP; j++) if (j < cnt) c += xv[j] > mid;
+        c = __reduce_add_sync(MPW_FULL, c);
         if (c <= w) hi = mid; else lo = mid;
     }
     float s = 0.0f;
     int c = 0;
-    for (int j = 0; j < cnt; j++) if (xv[j] > hi) { s += xv[j]; c++; }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        s += __shfl_xor_sync(MPW_FULL, s, o);
-        c += __shfl_xor_sync(MPW_FULL, c, o);
-    }
+    for (int j = 0; j < CAP; j++) if (j < cnt && xv[j] > hi) { s += xv[j]; c++; }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(MPW_FULL, s, o);
+    c = __reduce_add_sync(MPW_FULL, c);
     return (s + (float)(w - c) * hi) * 1.0001f;
 }
 
@@ -144,21 +149,26 @@ __device__ __forceinline__ float warp_topw_bound(const float* xv, int cnt, int w
 // an fp32 accumulation bound of (terms) * 2^-23 * sum|t| (2^-23 = 2u per
 // add: the tensor cores' fp32 accumulation is not guaranteed to round to
 // nearest).
+template <int CNT = 0>
 __device__ __forceinline__ float4 warp_error_bounds(const float* __restrict__ yrow, int n, int wmax) {
     const int lane = threadIdx.x & 31;
-    float ay[32], e1[32], e2[32];
-    int cnt = 0;
-    for (int i = lane; i < n; i += 32, cnt++) {
-        const float y = yrow[i];
-        const float h = __half2float(__float2half_rn(y));
-        const float l = __half2float(__float2half_rn(y - h));
-        ay[cnt] = fabsf(y);
-        e1[cnt] = fabsf(y - h);
-        e2[cnt] = fabsf((y - h) - l);
+    constexpr int CAP = CNT ? CNT : 32;
+    float ay[CAP], e1[CAP], e2[CAP];
+    const int cnt = CNT ? CNT : (n - lane + 31) / 32;
+#pragma unroll
+    for (int j = 0; j < CAP; j++) {
+        if (j < cnt) {
+            const float y = yrow[lane + 32 * j];
+            const float h = __half2float(__float2half_rn(y));
+            const float l = __half2float(__float2half_rn(y - h));
+            ay[j] = fabsf(y);
+            e1[j] = fabsf(y - h);
+            e2[j] = fabsf((y - h) - l);
+        }
     }
-    const float A = warp_topw_bound(ay, cnt, wmax);
-    const float T1 = warp_topw_bound(e1, cnt, wmax);
-    const float T2 = warp_topw_bound(e2, cnt, wmax);
+    const float A = warp_topw_bound<CNT>(ay, cnt, wmax);
+    const float T1 = warp_topw_bound<CNT>(e1, cnt, wmax);
+    const float T2 = warp_topw_bound<CNT>(e2, cnt, wmax);
     const float u = 1.1920929e-7f;   // 2^-23
     return make_float4(T1 + (float)wmax * u * A, T2 + 2.0f * (float)wmax * u * A,
                        (float)wmax * u * A, A);
@@ -176,28 +186,37 @@ __device__ __forceinline__ float i8_inv_scale(float ymax) {
 }
 __device__ __forceinline__ int i8_quant(float ay, float inv_s) { return __float2int_rn(__fmul_rn(ay, inv_s)); }
 
+template <int CNT = 0>
 __device__ __forceinline__ float4 warp_i8_scale(const float* __restrict__ yrow, int n, int wmax) {
     const int lane = threadIdx.x & 31;
-    float ay[32], e8[32];
-    int cnt = 0;
+    constexpr int CAP = CNT ? CNT : 32;
+    float ay[CAP], e8[CAP];
+    const int cnt = CNT ? CNT : (n - lane + 31) / 32;
     float mx = 0.0f;
-    for (int i = lane; i < n; i += 32, cnt++) {
-        ay[cnt] = fabsf(yrow[i]);
-        mx = fmaxf(mx, ay[cnt]);
+#pragma unroll
+    for (int j = 0; j < CAP; j++) {
+        if (j < cnt) {
+            ay[j] = fabsf(yrow[lane + 32 * j]);
+            mx = fmaxf(mx, ay[j]);
+        }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(MPW_FULL, mx, o));
     const float inv_s = i8_inv_scale(mx);
     const float s = __frcp_rn(inv_s);
-    for (int j = 0; j < cnt; j++) {
-        const int q = i8_quant(ay[j], inv_s);
-        const double e = fabs((double)ay[j] - (double)s * (double)q);
-        e8[j] = __double2float_ru(e);
+#pragma unroll
+    for (int j = 0; j < CAP; j++) {
+        if (j < cnt) {
+            const int q = i8_quant(ay[j], inv_s);
+            const double e = fabs((double)ay[j] - (double)s * (double)q);
+            e8[j] = __double2float_ru(e);
+        }
     }
-    const float T8 = warp_topw_bound(e8, cnt, wmax);
+    const float T8 = warp_topw_bound<CNT>(e8, cnt, wmax);
     const float u = 1.1920929e-7f;   // 2^-23
     float sa = 0.0f;                 // sum |y_i|, rounded up below (certification bound)
-    for (int j = 0; j < cnt; j++) sa += ay[j];
+#pragma unroll
+    for (int j = 0; j < CAP; j++) if (j < cnt) sa += ay[j];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) sa += __shfl_xor_sync(MPW_FULL, sa, o);
     return make_float4(inv_s, s, T8 + 4.0f * u * s * 127.0f * (float)wmax, sa * 1.0001f);

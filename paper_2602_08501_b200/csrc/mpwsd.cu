@@ -151,6 +151,11 @@ struct FinalOut {
     uint32_t* anchors; uint8_t* flags; int32_t* best_k;
 };
 
+// CNT = n / 32 as a constant (n = 64 / 128 / 256): the frame's received word
+// and the codeword words live in registers; CNT = 0: any n.  The float64 sums
+// keep one order in both forms: lane-sequential over i = lane + 32 j, then the
+// xor butterfly.
+template <int CNT>
 __global__ void finalize_kernel(int n, int nw, int A, int T, const float* __restrict__ y,
                                 const double* __restrict__ y64, S2Dev s2, FinalOut out, float tie_rel) {
     const int lane = threadIdx.x & 31;
@@ -158,46 +163,90 @@ __global__ void finalize_kernel(int n, int nw, int A, int T, const float* __rest
     const int count = *s2.count;
     for (int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); q < count; q += warps) {
         const int f = s2.frame[q], na = s2.nanchor[q];
+        // per-anchor outputs of the frame, copied in bulk
+        if (out.iters)
+            for (int a = lane; a < A; a += 32) out.iters[(size_t)f * A + a] = a < na ? s2.traj_iters[(size_t)q * A + a] : 0;
+        if (out.hops)
+            for (int i = lane; i < na * T; i += 32) out.hops[(size_t)f * A * T + i] = s2.traj_hops[(size_t)q * A * T + i];
+        if (out.anchors)
+            for (int i = lane; i < na * nw; i += 32) out.anchors[(size_t)f * A * nw + i] = s2.anchors[(size_t)q * A * nw + i];
+        uint32_t flw = 0;
+        for (int a = lane; a < na; a += 32) flw |= s2.traj_flags[(size_t)q * A + a];
+        uint8_t fl = (uint8_t)__reduce_or_sync(MPW_FULL, flw);
+
         double best = CUDART_INF, second = CUDART_INF;
         int bk = 0;
-        uint8_t fl = 0;
-        for (int a = 0; a < na; a++) {
-            const uint32_t* cw = s2.traj_cw + ((size_t)q * A + a) * nw;
-            double acc = 0.0;
-            for (int i = lane; i < n; i += 32) {
-                const double x = ((cw[i >> 5] >> (i & 31)) & 1u) ? -1.0 : 1.0;
-                const double d = (y64 ? y64[(size_t)f * n + i] : (double)y[(size_t)f * n + i]) - x;
-                acc += d * d;
-            }
+        if constexpr (CNT > 0) {
+            double yd[CNT];
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(MPW_FULL, acc, o);
-            bool same = true;   // identical codeword to the current best?
-            if (a > 0) {
-                const uint32_t* bc = s2.traj_cw + ((size_t)q * A + bk) * nw;
-                bool diff = false;
-                for (int w = lane; w < nw; w += 32) diff |= cw[w] != bc[w];
-                same = !__any_sync(MPW_FULL, diff);
+            for (int j = 0; j < CNT; j++)
+                yd[j] = y64 ? y64[(size_t)f * n + lane + 32 * j] : (double)y[(size_t)f * n + lane + 32 * j];
+            uint32_t bw[CNT];
+#pragma unroll
+            for (int j = 0; j < CNT; j++) bw[j] = 0u;
+            for (int a = 0; a < na; a++) {
+                const uint32_t* cw = s2.traj_cw + ((size_t)q * A + a) * nw;
+                uint32_t w[CNT];
+                if constexpr (CNT % 4 == 0) {
+#pragma unroll
+                    for (int j = 0; j < CNT; j += 4) {
+                        const uint4 v = *reinterpret_cast<const uint4*>(cw + j);
+                        w[j] = v.x; w[j + 1] = v.y; w[j + 2] = v.z; w[j + 3] = v.w;
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < CNT; j++) w[j] = cw[j];
+                }
+                double acc = 0.0;
+                bool same = true;
+#pragma unroll
+                for (int j = 0; j < CNT; j++) {
+                    const double x = ((w[j] >> lane) & 1u) ? -1.0 : 1.0;
+                    const double d = yd[j] - x;
+                    acc += d * d;
+                    same = same && (w[j] == bw[j]);
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(MPW_FULL, acc, o);
+                if (a == 0) same = true;
+                if (acc < best) {
+                    if (a > 0 && !same) second = best;
+                    best = acc;
+                    bk = a;
+#pragma unroll
+                    for (int j = 0; j < CNT; j++) bw[j] = w[j];
+                } else if (!same && acc < second) {
+                    second = acc;
+                }
             }
-            if (acc < best) {
-                if (a > 0 && !same) second = best;
-                best = acc;
-                bk = a;
-            } else if (!same && acc < second) {
-                second = acc;
+        } else {
+            for (int a = 0; a < na; a++) {
+                const uint32_t* cw = s2.traj_cw + ((size_t)q * A + a) * nw;
+                double acc = 0.0;
+                for (int i = lane; i < n; i += 32) {
+                    const double x = ((cw[i >> 5] >> (i & 31)) & 1u) ? -1.0 : 1.0;
+                    const double d = (y64 ? y64[(size_t)f * n + i] : (double)y[(size_t)f * n + i]) - x;
+                    acc += d * d;
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(MPW_FULL, acc, o);
+                bool same = true;   // identical codeword to the current best?
+                if (a > 0) {
+                    const uint32_t* bc = s2.traj_cw + ((size_t)q * A + bk) * nw;
+                    bool diff = false;
+                    for (int w = lane; w < nw; w += 32) diff |= cw[w] != bc[w];
+                    same = !__any_sync(MPW_FULL, diff);
+                }
+                if (acc < best) {
+                    if (a > 0 && !same) second = best;
+                    best = acc;
+                    bk = a;
+                } else if (!same && acc < second) {
+                    second = acc;
+                }
             }
-            fl |= s2.traj_flags[(size_t)q * A + a];
-            if (lane == 0 && out.iters) out.iters[(size_t)f * A + a] = s2.traj_iters[(size_t)q * A + a];
-            if (out.hops)
-                for (int h = lane; h < T; h += 32)
-                    out.hops[((size_t)f * A + a) * T + h] = s2.traj_hops[((size_t)q * A + a) * T + h];
-            if (out.anchors)
-                for (int w = lane; w < nw; w += 32)
-                    out.anchors[((size_t)f * A + a) * nw + w] = s2.anchors[((size_t)q * A + a) * nw + w];
         }
         if (second - best < (double)tie_rel * best) fl |= 4;
-        for (int a = na + lane; a < A; a += 32) {
-            if (out.iters) out.iters[(size_t)f * A + a] = 0;
-        }
         for (int w = lane; w < nw; w += 32) out.best[(size_t)f * nw + w] = s2.traj_cw[((size_t)q * A + bk) * nw + w];
         if (lane == 0) {
             out.best_ed[f] = best;
@@ -276,53 +325,74 @@ __global__ void frame_kernel(FrameArgs fa) {
 // (warp per frame: also the per-frame score error bounds the hop kernels use)
 // float64 inputs: every screen bound also covers sum_{supp}|y64_i - y_i| <=
 // the sum of the wmax largest fp32 rounding errors of the frame
+template <int CNT = 0>
 __device__ __forceinline__ float y64_rounding_bound(const float* __restrict__ yrow, const double* __restrict__ y64row,
                                                     int n, int wmax) {
-    float r[32];
-    int cnt = 0;
-    for (int i = threadIdx.x & 31; i < n; i += 32, cnt++)
-        r[cnt] = __double2float_ru(fabs(y64row[i] - (double)yrow[i]));
-    return warp_topw_bound(r, cnt, wmax);
-}
-__device__ __forceinline__ float4 widen_for_y64(float4 eb, const float* __restrict__ yrow,
-                                                const double* __restrict__ y64row, int n, int wmax) {
-    const float R = y64_rounding_bound(yrow, y64row, n, wmax);
-    return make_float4(eb.x + R, eb.y + R, eb.z + R, eb.w);
+    constexpr int CAP = CNT ? CNT : 32;
+    const int lane = threadIdx.x & 31;
+    float r[CAP];
+    const int cnt = CNT ? CNT : (n - lane + 31) / 32;
+#pragma unroll
+    for (int j = 0; j < CAP; j++)
+        if (j < cnt) r[j] = __double2float_ru(fabs(y64row[lane + 32 * j] - (double)yrow[lane + 32 * j]));
+    return warp_topw_bound<CNT>(r, cnt, wmax);
 }
 
+// Bounds of one queue entry (warp): the fp16 / fp32 screens' error bounds only where a
+// hop that reads them will run (need_eb), the int8 quantisation always.
+template <int CNT>
+__device__ __forceinline__ void entry_bounds(const float* __restrict__ yr, const double* __restrict__ y64r, int n,
+                                             int q, bool need_eb, S2Dev s2) {
+    const int lane = threadIdx.x & 31;
+    const float R = y64r ? y64_rounding_bound<CNT>(yr, y64r, n, s2.wmax) : 0.0f;
+    if (need_eb) {
+        float4 eb = warp_error_bounds<CNT>(yr, n, s2.wmax);
+        if (y64r) eb = make_float4(eb.x + R, eb.y + R, eb.z + R, eb.w);
+        if (lane == 0) s2.ebound[q] = eb;
+    }
+    float4 qs = warp_i8_scale<CNT>(yr, n, s2.wmax);
+    qs.z += R;                                           // int8 screen of fp32(y64)
+    if (lane == 0) s2.qscale[q] = qs;
+}
+
+template <int CNT>
 __global__ void queue_identity_kernel(int F, int A, int n, const float* __restrict__ y,
-                                      const double* __restrict__ y64, const int32_t* nanchor, S2Dev s2) {
+                                      const double* __restrict__ y64, const int32_t* nanchor, S2Dev s2,
+                                      bool need_eb) {
     const int lane = threadIdx.x & 31;
     const int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (q == 0 && lane == 0) *s2.count = F;
     if (q < F) {
-        float4 eb = warp_error_bounds(y + (size_t)q * n, n, s2.wmax);
-        if (y64) eb = widen_for_y64(eb, y + (size_t)q * n, y64 + (size_t)q * n, n, s2.wmax);
-        float4 qs = warp_i8_scale(y + (size_t)q * n, n, s2.wmax);
-        if (y64) qs.z += y64_rounding_bound(y + (size_t)q * n, y64 + (size_t)q * n, n, s2.wmax);   // int8 screen of fp32(y64)
+        entry_bounds<CNT>(y + (size_t)q * n, y64 ? y64 + (size_t)q * n : nullptr, n, q, need_eb, s2);
         if (lane == 0) {
             s2.frame[q] = q;
             s2.nanchor[q] = nanchor ? min(nanchor[q], A) : A;
-            s2.ebound[q] = eb;
-            s2.qscale[q] = qs;
         }
     }
 }
 
 // per-frame score error bounds of the queued stage-2 frames (warp per entry)
-__global__ void ebound_kernel(int n, const float* __restrict__ y, const double* __restrict__ y64, S2Dev s2) {
-    const int lane = threadIdx.x & 31;
+template <int CNT>
+__global__ void ebound_kernel(int n, const float* __restrict__ y, const double* __restrict__ y64, S2Dev s2,
+                              bool need_eb) {
     const int warps = gridDim.x * (blockDim.x >> 5);
     const int count = *s2.count;
     for (int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); q < count; q += warps) {
-        const float* yr = y + (size_t)s2.frame[q] * n;
-        float4 eb = warp_error_bounds(yr, n, s2.wmax);
-        if (y64) eb = widen_for_y64(eb, yr, y64 + (size_t)s2.frame[q] * n, n, s2.wmax);
-        float4 qs = warp_i8_scale(yr, n, s2.wmax);
-        if (y64) qs.z += y64_rounding_bound(yr, y64 + (size_t)s2.frame[q] * n, n, s2.wmax);   // int8 screen of fp32(y64)
-        if (lane == 0) { s2.ebound[q] = eb; s2.qscale[q] = qs; }
+        const size_t f = (size_t)s2.frame[q];
+        entry_bounds<CNT>(y + f * n, y64 ? y64 + f * n : nullptr, n, q, need_eb, s2);
     }
 }
+
+// launches with the per-lane value count as a constant for n = 64 / 128 / 256
+#define MPW_BY_CNT(n_, CALL)                         \
+    do {                                             \
+        switch (n_) {                                \
+            case 64: { constexpr int CNT = 2; CALL; break; }   \
+            case 128: { constexpr int CNT = 4; CALL; break; }  \
+            case 256: { constexpr int CNT = 8; CALL; break; }  \
+            default: { constexpr int CNT = 0; CALL; break; }   \
+        }                                            \
+    } while (0)
 
 // float64 inputs: fp32 rounding for the screens and float64 channel LLRs
 // 2.0 * y / (sigma * sigma) with the reference's operation order (decoders.py:550)
@@ -477,6 +547,12 @@ int resolve_variant(mpw_handle* h, int variant, bool f64 = false) {
     return MPW_HOP_TENSOR;
 }
 
+// the int8 screens read only the int8 quantisation bounds (qscale); the fp16 screens and
+// the gather also the fp16 / fp32 score error bounds (ebound)
+bool needs_fp_bounds(int resolved_variant) {
+    return !(resolved_variant == MPW_HOP_TENSOR_I8 || resolved_variant == MPW_HOP_TENSOR_I8_ASYNC);
+}
+
 int run_hops(mpw_handle* h, const float* y, const double* y64, int Fmax, int A, int T, int variant, S2Dev s2,
              cudaStream_t st) {
     variant = resolve_variant(h, variant, y64 != nullptr);
@@ -522,7 +598,12 @@ int run_hops(mpw_handle* h, const float* y, const double* y64, int Fmax, int A, 
 int finalize(mpw_handle* h, const float* y, const double* y64, int Fmax, int A, int T, S2Dev s2, FinalOut fo,
              cudaStream_t st) {
     const int grid = std::max(1, std::min((Fmax + 7) / 8, h->num_sms * 8));
-    finalize_kernel<<<grid, 256, 0, st>>>(h->n, h->nw, A, T, y, y64, s2, fo, 1e-5f);
+    switch (h->n) {
+        case 64: finalize_kernel<2><<<grid, 256, 0, st>>>(h->n, h->nw, A, T, y, y64, s2, fo, 1e-5f); break;
+        case 128: finalize_kernel<4><<<grid, 256, 0, st>>>(h->n, h->nw, A, T, y, y64, s2, fo, 1e-5f); break;
+        case 256: finalize_kernel<8><<<grid, 256, 0, st>>>(h->n, h->nw, A, T, y, y64, s2, fo, 1e-5f); break;
+        default: finalize_kernel<0><<<grid, 256, 0, st>>>(h->n, h->nw, A, T, y, y64, s2, fo, 1e-5f); break;
+    }
     CK(cudaGetLastError());
     h->kernel_launches++;
     return 0;
@@ -739,7 +820,8 @@ int mpwsd_impl(mpw_handle* h, const float* y, const double* y64, const uint32_t*
     if (int rc = ensure_s2(h, F, A, T, hops != nullptr)) return rc;
     S2Dev s2 = s2_dev(h, anchors, hops != nullptr);
     CK(cudaMemsetAsync(s2.work_next, 0, sizeof(int32_t), st));
-    queue_identity_kernel<<<(F + 7) / 8, 256, 0, st>>>(F, A, h->n, y, y64, n_anchor, s2);
+    const bool need_eb = needs_fp_bounds(resolve_variant(h, variant, y64 != nullptr));
+    MPW_BY_CNT(h->n, (queue_identity_kernel<CNT><<<(F + 7) / 8, 256, 0, st>>>(F, A, h->n, y, y64, n_anchor, s2, need_eb)));
     CK(cudaGetLastError());
     h->kernel_launches++;
     if (int rc = run_hops(h, y, y64, F, A, T, variant, s2, st)) return rc;
@@ -862,7 +944,9 @@ int two_stage_impl(mpw_handle* h, const float* y, const double* y64, int F, cons
         if (int rc = launch_osd(h, a, st)) return rc;
         s1flags = h->s1_flags.p;
     }
-    ebound_kernel<<<std::max(1, std::min((F + 7) / 8, h->num_sms * 16)), 256, 0, st>>>(h->n, y, y64, s2);
+    const bool need_eb = needs_fp_bounds(resolve_variant(h, variant, y64 != nullptr));
+    MPW_BY_CNT(h->n, (ebound_kernel<CNT><<<std::max(1, std::min((F + 7) / 8, h->num_sms * 16)), 256, 0, st>>>(
+                         h->n, y, y64, s2, need_eb)));
     CK(cudaGetLastError());
     h->kernel_launches++;
     timing_mark(h, 1, st);

@@ -18,7 +18,7 @@ PROF_LIB = os.path.join(HERE, "libmpwsd_prof.so")
 SOURCES = ["mpwsd.cu", "hop_tc.cu", "hop_ar.cu", "scl_lane.cu", "sphere_tools.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CFLAGS = [*ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3"]
+CFLAGS = [*os.environ.get("MPW_EXTRA_CFLAGS", "").split(), *ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3"]
 
 
 def _deps():

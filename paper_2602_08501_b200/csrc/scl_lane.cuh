@@ -28,6 +28,12 @@
 // 3..RL-1 are stored per path instance in shared memory, levels RL..M in
 // registers (SclLane below).
 constexpr int SCL_VIRT = 2;
+#ifndef MPW_SCL_D2_UNROLL
+#define MPW_SCL_D2_UNROLL 1      // depth-2 node loop (measured on cfg4: 1: 7.35 ms, 2: 7.40, 4: 7.85, 8: 9.02: instruction fetch)
+#endif
+#ifndef MPW_SCL_RANK_UNROLL
+#define MPW_SCL_RANK_UNROLL 4    // unroll factor of the info-leaf ranking loop (measured: 2: 7.89 ms, 4: 7.85, 8: 8.21, 16: 9.26 on cfg4)
+#endif
 
 template <int N, int L>
 struct SclLane {
@@ -122,7 +128,8 @@ __device__ __forceinline__ void lane_node_d2(bool is_g, int n2, const double* __
                                              int lo) {
     constexpr int HALF = N / 8;
     const uint32_t word = (HALF >= 32) ? 0u : (psrow[lo >> 5] >> (lo & 31));
-#pragma unroll 4
+    constexpr int DU = MPW_SCL_D2_UNROLL;
+#pragma unroll (DU)
     for (int j = 0; j < HALF; j++) {
         const double a = lv2<N>(llr0, psrow, n2, j), c = lv2<N>(llr0, psrow, n2, j + HALF);
         if (!is_g) {
@@ -391,11 +398,14 @@ __global__ void __launch_bounds__(128, 4) scl_lane_kernel(CodeDev code, const fl
         // combine after leaf phi (:253-259); after the last leaf it runs up to the root
         auto combine = [&](int phi) {
             const int c = __ffs(~phi) - 1;
+            // (rolled: this runs after every leaf, and the kernel is bound by instruction fetch)
+#pragma unroll 1
             for (int d = M - 1; d >= M - c; d--) {
                 const int half = N >> (d + 1);
                 const int lo = (phi >> (M - d)) << (M - d);
                 if (half >= 32) {
                     const int hw = half >> 5, w0 = lo >> 5;
+#pragma unroll 1
                     for (int i = 0; i < hw; i++) psrow[w0 + i] ^= psrow[w0 + hw + i];
                 } else {
                     const uint32_t mask = ((1u << half) - 1u) << (lo & 31);
@@ -463,7 +473,8 @@ __global__ void __launch_bounds__(128, 4) scl_lane_kernel(CodeDev code, const fl
                 cand[l] = make_double2(vn, vf);
                 __syncwarp();
                 int rn = 0, rf = 0;
-#pragma unroll
+                constexpr int RU = MPW_SCL_RANK_UNROLL < L ? MPW_SCL_RANK_UNROLL : L;
+#pragma unroll (RU)
                 for (int k = 0; k < L; k++) {
                     const double2 ck = cand[k];
                     const double pk = ck.x, fk = ck.y;
@@ -547,6 +558,7 @@ __global__ void __launch_bounds__(128, 4) scl_lane_kernel(CodeDev code, const fl
         // ---- CRC gate (decoders.py:559-570) on v = u[info_set] (codebook.py:154-163, 287-297)
         uint64_t v = 0;
         if (code.is_ca) {
+#pragma unroll 1
             for (int j = 0; j < code.kp; j++) {
                 const int pos = code.info[j];
                 v |= (uint64_t)((psrow[pos >> 5] >> (pos & 31)) & 1u) << j;
@@ -555,6 +567,7 @@ __global__ void __launch_bounds__(128, 4) scl_lane_kernel(CodeDev code, const fl
         int gwin = 1 << 30;                 // lowest CRC-valid rank in this frame group
         if (mode == 1) {
             uint32_t syn = 0;
+#pragma unroll 1
             for (int j = 0; j < code.crc_deg; j++) syn |= (uint32_t)(__popcll(v & code.crc_h[j]) & 1) << j;
             gwin = (fin && syn == 0) ? rank : (1 << 30);
 #pragma unroll

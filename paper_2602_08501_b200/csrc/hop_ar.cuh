@@ -549,9 +549,9 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
                     // Per hit group (32 patterns): lane L holds byte L (positions 8 L .. 8 L + 7)
                     // of all 32 patterns (transposed bits, one 32-byte load per lane) and the
                     // row's int8 values of the same positions; the exact integer score Q_j of
-                    // pattern j is the warp sum (REDUX) of two DP4As per lane.  The patterns
-                    // inside the window of the final minimum are then scored from y in fp32 with
-                    // the same bytes (8 positions per lane, butterfly sum).
+                    // pattern j is the warp sum (shuffle butterfly) of two DP4As per lane.  The
+                    // patterns inside the window of the final minimum are then scored from y in
+                    // fp32 with the same bytes (8 positions per lane, butterfly sum).
                     auto load_group = [&](int grp, uint4& t0, uint4& t1) {
                         t0 = make_uint4(0u, 0u, 0u, 0u);
                         t1 = t0;
@@ -563,30 +563,43 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
                     };
                     auto do_group = [&](int grp, const uint4& t0, const uint4& t1) {
                         const uint32_t tb[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
-                        // this lane's share of Q_j for the 32 patterns: a nibble's bits -> 0/1 bytes by
-                        // one multiplication (bit k lands on bits k, k + 7, k + 14, k + 21; the four
-                        // copies of a nibble do not overlap, those of a whole byte would)
-                        int v[32];
+                        // this lane's share of Q_j, eight patterns at a time in a rolled loop (the
+                        // streaming loop of the scan warps shares the instruction caches with this
+                        // code): a nibble's bits -> 0/1 bytes by one multiplication (bit k lands on
+                        // bits k, k + 7, k + 14, k + 21; the four copies of a nibble do not overlap,
+                        // those of a whole byte would)
+                        unsigned cm = 0u;
+                        uint32_t rb[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
+#pragma unroll 1
+                        for (int c8 = 0; c8 < 4; c8++) {
+                            int v[8];
 #pragma unroll
-                        for (int j = 0; j < 32; j++) {
-                            const uint32_t byte = (tb[j >> 2] >> (8 * (j & 3))) & 0xFFu;
-                            const uint32_t lo = ((byte & 0xFu) * 0x00204081u) & 0x01010101u;
-                            const uint32_t hi = ((byte >> 4) * 0x00204081u) & 0x01010101u;
-                            v[j] = __dp4a((int)q2.y, (int)hi, __dp4a((int)q2.x, (int)lo, 0));
-                        }
-                        // transposing butterfly: after the five steps lane j holds the warp sum of v[j]
-#pragma unroll
-                        for (int o = 16; o > 0; o >>= 1) {
-                            const bool up = (lane & o) != 0;
-#pragma unroll
-                            for (int i = 0; i < o; i++) {
-                                const int send = up ? v[i] : v[i + o];
-                                const int keep = up ? v[i + o] : v[i];
-                                v[i] = keep + __shfl_xor_sync(MPW_FULL, send, o);
+                            for (int j = 0; j < 8; j++) {
+                                const uint32_t byte = (rb[j >> 2] >> (8 * (j & 3))) & 0xFFu;
+                                const uint32_t lo = ((byte & 0xFu) * 0x00204081u) & 0x01010101u;
+                                const uint32_t hi = ((byte >> 4) * 0x00204081u) & 0x01010101u;
+                                v[j] = __dp4a((int)q2.y, (int)hi, __dp4a((int)q2.x, (int)lo, 0));
                             }
+#pragma unroll
+                            for (int j = 0; j < 6; j++) rb[j] = rb[j + 2];
+                            // transposing butterfly over lane bits 2..0, then plain sums over bits 3, 4:
+                            // every lane with (lane & 7) = j holds the warp sum of v[j] (exact integers)
+#pragma unroll
+                            for (int o = 4; o > 0; o >>= 1) {
+                                const bool up = (lane & o) != 0;
+#pragma unroll
+                                for (int i = 0; i < o; i++) {
+                                    const int send = up ? v[i] : v[i + o];
+                                    const int keep = up ? v[i + o] : v[i];
+                                    v[i] = keep + __shfl_xor_sync(MPW_FULL, send, o);
+                                }
+                            }
+                            int Q = v[0];
+                            Q += __shfl_xor_sync(MPW_FULL, Q, 8);
+                            Q += __shfl_xor_sync(MPW_FULL, Q, 16);
+                            const unsigned b8 = __ballot_sync(MPW_FULL, lane < 8 && grp * 32 + c8 * 8 + lane < np_ && Q < limit);
+                            cm |= b8 << (8 * c8);
                         }
-                        const int Q = v[0];
-                        unsigned cm = __ballot_sync(MPW_FULL, grp * 32 + lane < np_ && Q < limit);
                         if (STATS) st_chunks++;
                         if (cm && !tv_ready) {
                             const float yv[8] = {ya.x, ya.y, ya.z, ya.w, yb.x, yb.y, yb.z, yb.w};

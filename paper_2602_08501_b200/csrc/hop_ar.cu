@@ -18,7 +18,7 @@ static float ar_cert_gamma(int wmax, bool y64) {
 
 bool ar_supported(const TcPatterns& t, int n) {
     // u8 images present (|P| <= 2^17, 127 wmax < 8192), 32-pattern group ids fit 16 bits
-    return t.ready8 && t.pbT && (n == 128 || n == 256) && t.np <= (1 << 17);
+    return t.ready8 && (n == 128 || n == 256) && t.np <= (1 << 17);
 }
 
 template <int KB, int NW, bool STATS>
@@ -26,7 +26,7 @@ static int ar_launch_t(const TcPatterns& t, int n, int A, int T, const float* y,
                        int experiment, int hit_cap, cudaStream_t st) {
     ar::Params prm;
     prm.n = n; prm.nw = NW; prm.A = A; prm.T = T; prm.np = t.np; prm.ntiles = t.ntiles8;
-    prm.y = y; prm.y64 = y64; prm.s2 = s2; prm.pbits = P.bits; prm.pbT = t.pbT; prm.btiles = t.tiles8;
+    prm.y = y; prm.y64 = y64; prm.s2 = s2; prm.pbits = P.bits; prm.btiles = t.tiles8;
     prm.tie_rel = 1e-5f;
     prm.cap = hit_cap > 0 && hit_cap < ar::CAP ? hit_cap : ar::CAP;
     prm.cert_g = ar_cert_gamma(s2.wmax, y64 != nullptr);

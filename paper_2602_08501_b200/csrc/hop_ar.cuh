@@ -12,8 +12,8 @@
 // predicated store).  When a row's cycle ends its bit is set in a ready mask;
 // any of the worker warps takes it, keeps the hit groups inside the window of
 // the final minimum m, recomputes the exact integer scores Q_p of their
-// patterns (DP4A on the row's int8 image and the pattern bits, transposed so a
-// lane holds its 8 positions of all 32 patterns), scores every pattern with
+// patterns (lane = pattern: popcounts of the pattern words against the eight bit
+// planes of the row's int8 image, no cross-lane reduction), scores every pattern with
 // Q_p < m + wq from y in fp32, certifies the argmin / accept decision
 // (decoders.py:385-398) with the recursive-summation bound or re-scores the
 // finalists in float64, applies the move to the row's int8 image (or stores the
@@ -84,7 +84,6 @@ struct Params {
     const double* y64;           // float64 inputs: the caller's received words (y = their fp32 rounding), else null
     S2Dev s2;
     const uint32_t* pbits;       // np x nw
-    const uint4* pbT;            // bits transposed for the workers: [group of 32 patterns][n / 8 position bytes][32 patterns]
     const uint8_t* btiles;       // [ntiles][KB][256 x 128 u8] swizzled images
     float tie_rel;
     int cap;                     // hit-list entries per scan thread and cycle in use (<= CAP)
@@ -100,7 +99,8 @@ __host__ __device__ constexpr size_t smem_bytes(int kb) {
     return (size_t)kb * A_KBLK_BYTES + (size_t)AR_STAGES * I8_STAGE_BYTES + (size_t)CAP * SCAN_T * 4 +
            ROWS * 8 /*row_ctl*/ + ROWS * 4 /*row_best*/ + ROWS * 4 /*row_done*/ + SCAN_T /*hit_cnt*/ +
            ROWS * RSW * 4 /*row state*/ + 16 /*ready mask*/ +
-           (2 * AR_STAGES + 4) * 8 /*barriers*/ + 16 /*tmem slot, stop tile, issue counter, rows left*/;
+           (2 * AR_STAGES + 4) * 8 /*barriers*/ + 16 /*tmem slot, stop tile, issue counter, rows left*/ +
+           NWORK * 256 /*bit planes of the row a worker is deciding*/;
 }
 
 __device__ __forceinline__ uint2 ld_shared_volatile_v2(const uint2* p) {
@@ -216,6 +216,7 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
     volatile uint32_t* stop_tile = tmem_slot + 1;    // first tile nobody processes (0xFFFFFFFF while rows are left)
     volatile uint32_t* issue_ctr = tmem_slot + 2;    // tile whose MMAs the issuer is about to issue
     int* rows_left = reinterpret_cast<int*>(tmem_slot + 3);
+    unsigned char* planes = reinterpret_cast<unsigned char*>(tmem_slot + 4);   // [NWORK][8 planes][32 bytes]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n = prm.n, A = prm.A, T = prm.T, np_ = prm.np, ntiles = prm.ntiles;
@@ -546,60 +547,49 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
                     int fi = 0x7FFFFFFF;
                     bool tv_ready = false;
                     uint32_t pw = 0u;          // lanes < NW: word `lane` of the running best pattern
-                    // Per hit group (32 patterns): lane L holds byte L (positions 8 L .. 8 L + 7)
-                    // of all 32 patterns (transposed bits, one 32-byte load per lane) and the
-                    // row's int8 values of the same positions; the exact integer score Q_j of
-                    // pattern j is the warp sum (shuffle butterfly) of two DP4As per lane.  The
-                    // patterns inside the window of the final minimum are then scored from y in
-                    // fp32 with the same bytes (8 positions per lane, butterfly sum).
+                    // Per hit group (32 patterns): lane j holds pattern j of the group (its NW
+                    // words, one row-major load) and computes the exact integer score
+                    // Q_j = sum_i q_i P[j, i] from the bit planes of the row's int8 image:
+                    // Q_j = sum_{b < 7} 2^b popc(P_j & plane_b) - 128 popc(P_j & plane_7)
+                    // (two's complement), planes read by broadcast from shared memory; no
+                    // cross-lane reduction.  The patterns inside the window of the final minimum
+                    // are then scored from y in fp32 (8 positions per lane, butterfly sum).
+                    unsigned char* const pl = planes + (warp - WORK_W0) * 256;
+                    bool planes_ready = false;
                     auto load_group = [&](int grp, uint4& t0, uint4& t1) {
                         t0 = make_uint4(0u, 0u, 0u, 0u);
                         t1 = t0;
-                        if (pos_on) {
-                            const uint4* s4 = prm.pbT + ((size_t)grp * (NW * 4) + lane) * 2;
+                        const int pc = grp * 32 + lane;
+                        if (pc < np_) {
+                            const uint4* s4 = reinterpret_cast<const uint4*>(prm.pbits + (size_t)pc * NW);
                             t0 = __ldg(s4);
-                            t1 = __ldg(s4 + 1);
+                            if (NW > 4) t1 = __ldg(s4 + 1);
                         }
                     };
                     auto do_group = [&](int grp, const uint4& t0, const uint4& t1) {
-                        const uint32_t tb[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
-                        // this lane's share of Q_j, eight patterns at a time in a rolled loop (the
-                        // streaming loop of the scan warps shares the instruction caches with this
-                        // code): a nibble's bits -> 0/1 bytes by one multiplication (bit k lands on
-                        // bits k, k + 7, k + 14, k + 21; the four copies of a nibble do not overlap,
-                        // those of a whole byte would)
-                        unsigned cm = 0u;
-                        uint32_t rb[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
-#pragma unroll 1
-                        for (int c8 = 0; c8 < 4; c8++) {
-                            int v[8];
+                        if (!planes_ready) {
+                            // plane b, byte `lane` = bit b of this lane's 8 values (positions 8 lane ..)
 #pragma unroll
-                            for (int j = 0; j < 8; j++) {
-                                const uint32_t byte = (rb[j >> 2] >> (8 * (j & 3))) & 0xFFu;
-                                const uint32_t lo = ((byte & 0xFu) * 0x00204081u) & 0x01010101u;
-                                const uint32_t hi = ((byte >> 4) * 0x00204081u) & 0x01010101u;
-                                v[j] = __dp4a((int)q2.y, (int)hi, __dp4a((int)q2.x, (int)lo, 0));
+                            for (int b = 0; b < 8; b++) {
+                                const uint32_t lo4 = (((q2.x >> b) & 0x01010101u) * 0x01020408u) >> 24;
+                                const uint32_t hi4 = (((q2.y >> b) & 0x01010101u) * 0x01020408u) >> 24;
+                                pl[b * 32 + lane] = (unsigned char)(lo4 | (hi4 << 4));
                             }
-#pragma unroll
-                            for (int j = 0; j < 6; j++) rb[j] = rb[j + 2];
-                            // transposing butterfly over lane bits 2..0, then plain sums over bits 3, 4:
-                            // every lane with (lane & 7) = j holds the warp sum of v[j] (exact integers)
-#pragma unroll
-                            for (int o = 4; o > 0; o >>= 1) {
-                                const bool up = (lane & o) != 0;
-#pragma unroll
-                                for (int i = 0; i < o; i++) {
-                                    const int send = up ? v[i] : v[i + o];
-                                    const int keep = up ? v[i + o] : v[i];
-                                    v[i] = keep + __shfl_xor_sync(MPW_FULL, send, o);
-                                }
-                            }
-                            int Q = v[0];
-                            Q += __shfl_xor_sync(MPW_FULL, Q, 8);
-                            Q += __shfl_xor_sync(MPW_FULL, Q, 16);
-                            const unsigned b8 = __ballot_sync(MPW_FULL, lane < 8 && grp * 32 + c8 * 8 + lane < np_ && Q < limit);
-                            cm |= b8 << (8 * c8);
+                            __syncwarp();
+                            planes_ready = true;
                         }
+                        int Q = 0;
+#pragma unroll 1
+                        for (int b = 0; b < 8; b++) {
+                            const uint4 a0 = *reinterpret_cast<const uint4*>(pl + b * 32);
+                            int c = __popc(t0.x & a0.x) + __popc(t0.y & a0.y) + __popc(t0.z & a0.z) + __popc(t0.w & a0.w);
+                            if (NW > 4) {
+                                const uint4 a1 = *reinterpret_cast<const uint4*>(pl + b * 32 + 16);
+                                c += __popc(t1.x & a1.x) + __popc(t1.y & a1.y) + __popc(t1.z & a1.z) + __popc(t1.w & a1.w);
+                            }
+                            Q += (b == 7 ? -c : c) << b;
+                        }
+                        unsigned cm = __ballot_sync(MPW_FULL, grp * 32 + lane < np_ && Q < limit);
                         if (STATS) st_chunks++;
                         if (cm && !tv_ready) {
                             const float yv[8] = {ya.x, ya.y, ya.z, ya.w, yb.x, yb.y, yb.z, yb.w};
@@ -612,7 +602,8 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
                             const int j = __ffs(cm) - 1;
                             cm &= cm - 1;
                             const int pc = grp * 32 + j;
-                            const uint32_t byte = (select_word<8>(tb, j >> 2) >> (8 * (j & 3))) & 0xFFu;
+                            const uint32_t byte =
+                                pos_on ? (uint32_t)__ldg(reinterpret_cast<const unsigned char*>(prm.pbits) + (size_t)pc * (NW * 4) + lane) : 0u;
                             float sp = 0.f;
 #pragma unroll
                             for (int k = 0; k < 8; k++)

@@ -33,8 +33,6 @@ bool tc_i8_supported(int n, int np) { return (n == 128 || n == 256) && np >= 1; 
 void tc_release(TcPatterns& t) {
     if (t.tiles) cudaFree(t.tiles);
     if (t.tiles8) cudaFree(t.tiles8);
-    if (t.pbT) cudaFree(t.pbT);
-    t.pbT = nullptr;
     if (t.ar_stat) cudaFree(t.ar_stat);
     t.ar_stat = nullptr;
     t.tiles = nullptr;
@@ -74,14 +72,6 @@ static int tc_build8(TcPatterns& t, const uint32_t* bits, int np, int n, int nw)
     t.kb8 = kb;
     t.ntiles8 = ntiles;
     t.ready8 = true;
-    // the workers' view: group g of 32 patterns, position byte b (positions 8 b .. 8 b + 7), pattern j -> one byte
-    const int ngrp = (np + 31) / 32, nb = n / 8;
-    std::vector<uint8_t> tr((size_t)ngrp * nb * 32, 0);
-    for (int p = 0; p < np; p++)
-        for (int b = 0; b < nb; b++)
-            tr[((size_t)(p / 32) * nb + b) * 32 + (p % 32)] = (uint8_t)((bits[(size_t)p * nw + (b >> 2)] >> (8 * (b & 3))) & 0xFFu);
-    if (cudaMalloc(&t.pbT, tr.size()) != cudaSuccess) return -1;
-    if (cudaMemcpy(t.pbT, tr.data(), tr.size(), cudaMemcpyHostToDevice) != cudaSuccess) return -1;
     if (cudaMalloc(&t.ar_stat, 2 * sizeof(unsigned long long)) != cudaSuccess) return -1;
     if (cudaMemset(t.ar_stat, 0, 2 * sizeof(unsigned long long)) != cudaSuccess) return -1;
     return 0;

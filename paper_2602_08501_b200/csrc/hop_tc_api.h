@@ -14,8 +14,6 @@ struct TcPatterns {
     bool ready8 = false;
     uint8_t* tiles8 = nullptr;
     int kb8 = 0, ntiles8 = 0;   // int8 tiles are tc::I8_TILE patterns wide
-    // asynchronous-row hop, worker view of P: bits transposed [group of 32 patterns][n / 8 position bytes][32 patterns]
-    uint4* pbT = nullptr;
     // asynchronous-row hop, launch statistics accumulated by the kernel: [0] tiles, [1] clock cycles of the
     // first MMA issuer thread, summed over CTAs (read by mpw_hop_tile_stats)
     unsigned long long* ar_stat = nullptr;

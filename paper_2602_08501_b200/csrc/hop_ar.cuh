@@ -92,7 +92,8 @@ struct Params {
     unsigned long long* tilestat;   // optional (any build): [0] += tiles, [1] += clock64 cycles of issuer 0, per CTA
     int experiment;              // STATS builds, timing probes (results wrong): 2 workers decide "no move" without
                                  // scoring, 4 the producer stops copying once the ring is full, 8 scan skips the TMEM loads,
-                                 // 16 workers skip the proxy fence
+                                 // 16 workers skip the proxy fence, 64 workers skip the fp32 scoring of the window patterns,
+                                 // 128 workers skip the bit-plane filter
 };
 
 __host__ __device__ constexpr size_t smem_bytes(int kb) {
@@ -580,7 +581,7 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
                         }
                         int Q = 0;
 #pragma unroll 1
-                        for (int b = 0; b < 8; b++) {
+                        for (int b = (STATS && (prm.experiment & 128)) ? 8 : 0; b < 8; b++) {   // (128: timing probe without the filter)
                             const uint4 a0 = *reinterpret_cast<const uint4*>(pl + b * 32);
                             int c = __popc(t0.x & a0.x) + __popc(t0.y & a0.y) + __popc(t0.z & a0.z) + __popc(t0.w & a0.w);
                             if (NW > 4) {
@@ -590,6 +591,7 @@ __global__ void __launch_bounds__(THREADS, 1) hop_ar_kernel(Params prm) {
                             Q += (b == 7 ? -c : c) << b;
                         }
                         unsigned cm = __ballot_sync(MPW_FULL, grp * 32 + lane < np_ && Q < limit);
+                        if (STATS && (prm.experiment & 64)) cm = 0u;          // timing probe: filter only
                         if (STATS) st_chunks++;
                         if (cm && !tv_ready) {
                             const float yv[8] = {ya.x, ya.y, ya.z, ya.w, yb.x, yb.y, yb.z, yb.w};

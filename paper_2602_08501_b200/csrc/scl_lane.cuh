@@ -127,6 +127,37 @@ __device__ __forceinline__ void lane_node_d2(bool is_g, int n2, const double* __
                                              const uint32_t* __restrict__ psrow, double* __restrict__ o,
                                              int lo) {
     constexpr int HALF = N / 8;
+    if constexpr (N == 256) {
+        // N = 256: element j of this node reads positions j + 32 k (k = 0..7) of llr0, and every
+        // partial-sum bit it needs is bit j of one word: the words are read once, a sign flip is
+        // an XOR of the sign bit (-a and a differ in nothing else), the f / g choices are
+        // warp-uniform.  Same IEEE operations on the same operands as lv1 / lv2 above.
+        const int n1 = n2 >> 1;
+        const bool g1 = n1 != 0, g2 = (n2 & 1) != 0;
+        uint32_t w1[4] = {0u, 0u, 0u, 0u}, w2[2] = {0u, 0u}, w3 = 0u;
+        if (g1) {
+#pragma unroll
+            for (int k = 0; k < 4; k++) w1[k] = psrow[k];             // left half's level-1 bits
+        }
+        if (g2) { w2[0] = psrow[n1 * 4]; w2[1] = psrow[n1 * 4 + 1]; }   // left sibling's level-2 bits
+        if (is_g) w3 = psrow[lo >> 5];                                // left sibling's level-3 bits
+        auto flip = [](double a, uint32_t w, int j) {
+            return __hiloint2double(__double2hiint(a) ^ (int)(((w >> j) & 1u) << 31), __double2loint(a));
+        };
+#pragma unroll 1
+        for (int j = 0; j < HALF; j++) {
+            double x[8];
+#pragma unroll
+            for (int k = 0; k < 8; k++) x[k] = llr0[j + 32 * k];
+            double v1[4];
+#pragma unroll
+            for (int k = 0; k < 4; k++) v1[k] = g1 ? x[k + 4] + flip(x[k], w1[k], j) : scl_f(x[k], x[k + 4]);
+            const double a = g2 ? v1[2] + flip(v1[0], w2[0], j) : scl_f(v1[0], v1[2]);
+            const double c = g2 ? v1[3] + flip(v1[1], w2[1], j) : scl_f(v1[1], v1[3]);
+            o[j] = is_g ? c + flip(a, w3, j) : scl_f(a, c);
+        }
+        return;
+    }
     const uint32_t word = (HALF >= 32) ? 0u : (psrow[lo >> 5] >> (lo & 31));
     constexpr int DU = MPW_SCL_D2_UNROLL;
 #pragma unroll (DU)

@@ -536,13 +536,9 @@ __global__ void __launch_bounds__(128, 4) scl_lane_kernel(CodeDev code, const fl
 #pragma unroll
                 for (int w = 0; w < Lay::PTRW; w++) rp[w] = sp[w];
                 __syncwarp();
-                if (bit) {
-#pragma unroll
-                    for (int w = 0; w < NW; w++)
-                        if (w == (phi >> 5)) rps[w] |= 1u << (phi & 31);
-                }
 #pragma unroll
                 for (int w = 0; w < NW; w++) psrow[w] = rps[w];
+                if (bit) psrow[phi >> 5] |= 1u << (phi & 31);     // the leaf's decision (one word, addressed)
                 uint32_t* mp = reinterpret_cast<uint32_t*>(ptrrow);
 #pragma unroll
                 for (int w = 0; w < Lay::PTRW; w++) mp[w] = rp[w];
